@@ -1,0 +1,1084 @@
+// optimus_oracle.cpp — CPU ORACLE FOR THE OPTIMUS BUBBLE-SCHEDULING SEARCH.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load this library.  It
+// shares no code, header, table or helper with the CUDA path
+// (paper_2408_03505_b200/), and the CUDA path never calls it.
+//
+// It is the plain, slow, literal per-candidate form of the paper's method:
+//   Alg. 1 "Optimus workflow"
+//   Alg. 2 "BubbleScheduler"           P:320-355 (OptimizeSchedule P:344-354)
+//   §4.1 model planner
+//   §4.2 bubble scheduling
+//   §4.3 encoder-LLM dependency
+//   §4.4 multi-branch encoders
+//   §4.5 memory analysis
+// under the readings R1-R22 of SURVEY.md §8(c), restated in DESIGN.md §3.
+// Every candidate gets fresh per-device state, chains are placed kernel by
+// kernel by first-fit on explicit interval lists, dependency checks sort the
+// EF lists, and the minimal shift is found by binary search on its definition.
+// It does NOT use the per-row factorisation (R-FACT) the GPU uses.
+//
+// Parity status: a1 plans/prune, a2 compositions, a3 template (closed forms,
+// Fig. 9 property), a4 GPipe fill, a5 first fit (brute force), the min-shift
+// Δ (closed form), a7 ordering (Fig. 10) and the p=v=t=P=T=1 special case are
+// pinned by tests/test_oracle_pins.py.  The greedy trajectory as a whole
+// (which pipeline is critical when dependencies dominate, where the loop
+// stops) is pinned only by invariants + the independent Python twin
+// (oracle/twin.py) + the SURVEY Appendix C regression values: "parity
+// unpinned beyond invariants" for that part, as DESIGN.md says.
+//
+// All times are int64 nanoseconds (R1).  No floating point anywhere.
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+using i64 = int64_t;
+using u64 = uint64_t;
+const i64 INF = INT64_MAX / 4;
+
+struct Kern {
+  int kind;  // 0 = compute, 1 = TP communication (R3)
+  i64 ns;
+};
+using KList = std::vector<Kern>;
+
+struct Branch {
+  i64 layers, params;
+  std::vector<KList> fwd, bwd;  // per TP option
+};
+
+struct Problem {
+  i64 n_gpu, gpu_mem, reserve, k;
+  i64 dp, pp, tp, v, llm_layers, n_mb, warmup_policy;
+  i64 T_ag, T_rs, pp_p2p, enc_p2p, enc_llm_p2p;
+  i64 llm_params;
+  std::vector<i64> tp_opts;
+  KList llm_fwd, llm_bwd;
+  std::vector<Branch> branches;
+};
+
+// ------------------------------------------------------------------ parsing
+struct Reader {
+  const int64_t* b;
+  i64 n, i = 0;
+  bool bad = false;
+  i64 get() {
+    if (i >= n) { bad = true; return 0; }
+    return b[i++];
+  }
+  KList list() {
+    i64 len = get();
+    KList out;
+    if (len < 0 || len > 1000000) { bad = true; return out; }
+    for (i64 q = 0; q < len; ++q) {
+      Kern kk;
+      kk.kind = (int)get();
+      kk.ns = get();
+      out.push_back(kk);
+    }
+    return out;
+  }
+};
+
+bool parse(const int64_t* blob, i64 len, Problem& P) {
+  Reader r{blob, len};
+  if (r.get() != 0x4F50544D) return false;  // "OPTM"
+  if (r.get() != 1) return false;
+  P.n_gpu = r.get(); P.gpu_mem = r.get(); P.reserve = r.get(); P.k = r.get();
+  P.dp = r.get(); P.pp = r.get(); P.tp = r.get(); P.v = r.get();
+  P.llm_layers = r.get(); P.n_mb = r.get(); P.warmup_policy = r.get();
+  P.T_ag = r.get(); P.T_rs = r.get(); P.pp_p2p = r.get(); P.enc_p2p = r.get();
+  P.enc_llm_p2p = r.get(); P.llm_params = r.get();
+  i64 nt = r.get();
+  for (i64 q = 0; q < nt && !r.bad; ++q) P.tp_opts.push_back(r.get());
+  P.llm_fwd = r.list();
+  P.llm_bwd = r.list();
+  i64 nb = r.get();
+  for (i64 q = 0; q < nb && !r.bad; ++q) {
+    Branch b;
+    b.layers = r.get();
+    b.params = r.get();
+    for (i64 t = 0; t < nt; ++t) {
+      b.fwd.push_back(r.list());
+      b.bwd.push_back(r.list());
+    }
+    P.branches.push_back(b);
+  }
+  if (r.bad) return false;
+  // minimal sanity (the C-ABI library does full validation)
+  if (P.pp < 1 || P.tp < 1 || P.v < 1 || P.n_mb < 1) return false;
+  if (P.llm_layers % (P.pp * P.v) != 0) return false;
+  if (P.n_mb % P.pp != 0) return false;
+  return true;
+}
+
+// ------------------------------------------------- LLM template (R2-R6)
+// One pipeline op: forward or backward of model chunk `chunk` for microbatch
+// `mb` on one stage.
+struct OpId {
+  int fwd, chunk, mb;
+};
+
+// Megatron interleaved order (R2, Megatron-LM [narayanan2021]):
+// virtual id k -> forward chunk floor((k mod pv)/p), backward chunk v-1-that,
+// microbatch floor(k/(pv))*p + (k mod p).
+OpId virt(const Problem& P, int k, bool fwd) {
+  int p = (int)P.pp, v = (int)P.v;
+  int ch = (k % (p * v)) / p;
+  int mb = (k / (p * v)) * p + (k % p);
+  return OpId{fwd ? 1 : 0, fwd ? ch : v - 1 - ch, mb};
+}
+
+// Per-stage op order: W forwards, then (F, B) pairs, then the remaining B.
+std::vector<OpId> stage_order(const Problem& P, int W) {
+  int nv = (int)(P.n_mb * P.v);
+  std::vector<OpId> o;
+  for (int k = 0; k < W; ++k) o.push_back(virt(P, k, true));
+  for (int i = 0; i < nv - W; ++i) {
+    o.push_back(virt(P, W + i, true));
+    o.push_back(virt(P, i, false));
+  }
+  for (int i = nv - W; i < nv; ++i)
+    if (i >= 0) o.push_back(virt(P, i, false));
+  return o;
+}
+
+// Megatron default warm-up counts (R2).
+std::vector<int> default_warmup(const Problem& P) {
+  int p = (int)P.pp, v = (int)P.v, n = (int)P.n_mb;
+  std::vector<int> W(p);
+  for (int s = 0; s < p; ++s) {
+    if (v == 1) W[s] = std::min(n, p - 1 - s);
+    else if (n == p) W[s] = n * v;
+    else W[s] = std::min(n * v, 2 * (p - 1 - s) + (v - 1) * p);
+  }
+  return W;
+}
+
+i64 list_sum(const KList& l) {
+  i64 s = 0;
+  for (auto& k : l) s += k.ns;
+  return s;
+}
+
+struct Sim {
+  bool ok = false;
+  std::vector<std::vector<OpId>> order;
+  std::vector<std::vector<i64>> start, end;
+  i64 span = 0;                   // max last-op end (LLM span)
+  std::vector<i64> last_end;      // per stage
+};
+
+// ASAP list schedule in the fixed per-stage order (R2, R3).
+Sim simulate(const Problem& P, const std::vector<int>& W) {
+  int p = (int)P.pp, v = (int)P.v, n = (int)P.n_mb;
+  i64 lc = P.llm_layers / (P.pp * P.v);
+  i64 dur_f = lc * list_sum(P.llm_fwd), dur_b = lc * list_sum(P.llm_bwd);
+  Sim S;
+  S.order.resize(p);
+  S.start.resize(p);
+  S.end.resize(p);
+  for (int s = 0; s < p; ++s) {
+    S.order[s] = stage_order(P, W[s]);
+    S.start[s].assign(S.order[s].size(), -1);
+    S.end[s].assign(S.order[s].size(), -1);
+  }
+  // done[s][fwd][chunk][mb] = end time or -1
+  std::vector<i64> done((size_t)p * 2 * v * n, -1);
+  auto D = [&](int s, int f, int c, int i) -> i64& { return done[(((size_t)s * 2 + f) * v + c) * n + i]; };
+  std::vector<size_t> pos(p, 0);
+  std::vector<i64> free_at(p, 0);
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int s = 0; s < p; ++s) {
+      while (pos[s] < S.order[s].size()) {
+        OpId op = S.order[s][pos[s]];
+        int ds = -1, df = 0, dc = 0;  // dependency op (R2)
+        if (op.fwd) {
+          if (s > 0) { ds = s - 1; df = 1; dc = op.chunk; }
+          else if (op.chunk > 0) { ds = p - 1; df = 1; dc = op.chunk - 1; }
+        } else {
+          if (s < p - 1) { ds = s + 1; df = 0; dc = op.chunk; }
+          else if (op.chunk < v - 1) { ds = 0; df = 0; dc = op.chunk + 1; }
+          else { ds = p - 1; df = 1; dc = v - 1; }
+        }
+        i64 t = std::max(free_at[s], P.T_ag);  // all ops start >= T_ag (R3)
+        if (ds >= 0) {
+          i64 e = D(ds, df, dc, op.mb);
+          if (e < 0) break;  // dependency not finished yet
+          t = std::max(t, e + (ds != s ? P.pp_p2p : 0));
+        }
+        i64 d = op.fwd ? dur_f : dur_b;
+        S.start[s][pos[s]] = t;
+        S.end[s][pos[s]] = t + d;
+        D(s, op.fwd, op.chunk, op.mb) = t + d;
+        free_at[s] = t + d;
+        ++pos[s];
+        changed = true;
+      }
+    }
+  }
+  S.ok = true;
+  for (int s = 0; s < p; ++s)
+    if (pos[s] != S.order[s].size()) S.ok = false;
+  S.last_end = free_at;
+  S.span = 0;
+  for (int s = 0; s < p; ++s) S.span = std::max(S.span, free_at[s]);
+  return S;
+}
+
+struct Interval {
+  i64 lo, hi;  // lo = fill pointer (initially the interval start), hi = end
+};
+
+struct Template {
+  std::vector<int> Wdef, W;
+  i64 span_def = 0, span = 0, T_end = 0;
+  std::vector<i64> F, B;           // dependency points (R4)
+  std::vector<i64> w, z;           // first / last LLM compute instant per stage
+  std::vector<std::vector<Interval>> comp_free, comm_free;  // per stage (R6)
+  // raw kernel timeline (for trace / invariant checks)
+  std::vector<std::vector<std::pair<i64, i64>>> comp_k, comm_k;
+  bool ok = false;
+};
+
+// GetEncLLMDep with the warm-up adjustment (R5).
+Template build_template(const Problem& P) {
+  Template T;
+  int p = (int)P.pp, n = (int)P.n_mb;
+  T.Wdef = default_warmup(P);
+  Sim def = simulate(P, T.Wdef);
+  if (!def.ok) return T;
+  T.span_def = def.span;
+  T.W = T.Wdef;
+  if (P.warmup_policy == 1) {
+    // reverse-stage greedy: smallest w keeping deadlock-freedom and the span
+    for (int s = p - 1; s >= 0; --s) {
+      for (int w = 0; w <= T.Wdef[s]; ++w) {
+        std::vector<int> Wt = T.W;
+        Wt[s] = w;
+        Sim t = simulate(P, Wt);
+        if (t.ok && t.span == T.span_def) { T.W[s] = w; break; }
+      }
+    }
+  }
+  Sim S = simulate(P, T.W);
+  if (!S.ok) return T;
+  T.span = S.span;
+  T.T_end = 0;
+  for (int s = 0; s < p; ++s) T.T_end = std::max(T.T_end, S.last_end[s] + P.T_rs);
+  T.F.assign(n, -1);
+  T.B.assign(n, -1);
+  for (size_t q = 0; q < S.order[0].size(); ++q) {
+    OpId op = S.order[0][q];
+    if (op.chunk != 0) continue;
+    if (op.fwd) T.F[op.mb] = S.start[0][q];   // F_i = start of F(0,0,i)
+    else T.B[op.mb] = S.end[0][q];            // B_i = end of B(0,0,i)
+  }
+  // kernel timelines and free intervals (R3, R6)
+  i64 lc = P.llm_layers / (P.pp * P.v);
+  T.w.assign(p, 0);
+  T.z.assign(p, 0);
+  T.comp_free.resize(p);
+  T.comm_free.resize(p);
+  T.comp_k.resize(p);
+  T.comm_k.resize(p);
+  for (int s = 0; s < p; ++s) {
+    std::vector<std::pair<i64, i64>> comp, comm;
+    for (size_t q = 0; q < S.order[s].size(); ++q) {
+      const KList& L = S.order[s][q].fwd ? P.llm_fwd : P.llm_bwd;
+      i64 t = S.start[s][q];
+      for (i64 rep = 0; rep < lc; ++rep)
+        for (auto& k : L) {
+          if (k.kind == 0) comp.push_back({t, t + k.ns});
+          else comm.push_back({t, t + k.ns});
+          t += k.ns;
+        }
+    }
+    T.comp_k[s] = comp;
+    T.comm_k[s] = comm;
+    if (comp.empty()) return T;
+    // maximal busy runs of LLM compute
+    std::vector<std::pair<i64, i64>> runs;
+    for (auto& c : comp) {
+      if (!runs.empty() && c.first <= runs.back().second) runs.back().second = std::max(runs.back().second, c.second);
+      else runs.push_back(c);
+    }
+    T.w[s] = runs.front().first;
+    T.z[s] = runs.back().second;
+    // compute-free intervals: gaps between LLM compute (TP + PP bubbles)
+    for (size_t r = 0; r + 1 < runs.size(); ++r)
+      if (runs[r + 1].first > runs[r].second) T.comp_free[s].push_back({runs[r].second, runs[r + 1].first});
+    // comm-free intervals: [w, z] minus LLM comm kernels
+    i64 cur = T.w[s];
+    for (auto& c : comm) {
+      if (cur >= T.z[s]) break;
+      if (c.first > cur) T.comm_free[s].push_back({cur, std::min(c.first, T.z[s])});
+      cur = std::max(cur, c.second);
+    }
+    if (cur < T.z[s]) T.comm_free[s].push_back({cur, T.z[s]});
+  }
+  T.ok = true;
+  return T;
+}
+
+// ------------------------------------------------------ model planner (a1)
+struct Plan {
+  i64 P, T, dp_enc, m, r_p, r_t;
+  bool kept;
+  u64 count;  // compositions C(n-1, m-1), 0 if m > n or pruned
+  u64 first;  // global index of its first candidate
+};
+
+u64 binom(i64 a, i64 b) {  // exact for the sizes used; saturates
+  if (b < 0 || b > a) return 0;
+  b = std::min(b, a - b);
+  unsigned __int128 r = 1;
+  for (i64 i = 1; i <= b; ++i) {
+    r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+    if (r > (unsigned __int128)UINT64_MAX) return UINT64_MAX;
+  }
+  return (u64)r;
+}
+
+std::vector<Plan> plans(const Problem& P) {
+  std::vector<Plan> out;
+  i64 dp_llm = P.n_gpu / (P.pp * P.tp);
+  i64 phi_enc = 0;
+  for (auto& b : P.branches) phi_enc += b.params;
+  u64 first = 0;
+  for (i64 Pe = 1; Pe <= P.pp; ++Pe) {
+    if (P.pp % Pe) continue;  // PP_enc | PP_llm
+    for (i64 Te : P.tp_opts) {
+      if (P.tp % Te) continue;  // TP_enc | TP_llm
+      Plan pl;
+      pl.P = Pe;
+      pl.T = Te;
+      pl.dp_enc = P.n_gpu / (Pe * Te);
+      pl.r_p = P.pp / Pe;
+      pl.r_t = P.tp / Te;
+      pl.m = pl.r_p * pl.r_t;  // m = DP_enc / DP_llm
+      // §4.5: MEM_model = k (DP_enc phi_enc + DP_llm phi_llm) / n_gpu; keep iff
+      // MEM_model + reserve <= capacity, multiplied through by n_gpu (R19)
+      __int128 lhs = (__int128)P.k * ((__int128)pl.dp_enc * phi_enc + (__int128)dp_llm * P.llm_params) +
+                     (__int128)P.reserve * P.n_gpu;
+      __int128 rhs = (__int128)P.gpu_mem * P.n_gpu;
+      pl.kept = lhs <= rhs;
+      pl.count = (pl.kept && pl.m <= P.n_mb) ? binom(P.n_mb - 1, pl.m - 1) : 0;
+      pl.first = first;
+      first += pl.count;
+      out.push_back(pl);
+    }
+  }
+  return out;
+}
+
+// Lexicographic unranking of a composition of n into m positive parts (R17):
+// count the compositions that start with each smaller first part.
+std::vector<int> unrank(i64 n, i64 m, u64 rank) {
+  std::vector<int> N;
+  i64 rem = n;
+  for (i64 j = 0; j < m - 1; ++j) {
+    i64 parts_left = m - j;
+    for (i64 x = 1; x <= rem - (parts_left - 1); ++x) {
+      u64 cnt = binom(rem - x - 1, parts_left - 2);  // compositions of rem-x into parts_left-1
+      if (rank < cnt) { N.push_back((int)x); rem -= x; break; }
+      rank -= cnt;
+    }
+  }
+  N.push_back((int)rem);
+  return N;
+}
+
+// ---------------------------------------- encoder stage kernel lists (R8)
+struct StageLists {
+  std::vector<KList> fwd;   // per stage, real-time forward order
+  std::vector<KList> bwdm;  // per stage, mirrored-time order of the backward
+  std::vector<i64> tau_f, tau_b;
+};
+
+StageLists stage_lists(const Problem& P, const Plan& pl) {
+  StageLists SL;
+  size_t ti = 0;
+  while (P.tp_opts[ti] != pl.T) ++ti;
+  for (i64 s = 0; s < pl.P; ++s) {
+    KList f, breal;
+    std::vector<std::pair<size_t, i64>> layers;  // (branch, layer) in forward order
+    for (size_t b = 0; b < P.branches.size(); ++b) {
+      i64 L = P.branches[b].layers;
+      for (i64 l = s * L / pl.P; l < (s + 1) * L / pl.P; ++l) layers.push_back({b, l});
+    }
+    for (auto& bl : layers)
+      for (auto& k : P.branches[bl.first].fwd[ti]) f.push_back(k);
+    // real-time backward: layers in reverse, each layer's backward list
+    for (size_t q = layers.size(); q-- > 0;)
+      for (auto& k : P.branches[layers[q].first].bwd[ti]) breal.push_back(k);
+    KList bm(breal.rbegin(), breal.rend());  // mirrored time reverses it (R15)
+    SL.fwd.push_back(f);
+    SL.bwdm.push_back(bm);
+    SL.tau_f.push_back(list_sum(f));
+    SL.tau_b.push_back(list_sum(breal));
+  }
+  return SL;
+}
+
+// Coarse GPipe fill from absolute 0 (R9): end(s,x) = max(end(s,x-1),
+// end(s-1,x) + enc_p2p) + tau[s];  returns table [s][x], x = 0..c.
+std::vector<std::vector<i64>> gpipe(const std::vector<i64>& tau, i64 p2p, i64 c) {
+  size_t Pn = tau.size();
+  std::vector<std::vector<i64>> e(Pn, std::vector<i64>(c + 1, 0));
+  for (i64 x = 1; x <= c; ++x)
+    for (size_t s = 0; s < Pn; ++s) {
+      i64 st = e[s][x - 1];
+      if (s > 0) st = std::max(st, e[s - 1][x] + p2p);
+      e[s][x] = st + tau[s];
+    }
+  return e;
+}
+
+// ------------------------------------------- the minimal shift (R10, R15)
+// min Delta >= 0 such that sortasc({x - Delta : x in pre} U fixed)[i] <= dl[i]
+// for all i (dl given in slot order); INF if no Delta works.  Found by
+// binary search on the definition (feasibility is monotone in Delta).
+bool feasible(const std::vector<i64>& pre, const std::vector<i64>& fixed, const std::vector<i64>& dl, i64 d) {
+  std::vector<i64> vals;
+  for (i64 x : pre) vals.push_back(x - d);
+  for (i64 x : fixed) vals.push_back(x);
+  std::sort(vals.begin(), vals.end());
+  for (size_t i = 0; i < vals.size(); ++i)
+    if (vals[i] > dl[i]) return false;
+  return true;
+}
+
+i64 min_shift(const std::vector<i64>& pre, const std::vector<i64>& fixed, const std::vector<i64>& dl) {
+  i64 hi = 0;
+  if (!pre.empty()) {
+    i64 mx = *std::max_element(pre.begin(), pre.end());
+    i64 mn = *std::min_element(dl.begin(), dl.end());
+    hi = std::max<i64>(0, mx - mn);  // beyond hi every pre value is below every deadline
+  }
+  if (!feasible(pre, fixed, dl, hi)) return INF;
+  i64 lo = 0;
+  while (lo < hi) {
+    i64 mid = lo + (hi - lo) / 2;
+    if (feasible(pre, fixed, dl, mid)) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------ global ordering (R14)
+// checkEncLLMDep's global ordering: sort every encoder forward finish
+// ascending (ties by pipeline, then local index); position i is LLM
+// microbatch i.  Returns S_j = the positions designated to pipeline j.
+struct OrdE {
+  i64 v;
+  int j, local;
+};
+std::vector<std::vector<int>> global_order(std::vector<OrdE>& ent, int m) {
+  std::sort(ent.begin(), ent.end(), [](const OrdE& a, const OrdE& b) {
+    if (a.v != b.v) return a.v < b.v;
+    if (a.j != b.j) return a.j < b.j;
+    return a.local < b.local;
+  });
+  std::vector<std::vector<int>> S(m);
+  for (size_t i = 0; i < ent.size(); ++i) S[ent[i].j].push_back((int)i);
+  return S;
+}
+
+// ------------------------------------- kernel-level first fit (R12)
+struct Inst {
+  std::vector<Interval> res[2];  // [0] compute-free, [1] comm-free
+};
+struct Undo {
+  Interval* iv;
+  i64 lo;
+};
+
+// Place one microbatch as a chain over stages 0..P-1 (ScheduleKernels,
+// P:347).  inst[s] is the device instance of stage s; wst[s] the
+// earliest LLM compute instant of its LLM stage.  Returns false (state
+// restored by the caller through `undo`) when some kernel finds no interval.
+bool place_chain(std::vector<Inst*>& inst, const std::vector<KList>& lists, const std::vector<i64>& wst, i64 p2p,
+                 i64& EF, std::vector<Undo>& undo, std::vector<std::vector<i64>>* rec) {
+  i64 ready = 0, prev_end = 0;
+  for (size_t s = 0; s < lists.size(); ++s) {
+    ready = (s == 0) ? wst[0] : std::max(prev_end + p2p, wst[s]);
+    for (auto& k : lists[s]) {
+      std::vector<Interval>& ivs = inst[s]->res[k.kind];
+      // the first interval whose end is after `ready`
+      auto it = std::partition_point(ivs.begin(), ivs.end(), [&](const Interval& iv) { return iv.hi <= ready; });
+      bool placed = false;
+      for (; it != ivs.end(); ++it) {
+        i64 x = std::max(ready, it->lo);
+        if (x + k.ns <= it->hi) {
+          undo.push_back({&*it, it->lo});
+          it->lo = x + k.ns;
+          if (rec) rec->push_back({(i64)s, (i64)k.kind, x, x + k.ns});
+          ready = x + k.ns;
+          placed = true;
+          break;
+        }
+      }
+      if (!placed) return false;
+    }
+    prev_end = ready;
+  }
+  EF = ready;
+  return true;
+}
+
+// -------------------------------------------------- one candidate (Alg. 2)
+struct Result {
+  i64 lat = 0, df = 0, db = 0;
+  int mf = 0, mb = 0;
+};
+
+struct Ctx {
+  Problem P;
+  Template T;
+  std::vector<Plan> PL;
+  u64 total = 0;
+  std::vector<StageLists> SL;                      // per plan
+  std::vector<std::vector<std::vector<i64>>> preF, preB;  // per plan GPipe tables
+};
+
+struct Trace {
+  std::string s;
+  void add(const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+};
+void Trace::add(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  s += buf;
+}
+
+// Evaluate one candidate literally.  If tr != nullptr, emit a JSON trace of
+// every placement (real time) for the invariant suite.
+Result eval_candidate(const Ctx& C, size_t e, const std::vector<int>& N, Trace* tr) {
+  const Problem& P = C.P;
+  const Template& T = C.T;
+  const Plan& pl = C.PL[e];
+  const StageLists& SL = C.SL[e];
+  const auto& preF = C.preF[e];
+  const auto& preB = C.preB[e];
+  int m = (int)pl.m, Pn = (int)pl.P, n = (int)P.n_mb;
+  i64 L = P.enc_llm_p2p;
+  auto row = [&](int j) { return j / (int)pl.r_t; };  // a = j div r_t (R7)
+
+  // fresh per-device state: pipeline j, stage s -> LLM stage aP+s, TP slot b
+  std::vector<std::unique_ptr<Inst>> inst((size_t)m * Pn);
+  auto get_inst = [&](int j, int s) -> Inst* {
+    auto& u = inst[(size_t)j * Pn + s];
+    if (!u) {  // private copy of that LLM stage's interval lists (lazy)
+      u.reset(new Inst);
+      int q = row(j) * Pn + s;
+      u->res[0] = T.comp_free[q];
+      u->res[1] = T.comm_free[q];
+    }
+    return u.get();
+  };
+
+  std::vector<std::vector<i64>> recF, recB;  // trace records
+  // ---------------- forward OptimizeSchedule (Alg. 2 line "7") ----------
+  std::vector<int> c(N.begin(), N.end());
+  std::vector<std::vector<i64>> Q(m);
+  std::vector<i64> G(n);
+  for (int i = 0; i < n; ++i) G[i] = T.F[i] - L;  // EF_i + L <= F_i (R20)
+
+  auto dev_f = [&](const std::vector<int>& cc, int* jstar) {
+    i64 best = -INF;
+    int bj = -1;
+    for (int j = 0; j < m; ++j) {
+      if (cc[j] == 0) continue;
+      i64 d = -INF;
+      for (int s = 0; s < Pn; ++s) d = std::max(d, preF[s][cc[j]] - T.w[row(j) * Pn + s]);
+      if (d > best) { best = d; bj = j; }  // ties -> lowest j (R11)
+    }
+    if (jstar) *jstar = bj;
+    return best;
+  };
+  auto dep_f = [&](const std::vector<int>& cc, const std::vector<std::vector<i64>>& QQ) {
+    std::vector<i64> pre, fixed;
+    for (int j = 0; j < m; ++j) {
+      for (int t = 1; t <= cc[j]; ++t) pre.push_back(preF[Pn - 1][t]);  // PRE_EF(t)
+      for (i64 q : QQ[j]) fixed.push_back(q);
+    }
+    return min_shift(pre, fixed, G);
+  };
+
+  Result R;
+  i64 Delta;
+  int moves_f = 0;
+  std::vector<i64> deltas_f;
+  for (;;) {
+    int js;
+    i64 dev = dev_f(c, &js);
+    i64 dep = dep_f(c, Q);
+    Delta = std::max<i64>(0, std::max(dev, dep));
+    deltas_f.push_back(Delta);
+    bool all0 = true;
+    for (int j = 0; j < m; ++j) all0 = all0 && c[j] == 0;
+    if (Delta == 0 || all0) break;
+    // findCritical (R11) -> js; ScheduleKernels (R12) on its instances
+    std::vector<Inst*> ins(Pn);
+    std::vector<i64> wst(Pn);
+    for (int s = 0; s < Pn; ++s) { ins[s] = get_inst(js, s); wst[s] = T.w[row(js) * Pn + s]; }
+    std::vector<Undo> undo;
+    std::vector<std::vector<i64>> rec;
+    i64 EF;
+    bool ok = place_chain(ins, SL.fwd, wst, P.enc_p2p, EF, undo, tr ? &rec : nullptr);
+    bool commit = false;
+    if (ok) {
+      std::vector<int> c2 = c;
+      c2[js] -= 1;
+      auto Q2 = Q;
+      Q2[js].push_back(EF);
+      // checkEncLLMDep on the new schedule in the current timeline (R13)
+      if (dep_f(c2, Q2) <= Delta) { c = c2; Q = Q2; commit = true; }
+    }
+    if (!commit) {
+      for (size_t u = undo.size(); u-- > 0;) undo[u].iv->lo = undo[u].lo;
+      break;
+    }
+    ++moves_f;
+    if (tr) for (auto& r : rec) { auto rr = r; rr.insert(rr.begin(), js); rr.push_back(moves_f - 1); recF.push_back(rr); }
+  }
+  i64 Df = Delta;
+
+  // ---------------- global ordering (R14) ------------------------
+  std::vector<OrdE> ent;
+  for (int j = 0; j < m; ++j) {
+    for (int t = 1; t <= c[j]; ++t) ent.push_back({preF[Pn - 1][t] - Df, j, t - 1});
+    for (size_t k = 0; k < Q[j].size(); ++k) ent.push_back({Q[j][k], j, c[j] + (int)k});
+  }
+  std::vector<std::vector<int>> S = global_order(ent, m);  // S_j (0-based positions)
+
+  // ---------------- backward OptimizeSchedule (Alg. 2 line "8", R15) -----
+  // time-mirrored problem t -> T_end - t, carrying the forward fill pointers
+  std::vector<std::unique_ptr<Inst>> minst((size_t)m * Pn);
+  auto get_minst = [&](int j, int s) -> Inst* {
+    auto& u = minst[(size_t)j * Pn + s];
+    if (!u) {
+      u.reset(new Inst);
+      int q = row(j) * Pn + s;
+      for (int r = 0; r < 2; ++r) {
+        const std::vector<Interval>& src =
+            inst[(size_t)j * Pn + s] ? inst[(size_t)j * Pn + s]->res[r] : (r == 0 ? T.comp_free[q] : T.comm_free[q]);
+        for (size_t x = src.size(); x-- > 0;) {
+          Interval mi{T.T_end - src[x].hi, T.T_end - src[x].lo};
+          if (mi.hi > mi.lo) u->res[r].push_back(mi);
+        }
+      }
+    }
+    return u.get();
+  };
+  std::vector<i64> wm(P.pp);
+  for (int q = 0; q < P.pp; ++q) wm[q] = T.T_end - T.z[q];  // w'_p = T_end - z_p
+  // per-pipeline deadlines D_j = sortasc{T_end - B_i - L : i in S_j}
+  std::vector<std::vector<i64>> Dl(m);
+  for (int j = 0; j < m; ++j) {
+    for (int i : S[j]) Dl[j].push_back(T.T_end - T.B[i] - L);
+    std::sort(Dl[j].begin(), Dl[j].end());
+  }
+  std::vector<int> cb(N.begin(), N.end());
+  std::vector<std::vector<i64>> Qb(m);
+  auto dev_b = [&](const std::vector<int>& cc, int* jstar) {
+    i64 best = -INF;
+    int bj = -1;
+    for (int j = 0; j < m; ++j) {
+      if (cc[j] == 0) continue;
+      i64 d = -INF;
+      for (int s = 0; s < Pn; ++s) d = std::max(d, preB[s][cc[j]] - wm[row(j) * Pn + s]);
+      if (d > best) { best = d; bj = j; }
+    }
+    if (jstar) *jstar = bj;
+    return best;
+  };
+  auto dep_b = [&](const std::vector<int>& cc, const std::vector<std::vector<i64>>& QQ) {
+    i64 d = 0;
+    for (int j = 0; j < m; ++j) {
+      std::vector<i64> pre;
+      for (int t = 1; t <= cc[j]; ++t) pre.push_back(preB[Pn - 1][t]);
+      d = std::max(d, min_shift(pre, QQ[j], Dl[j]));
+    }
+    return d;
+  };
+  int moves_b = 0;
+  std::vector<i64> deltas_b;
+  for (;;) {
+    int js;
+    i64 dev = dev_b(cb, &js);
+    i64 dep = dep_b(cb, Qb);
+    Delta = std::max<i64>(0, std::max(dev, dep));
+    deltas_b.push_back(Delta);
+    bool all0 = true;
+    for (int j = 0; j < m; ++j) all0 = all0 && cb[j] == 0;
+    if (Delta == 0 || all0) break;
+    std::vector<Inst*> ins(Pn);
+    std::vector<i64> wst(Pn);
+    for (int s = 0; s < Pn; ++s) { ins[s] = get_minst(js, s); wst[s] = wm[row(js) * Pn + s]; }
+    std::vector<Undo> undo;
+    std::vector<std::vector<i64>> rec;
+    i64 EF;
+    bool ok = place_chain(ins, SL.bwdm, wst, P.enc_p2p, EF, undo, tr ? &rec : nullptr);
+    bool commit = false;
+    if (ok) {
+      std::vector<int> c2 = cb;
+      c2[js] -= 1;
+      auto Q2 = Qb;
+      Q2[js].push_back(EF);
+      if (dep_b(c2, Q2) <= Delta) { cb = c2; Qb = Q2; commit = true; }
+    }
+    if (!commit) {
+      for (size_t u = undo.size(); u-- > 0;) undo[u].iv->lo = undo[u].lo;
+      break;
+    }
+    ++moves_b;
+    if (tr) for (auto& r : rec) { auto rr = r; rr.insert(rr.begin(), js); rr.push_back(moves_b - 1); recB.push_back(rr); }
+  }
+  i64 Db = Delta;
+  R.lat = T.T_end + Df + Db;  // R16
+  R.df = Df;
+  R.db = Db;
+  R.mf = moves_f;
+  R.mb = moves_b;
+
+  if (tr) {
+    Trace& o = *tr;
+    o.add("{\"lat\":%lld,\"df\":%lld,\"db\":%lld,\"mf\":%d,\"mb\":%d,\"m\":%d,\"P\":%lld,\"T\":%lld,\"r_t\":%lld,",
+          (long long)R.lat, (long long)Df, (long long)Db, moves_f, moves_b, m, (long long)pl.P, (long long)pl.T,
+          (long long)pl.r_t);
+    o.add("\"N\":[");
+    for (int j = 0; j < m; ++j) o.add("%s%d", j ? "," : "", N[j]);
+    o.add("],\"c_final\":[");
+    for (int j = 0; j < m; ++j) o.add("%s%d", j ? "," : "", c[j]);
+    o.add("],\"cb_final\":[");
+    for (int j = 0; j < m; ++j) o.add("%s%d", j ? "," : "", cb[j]);
+    o.add("],\"deltas_f\":[");
+    for (size_t q = 0; q < deltas_f.size(); ++q) o.add("%s%lld", q ? "," : "", (long long)deltas_f[q]);
+    o.add("],\"deltas_b\":[");
+    for (size_t q = 0; q < deltas_b.size(); ++q) o.add("%s%lld", q ? "," : "", (long long)deltas_b[q]);
+    o.add("],\"Q\":[");
+    for (int j = 0; j < m; ++j) {
+      o.add("%s[", j ? "," : "");
+      for (size_t k = 0; k < Q[j].size(); ++k) o.add("%s%lld", k ? "," : "", (long long)Q[j][k]);
+      o.add("]");
+    }
+    o.add("],\"Qb\":[");
+    for (int j = 0; j < m; ++j) {
+      o.add("%s[", j ? "," : "");
+      for (size_t k = 0; k < Qb[j].size(); ++k) o.add("%s%lld", k ? "," : "", (long long)Qb[j][k]);
+      o.add("]");
+    }
+    o.add("],\"order\":[");  // position i -> (value, j)
+    for (int i = 0; i < n; ++i) o.add("%s[%lld,%d]", i ? "," : "", (long long)ent[i].v, ent[i].j);
+    o.add("],\"tau_f\":[");
+    for (int s = 0; s < Pn; ++s) o.add("%s%lld", s ? "," : "", (long long)SL.tau_f[s]);
+    o.add("],\"tau_b\":[");
+    for (int s = 0; s < Pn; ++s) o.add("%s%lld", s ? "," : "", (long long)SL.tau_b[s]);
+    // in-bubble placements in TEMPLATE time: [j, stage, kind, start, end, chain]
+    o.add("],\"fwd_place\":[");
+    for (size_t q = 0; q < recF.size(); ++q)
+      o.add("%s[%lld,%lld,%lld,%lld,%lld,%lld]", q ? "," : "", (long long)recF[q][0], (long long)recF[q][1],
+            (long long)recF[q][2], (long long)recF[q][3], (long long)recF[q][4], (long long)recF[q][5]);
+    // backward placements converted back to template (real, unshifted) time
+    o.add("],\"bwd_place\":[");
+    for (size_t q = 0; q < recB.size(); ++q)
+      o.add("%s[%lld,%lld,%lld,%lld,%lld,%lld]", q ? "," : "", (long long)recB[q][0], (long long)recB[q][1],
+            (long long)recB[q][2], (long long)(T.T_end - recB[q][4]), (long long)(T.T_end - recB[q][3]),
+            (long long)recB[q][5]);
+    o.add("]}");
+  }
+  return R;
+}
+
+bool build_ctx(const int64_t* blob, i64 len, Ctx& C) {
+  if (!parse(blob, len, C.P)) return false;
+  C.T = build_template(C.P);
+  if (!C.T.ok) return false;
+  C.PL = plans(C.P);
+  C.total = 0;
+  for (auto& pl : C.PL) C.total += pl.count;
+  for (auto& pl : C.PL) {
+    C.SL.push_back(stage_lists(C.P, pl));
+    C.preF.push_back(gpipe(C.SL.back().tau_f, C.P.enc_p2p, C.P.n_mb));
+    C.preB.push_back(gpipe(C.SL.back().tau_b, C.P.enc_p2p, C.P.n_mb));
+  }
+  return true;
+}
+
+// candidate g -> (plan, composition) (R17)
+bool decode(const Ctx& C, u64 g, size_t& e, std::vector<int>& N) {
+  for (size_t q = 0; q < C.PL.size(); ++q) {
+    const Plan& pl = C.PL[q];
+    if (pl.count && g >= pl.first && g < pl.first + pl.count) {
+      e = q;
+      N = unrank(C.P.n_mb, pl.m, g - pl.first);
+      return true;
+    }
+  }
+  return false;
+}
+
+template <class F>
+void parallel_for(i64 count, int threads, F f) {
+  if (threads <= 1 || count < 2) {
+    for (i64 i = 0; i < count; ++i) f(i);
+    return;
+  }
+  std::atomic<i64> next{0};
+  std::vector<std::thread> th;
+  for (int t = 0; t < threads; ++t)
+    th.emplace_back([&]() {
+      for (;;) {
+        i64 b = next.fetch_add(64);
+        if (b >= count) break;
+        for (i64 i = b; i < std::min(count, b + 64); ++i) f(i);
+      }
+    });
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ======================================================================
+// C entry points (the oracle's own, declared nowhere under include/)
+// ======================================================================
+extern "C" {
+
+int oracle_version() { return 1; }
+
+// Template: out = [p, n, T_end, span_def, span, W[p], Wdef[p], F[n], B[n],
+//                  w[p], z[p], ncomp[p], ncomm[p], then per stage comp
+//                  intervals (lo,hi)..., comm intervals ...]
+long long oracle_template(const int64_t* blob, long long len, int64_t* out, long long cap) {
+  Problem P;
+  if (!parse(blob, len, P)) return -1;
+  Template T = build_template(P);
+  if (!T.ok) return -2;
+  std::vector<i64> o;
+  int p = (int)P.pp, n = (int)P.n_mb;
+  o.push_back(p); o.push_back(n); o.push_back(T.T_end); o.push_back(T.span_def); o.push_back(T.span);
+  for (int s = 0; s < p; ++s) o.push_back(T.W[s]);
+  for (int s = 0; s < p; ++s) o.push_back(T.Wdef[s]);
+  for (int i = 0; i < n; ++i) o.push_back(T.F[i]);
+  for (int i = 0; i < n; ++i) o.push_back(T.B[i]);
+  for (int s = 0; s < p; ++s) o.push_back(T.w[s]);
+  for (int s = 0; s < p; ++s) o.push_back(T.z[s]);
+  for (int s = 0; s < p; ++s) o.push_back((i64)T.comp_free[s].size());
+  for (int s = 0; s < p; ++s) o.push_back((i64)T.comm_free[s].size());
+  for (int s = 0; s < p; ++s) {
+    for (auto& iv : T.comp_free[s]) { o.push_back(iv.lo); o.push_back(iv.hi); }
+    for (auto& iv : T.comm_free[s]) { o.push_back(iv.lo); o.push_back(iv.hi); }
+  }
+  if ((long long)o.size() > cap) return -(long long)o.size() - 10;
+  std::memcpy(out, o.data(), o.size() * sizeof(i64));
+  return (long long)o.size();
+}
+
+// Raw LLM kernel timeline of one stage: out = [ncomp, ncomm, (s,e)..., (s,e)...]
+long long oracle_llm_kernels(const int64_t* blob, long long len, int stage, int64_t* out, long long cap) {
+  Problem P;
+  if (!parse(blob, len, P)) return -1;
+  Template T = build_template(P);
+  if (!T.ok || stage < 0 || stage >= P.pp) return -2;
+  std::vector<i64> o{(i64)T.comp_k[stage].size(), (i64)T.comm_k[stage].size()};
+  for (auto& k : T.comp_k[stage]) { o.push_back(k.first); o.push_back(k.second); }
+  for (auto& k : T.comm_k[stage]) { o.push_back(k.first); o.push_back(k.second); }
+  if ((long long)o.size() > cap) return -(long long)o.size() - 10;
+  std::memcpy(out, o.data(), o.size() * sizeof(i64));
+  return (long long)o.size();
+}
+
+// Simulate with explicit warm-up counts W[p]: out = [ok, span, F[n], B[n], last_end[p]]
+long long oracle_simulate(const int64_t* blob, long long len, const int32_t* W, int64_t* out, long long cap) {
+  Problem P;
+  if (!parse(blob, len, P)) return -1;
+  std::vector<int> Wv(W, W + P.pp);
+  Sim S = simulate(P, Wv);
+  int n = (int)P.n_mb;
+  std::vector<i64> o{S.ok ? 1 : 0, S.span};
+  std::vector<i64> F(n, -1), B(n, -1);
+  if (S.ok)
+    for (size_t q = 0; q < S.order[0].size(); ++q) {
+      OpId op = S.order[0][q];
+      if (op.chunk) continue;
+      if (op.fwd) F[op.mb] = S.start[0][q];
+      else B[op.mb] = S.end[0][q];
+    }
+  for (int i = 0; i < n; ++i) o.push_back(F[i]);
+  for (int i = 0; i < n; ++i) o.push_back(B[i]);
+  for (int s = 0; s < P.pp; ++s) o.push_back(S.last_end[s]);
+  if ((long long)o.size() > cap) return -1;
+  std::memcpy(out, o.data(), o.size() * sizeof(i64));
+  return (long long)o.size();
+}
+
+// Plans: out = [nplans, total, then per plan (P, T, dp_enc, m, kept, count, first)]
+long long oracle_plans(const int64_t* blob, long long len, int64_t* out, long long cap) {
+  Problem P;
+  if (!parse(blob, len, P)) return -1;
+  auto PL = plans(P);
+  std::vector<i64> o{(i64)PL.size(), 0};
+  u64 tot = 0;
+  for (auto& pl : PL) {
+    o.push_back(pl.P); o.push_back(pl.T); o.push_back(pl.dp_enc); o.push_back(pl.m);
+    o.push_back(pl.kept); o.push_back((i64)pl.count); o.push_back((i64)pl.first);
+    tot += pl.count;
+  }
+  o[1] = (i64)tot;
+  if ((long long)o.size() > cap) return -1;
+  std::memcpy(out, o.data(), o.size() * sizeof(i64));
+  return (long long)o.size();
+}
+
+int oracle_unrank(long long n, long long m, unsigned long long rank, int32_t* out) {
+  auto N = unrank(n, m, rank);
+  for (size_t j = 0; j < N.size(); ++j) out[j] = N[j];
+  return (int)N.size();
+}
+
+unsigned long long oracle_binom(long long a, long long b) { return binom(a, b); }
+
+// min Delta >= 0 with sortasc(pre - Delta U fixed) <= dl elementwise; INF -> -1
+long long oracle_min_shift(const int64_t* pre, long long npre, const int64_t* fixed, long long nfix, const int64_t* dl) {
+  std::vector<i64> a(pre, pre + npre), b(fixed, fixed + nfix), d(dl, dl + npre + nfix);
+  i64 r = min_shift(a, b, d);
+  return r >= INF ? -1 : r;
+}
+
+// Global ordering: vals[k] finishing time of entry k, pipe[k] its pipeline;
+// owner[i] <- pipeline of LLM microbatch position i.
+int oracle_global_order(const int64_t* vals, const int32_t* pipe, int count, int m, int32_t* owner) {
+  std::vector<OrdE> ent;
+  std::vector<int> seen(m, 0);
+  for (int k = 0; k < count; ++k) ent.push_back({vals[k], pipe[k], seen[pipe[k]]++});
+  auto S = global_order(ent, m);
+  for (int j = 0; j < m; ++j)
+    for (int i : S[j]) owner[i] = j;
+  return 0;
+}
+
+// GPipe fill table: out[s*(c+1)+x]
+int oracle_gpipe(const int64_t* tau, int P, long long p2p, int c, int64_t* out) {
+  std::vector<i64> t(tau, tau + P);
+  auto e = gpipe(t, p2p, c);
+  for (int s = 0; s < P; ++s)
+    for (int x = 0; x <= c; ++x) out[s * (c + 1) + x] = e[s][x];
+  return 0;
+}
+
+// First fit of ONE chain on explicit intervals.  ivs: per stage, per
+// resource: count then (lo,hi) pairs, laid out stage-major; lists: per stage
+// count then (kind, ns).  Returns EF or -1 on failure; placements -> out as
+// (stage, kind, start, end) quads, *nplaced.
+long long oracle_first_fit(int P, const int64_t* ivs, const int64_t* lists, const int64_t* wst, long long p2p,
+                           int64_t* out, int* nplaced) {
+  std::vector<Inst> I(P);
+  std::vector<KList> Ls(P);
+  const int64_t* q = ivs;
+  for (int s = 0; s < P; ++s)
+    for (int r = 0; r < 2; ++r) {
+      i64 cnt = *q++;
+      for (i64 x = 0; x < cnt; ++x) { I[s].res[r].push_back({q[0], q[1]}); q += 2; }
+    }
+  q = lists;
+  for (int s = 0; s < P; ++s) {
+    i64 cnt = *q++;
+    for (i64 x = 0; x < cnt; ++x) { Ls[s].push_back({(int)q[0], q[1]}); q += 2; }
+  }
+  std::vector<Inst*> ins(P);
+  for (int s = 0; s < P; ++s) ins[s] = &I[s];
+  std::vector<i64> w(wst, wst + P);
+  std::vector<Undo> undo;
+  std::vector<std::vector<i64>> rec;
+  i64 EF;
+  bool ok = place_chain(ins, Ls, w, p2p, EF, undo, &rec);
+  *nplaced = (int)rec.size();
+  for (size_t k = 0; k < rec.size(); ++k)
+    for (int t = 0; t < 4; ++t) out[k * 4 + t] = rec[k][t];
+  return ok ? EF : -1;
+}
+
+// ------------------------------------------------------------ search
+struct OracleHandle {
+  Ctx C;
+};
+
+void* oracle_open(const int64_t* blob, long long len) {
+  auto* h = new OracleHandle;
+  if (!build_ctx(blob, len, h->C)) { delete h; return nullptr; }
+  return h;
+}
+void oracle_close(void* h) { delete (OracleHandle*)h; }
+unsigned long long oracle_total(void* h) { return ((OracleHandle*)h)->C.total; }
+
+// lat (and optionally aux = [df, db, mf, mb] per candidate) for given indices
+int oracle_eval(void* h, const uint64_t* idx, long long count, int64_t* lat, int64_t* aux, int threads) {
+  const Ctx& C = ((OracleHandle*)h)->C;
+  std::atomic<int> bad{0};
+  parallel_for(count, threads, [&](i64 i) {
+    size_t e;
+    std::vector<int> N;
+    if (!decode(C, idx[i], e, N)) { bad = 1; lat[i] = -1; return; }
+    Result r = eval_candidate(C, e, N, nullptr);
+    lat[i] = r.lat;
+    if (aux) { aux[4 * i] = r.df; aux[4 * i + 1] = r.db; aux[4 * i + 2] = r.mf; aux[4 * i + 3] = r.mb; }
+  });
+  return bad ? -5 : 0;
+}
+
+// lat for the contiguous range [begin, end)
+int oracle_eval_range(void* h, unsigned long long begin, unsigned long long end, int64_t* lat, int threads) {
+  const Ctx& C = ((OracleHandle*)h)->C;
+  if (end > C.total || begin > end) return -5;
+  std::vector<uint64_t> idx(end - begin);
+  for (u64 g = begin; g < end; ++g) idx[g - begin] = g;
+  return oracle_eval(h, idx.data(), (long long)idx.size(), lat, nullptr, threads);
+}
+
+// Alg. 1: strict-< minimum over the whole space; ties -> lowest index (R18)
+int oracle_best(void* h, int threads, int64_t* best2) {
+  const Ctx& C = ((OracleHandle*)h)->C;
+  std::vector<int64_t> lat(C.total);
+  int rc = oracle_eval_range(h, 0, C.total, lat.data(), threads);
+  if (rc) return rc;
+  i64 bl = INF;
+  u64 bg = 0;
+  for (u64 g = 0; g < C.total; ++g)
+    if (lat[g] < bl) { bl = lat[g]; bg = g; }
+  best2[0] = bl;
+  best2[1] = (int64_t)bg;
+  return 0;
+}
+
+// JSON trace of one candidate
+long long oracle_trace(void* h, unsigned long long g, char* buf, long long cap) {
+  const Ctx& C = ((OracleHandle*)h)->C;
+  size_t e;
+  std::vector<int> N;
+  if (!decode(C, g, e, N)) return -5;
+  Trace tr;
+  eval_candidate(C, e, N, &tr);
+  if ((long long)tr.s.size() + 1 > cap) return -(long long)tr.s.size() - 10;
+  std::memcpy(buf, tr.s.c_str(), tr.s.size() + 1);
+  return (long long)tr.s.size();
+}
+
+}  // extern "C"
