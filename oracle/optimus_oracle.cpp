@@ -1068,6 +1068,55 @@ int oracle_best(void* h, int threads, int64_t* best2) {
   return 0;
 }
 
+// Debug helper for localising GPU mismatches (not used by the search): on
+// fresh instances of PP-row `a` of plan `e`, place forward chains one after
+// another until the first failure (at most kmax); if kf >= 0, instead place
+// exactly kf forward chains (returns -1 if one fails), mirror (R15) and
+// place backward chains until the first failure.  EFs -> out.
+int oracle_row_chains(void* h, int e, int a, int kf, int kmax, int64_t* out) {
+  const Ctx& C = ((OracleHandle*)h)->C;
+  if (e < 0 || e >= (int)C.PL.size()) return -5;
+  const Plan& pl = C.PL[e];
+  int Pn = (int)pl.P;
+  std::vector<Inst> I(Pn);
+  std::vector<Inst*> ins(Pn);
+  std::vector<i64> wst(Pn);
+  for (int s = 0; s < Pn; ++s) {
+    int q = a * Pn + s;
+    I[s].res[0] = C.T.comp_free[q];
+    I[s].res[1] = C.T.comm_free[q];
+    ins[s] = &I[s];
+    wst[s] = C.T.w[q];
+  }
+  int nf = kf < 0 ? kmax : kf, k = 0;
+  for (; k < nf; ++k) {
+    std::vector<Undo> undo;
+    i64 EF;
+    if (!place_chain(ins, C.SL[e].fwd, wst, C.P.enc_p2p, EF, undo, nullptr)) break;
+    if (kf < 0) out[k] = EF;
+  }
+  if (kf < 0) return k;
+  if (k < kf) return -1;
+  std::vector<Inst> M(Pn);
+  for (int s = 0; s < Pn; ++s) {
+    for (int r = 0; r < 2; ++r)
+      for (size_t x = I[s].res[r].size(); x-- > 0;) {
+        Interval mi{C.T.T_end - I[s].res[r][x].hi, C.T.T_end - I[s].res[r][x].lo};
+        if (mi.hi > mi.lo) M[s].res[r].push_back(mi);
+      }
+    ins[s] = &M[s];
+    wst[s] = C.T.T_end - C.T.z[a * Pn + s];
+  }
+  k = 0;
+  for (; k < kmax; ++k) {
+    std::vector<Undo> undo;
+    i64 EF;
+    if (!place_chain(ins, C.SL[e].bwdm, wst, C.P.enc_p2p, EF, undo, nullptr)) break;
+    out[k] = EF;
+  }
+  return k;
+}
+
 // JSON trace of one candidate
 long long oracle_trace(void* h, unsigned long long g, char* buf, long long cap) {
   const Ctx& C = ((OracleHandle*)h)->C;

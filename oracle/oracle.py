@@ -61,6 +61,8 @@ def lib():
         L.oracle_global_order.restype = ctypes.c_int
         L.oracle_global_order.argtypes = [P64, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_int32)]
+        L.oracle_row_chains.restype = ctypes.c_int
+        L.oracle_row_chains.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P64]
         L.oracle_open.restype = ctypes.c_void_p
         L.oracle_open.argtypes = [P64, ctypes.c_longlong]
         L.oracle_close.argtypes = [ctypes.c_void_p]
@@ -291,6 +293,13 @@ class Oracle:
         if rc:
             raise ValueError(rc)
         return int(b[0]), int(b[1])
+
+    def row_chains(self, e: int, a: int, kf: int, kmax: int):
+        """Debug: successive chain EFs on fresh instances of row a of plan e
+        (forward if kf < 0, else backward after kf forward chains)."""
+        out = np.zeros(max(1, kmax), dtype=np.int64)
+        k = lib().oracle_row_chains(self.h, e, a, kf, kmax, _p64(out))
+        return None if k < 0 else out[:k].tolist()
 
     def trace(self, g: int) -> dict:
         cap = 1 << 26

@@ -1,0 +1,572 @@
+// capi.cu — host side of liboptimus (include/optimus.h).
+//
+// Validation, model-planner enumeration + memory prune (§4.1/§4.5, P:296-314,
+// P:482-496; a1 of SURVEY §8(a), host work at load), workspace layout,
+// host->device copy of the packed problem, and the launches of the build
+// kernels (template.cu, chains.cu) and the evaluation kernels (eval.cu).
+// No search step runs on the host; there is no CPU fallback.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/optimus.h"
+#include "optimus_dev.cuh"
+
+namespace optimus {
+int eval_grid(int sms);
+}
+
+using namespace optimus;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(OPTIMUS_ECUDA, "%s: %s", #x, cudaGetErrorString(e_));    \
+  } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct HostPlan {
+  PlanDesc d;
+  bool kept;
+  int64_t dp_enc;
+};
+
+// Everything derived from the problem on the host: packed inputs, plans, layout.
+struct Prep {
+  int32_t p, t, v, n, lc, nb, ntp, nops, icapc, icapm;
+  std::vector<int32_t> lkind, loff, blayers;
+  std::vector<int64_t> lns;
+  std::vector<uint64_t> binom;
+  std::vector<HostPlan> plans;
+  uint64_t total = 0;
+  int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0;
+  int kmax_all = 0;
+  // layout (byte offsets in the workspace)
+  size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
+  size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
+      o_comm_hi, o_sim, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, total_bytes;
+  int grid;
+};
+
+int check_seq(const optimus_seq& s, const char* what, bool need_compute, bool allow_empty) {
+  if (s.len < 0 || (s.len == 0 && !allow_empty)) return fail(OPTIMUS_EINVAL, "%s: empty kernel list", what);
+  if (s.len > 0 && (!s.kind || !s.ns)) return fail(OPTIMUS_EINVAL, "%s: null array", what);
+  bool comp = false;
+  for (int i = 0; i < s.len; ++i) {
+    if (s.kind[i] > 1) return fail(OPTIMUS_EINVAL, "%s[%d]: kind must be 0 (compute) or 1 (comm)", what, i);
+    if (s.ns[i] <= 0) return fail(OPTIMUS_EINVAL, "%s[%d]: duration must be > 0 ns", what, i);
+    comp |= s.kind[i] == 0;
+  }
+  if (need_compute && !comp) return fail(OPTIMUS_EINVAL, "%s: needs at least one compute kernel", what);
+  return OPTIMUS_OK;
+}
+
+int runs_of(const optimus_seq& s, int kind) {
+  int r = 0;
+  for (int i = 0; i < s.len; ++i)
+    if (s.kind[i] == kind && (i == 0 || s.kind[i - 1] != kind)) ++r;
+  return r;
+}
+
+uint64_t binom_sat(int a, int b) {
+  if (b < 0 || b > a) return 0;
+  unsigned __int128 r = 1;
+  b = b < a - b ? b : a - b;
+  for (int i = 1; i <= b; ++i) {
+    r = r * (unsigned __int128)(a - b + i) / (unsigned __int128)i;
+    if (r > (unsigned __int128)UINT64_MAX) return UINT64_MAX;
+  }
+  return (uint64_t)r;
+}
+
+int prepare(const optimus_problem* pb, Prep& X) {
+  if (!pb) return fail(OPTIMUS_EINVAL, "problem is NULL");
+  const optimus_plan& L = pb->llm;
+  if (L.dp < 1 || L.pp < 1 || L.tp < 1 || L.v < 1) return fail(OPTIMUS_EINVAL, "LLM plan fields must be >= 1");
+  if ((int64_t)L.dp * L.pp * L.tp != pb->n_gpu)
+    return fail(OPTIMUS_EINVAL, "dp*pp*tp = %lld != n_gpu = %d", (long long)L.dp * L.pp * L.tp, pb->n_gpu);
+  if (pb->llm_layers < 1 || pb->llm_layers % (L.pp * L.v) != 0)
+    return fail(OPTIMUS_EINVAL, "llm_layers = %d is not a multiple of PP*V = %d", pb->llm_layers, L.pp * L.v);
+  if (pb->n_mb < 1 || pb->n_mb % L.pp != 0)
+    return fail(OPTIMUS_EINVAL, "n_mb = %d must be a positive multiple of PP = %d (interleaved 1F1B)", pb->n_mb, L.pp);
+  if (pb->warmup_policy != 0 && pb->warmup_policy != 1) return fail(OPTIMUS_EINVAL, "warmup_policy must be 0 or 1");
+  if (L.pp > kMaxP) return fail(OPTIMUS_ERANGE, "PP = %d exceeds the supported %d stages", L.pp, kMaxP);
+  if (pb->n_mb > kMaxN) return fail(OPTIMUS_ERANGE, "n_mb = %d exceeds the supported %d", pb->n_mb, kMaxN);
+  if (pb->dp_allgather_ns < 0 || pb->dp_reducescatter_ns < 0 || pb->pp_p2p_ns < 0 || pb->enc_p2p_ns < 0 ||
+      pb->enc_llm_p2p_ns < 0)
+    return fail(OPTIMUS_EINVAL, "DP/P2P durations must be >= 0");
+  if (pb->bytes_per_param < 0 || pb->gpu_mem_bytes < 0 || pb->reserve_bytes < 0 || pb->llm_params < 0)
+    return fail(OPTIMUS_EINVAL, "memory fields must be >= 0");
+  int rc;
+  if ((rc = check_seq(pb->llm_fwd_layer, "llm_fwd_layer", true, false))) return rc;
+  if ((rc = check_seq(pb->llm_bwd_layer, "llm_bwd_layer", true, false))) return rc;
+  if ((runs_of(pb->llm_fwd_layer, 1) > 0) != (runs_of(pb->llm_bwd_layer, 1) > 0))
+    return fail(OPTIMUS_EINVAL, "llm_fwd_layer and llm_bwd_layer must both have TP comm kernels or neither");
+  if (pb->n_branches < 1 || !pb->branch_layers || !pb->branch_params)
+    return fail(OPTIMUS_EINVAL, "need at least one encoder branch");
+  for (int b = 0; b < pb->n_branches; ++b)
+    if (pb->branch_layers[b] < 1) return fail(OPTIMUS_EINVAL, "branch %d has %d layers (< 1)", b, pb->branch_layers[b]);
+  // tp_opts must be exactly the divisors of llm.tp, ascending
+  std::vector<int> divs;
+  for (int d = 1; d <= L.tp; ++d)
+    if (L.tp % d == 0) divs.push_back(d);
+  if (pb->n_tp_opts != (int)divs.size() || !pb->tp_opts)
+    return fail(OPTIMUS_EINVAL, "tp_opts must list the %zu divisors of tp = %d", divs.size(), L.tp);
+  for (size_t i = 0; i < divs.size(); ++i)
+    if (pb->tp_opts[i] != divs[i]) return fail(OPTIMUS_EINVAL, "tp_opts[%zu] = %d, expected %d", i, pb->tp_opts[i], divs[i]);
+  if (!pb->enc_fwd_layer || !pb->enc_bwd_layer) return fail(OPTIMUS_EINVAL, "encoder layer lists are NULL");
+  for (int i = 0; i < pb->n_branches * pb->n_tp_opts; ++i) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "enc_fwd_layer[%d]", i);
+    if ((rc = check_seq(pb->enc_fwd_layer[i], nm, false, true))) return rc;
+    snprintf(nm, sizeof nm, "enc_bwd_layer[%d]", i);
+    if ((rc = check_seq(pb->enc_bwd_layer[i], nm, false, true))) return rc;
+  }
+
+  X.p = L.pp; X.t = L.tp; X.v = L.v; X.n = pb->n_mb;
+  X.lc = pb->llm_layers / (L.pp * L.v);
+  X.nb = pb->n_branches;
+  X.ntp = pb->n_tp_opts;
+  X.nops = 2 * X.n * X.v;
+  const int64_t nv = (int64_t)X.n * X.v;
+  X.icapc = (int)(nv * X.lc * (runs_of(pb->llm_fwd_layer, 0) + runs_of(pb->llm_bwd_layer, 0)) + 1);
+  X.icapm = (int)(nv * X.lc * (runs_of(pb->llm_fwd_layer, 1) + runs_of(pb->llm_bwd_layer, 1)) + 2);
+
+  // packed kernel lists
+  auto push = [&](const optimus_seq& s) {
+    X.loff.push_back((int32_t)X.lkind.size());
+    for (int i = 0; i < s.len; ++i) { X.lkind.push_back(s.kind[i]); X.lns.push_back(s.ns[i]); }
+  };
+  push(pb->llm_fwd_layer);
+  push(pb->llm_bwd_layer);
+  for (int b = 0; b < X.nb; ++b)
+    for (int ti = 0; ti < X.ntp; ++ti) {
+      push(pb->enc_fwd_layer[b * X.ntp + ti]);
+      push(pb->enc_bwd_layer[b * X.ntp + ti]);
+    }
+  X.loff.push_back((int32_t)X.lkind.size());
+  if (X.lkind.empty()) { X.lkind.push_back(0); X.lns.push_back(0); }
+  X.blayers.assign(pb->branch_layers, pb->branch_layers + X.nb);
+  X.binom.assign((kMaxN + 1) * (kMaxN + 1), 0);
+  for (int a = 0; a <= kMaxN; ++a)
+    for (int b = 0; b <= kMaxN; ++b) X.binom[a * (kMaxN + 1) + b] = binom_sat(a, b);
+
+  // model planner: encoder plans (P | PP_llm, T | TP_llm), memory prune (R17, R19)
+  int64_t phi_enc = 0;
+  for (int b = 0; b < X.nb; ++b) phi_enc += pb->branch_params[b];
+  const int64_t dp_llm = L.dp;
+  uint64_t first = 0;
+  int64_t toff = 0, slot = 0;
+  for (int P = 1; P <= X.p; ++P) {
+    if (X.p % P) continue;
+    for (int ti = 0; ti < X.ntp; ++ti) {
+      const int T = pb->tp_opts[ti];
+      HostPlan hp;
+      memset(&hp, 0, sizeof hp);
+      PlanDesc& d = hp.d;
+      d.P = P; d.T = T; d.ti = ti;
+      d.rp = X.p / P; d.rt = X.t / T; d.m = d.rp * d.rt;
+      hp.dp_enc = (int64_t)pb->n_gpu / ((int64_t)P * T);
+      __int128 lhs = (__int128)pb->bytes_per_param * ((__int128)hp.dp_enc * phi_enc + (__int128)dp_llm * pb->llm_params) +
+                     (__int128)pb->reserve_bytes * pb->n_gpu;
+      __int128 rhs = (__int128)pb->gpu_mem_bytes * pb->n_gpu;
+      hp.kept = lhs <= rhs;
+      d.count = (hp.kept && d.m <= X.n) ? binom_sat(X.n - 1, d.m - 1) : 0;
+      d.first = first;
+      if (d.count > UINT64_MAX - first) return fail(OPTIMUS_ERANGE, "candidate count overflows uint64");
+      first += d.count;
+      if (d.count) {
+        d.kmax = X.n - d.m + 1;  // most microbatches one pipeline can hold
+        const int64_t np1 = X.n + 1;
+        d.preF = toff; toff += (int64_t)P * np1;
+        d.preB = toff; toff += (int64_t)P * np1;
+        d.devF = toff; toff += (int64_t)d.rp * np1;
+        d.devB = toff; toff += (int64_t)d.rp * np1;
+        d.inbF = toff; toff += (int64_t)d.rp * d.kmax;
+        d.lenF = toff; toff += d.rp;
+        d.inbB = toff; toff += (int64_t)d.rp * (d.kmax + 1) * d.kmax;
+        d.lenB = toff; toff += (int64_t)d.rp * (d.kmax + 1);
+        d.slot_base = slot;
+        slot += (int64_t)X.p * (d.kmax + 1);
+        X.fwd_units += d.rp;
+        X.bwd_units += (int64_t)d.rp * (d.kmax + 1);
+        X.kmax_all = std::max(X.kmax_all, d.kmax);
+      }
+      X.plans.push_back(hp);
+    }
+  }
+  X.total = first;
+  X.n_tables = std::max<int64_t>(toff, 1);
+  X.n_slots = std::max<int64_t>(slot, 1);
+
+  // workspace layout
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+  X.o_lkind = take(X.lkind.size() * 4);
+  X.o_lns = take(X.lns.size() * 8);
+  X.o_loff = take(X.loff.size() * 4);
+  X.o_blayers = take(X.blayers.size() * 4);
+  X.o_binom = take(X.binom.size() * 8);
+  X.o_plans = take(X.plans.size() * sizeof(PlanDesc));
+  X.inputs_bytes = o;
+  X.o_W = take(X.p * 4);
+  X.o_Wdef = take(X.p * 4);
+  X.o_scal = take(4 * 8);
+  X.o_F = take(X.n * 8);
+  X.o_B = take(X.n * 8);
+  X.o_w = take(X.p * 8);
+  X.o_z = take(X.p * 8);
+  X.o_opstart = take((size_t)X.p * X.nops * 8);
+  X.o_ncomp = take(X.p * 4);
+  X.o_ncomm = take(X.p * 4);
+  X.o_comp_lo = take((size_t)X.p * X.icapc * 8);
+  X.o_comp_hi = take((size_t)X.p * X.icapc * 8);
+  X.o_comm_lo = take((size_t)X.p * X.icapm * 8);
+  X.o_comm_hi = take((size_t)X.p * X.icapm * 8);
+  X.o_sim = take((size_t)kSimWarps * X.p * 2 * X.v * X.n * 8);
+  X.o_tables = take((size_t)X.n_tables * 8);
+  X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
+  X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
+  X.o_snap_hw = take((size_t)X.n_slots * 2 * 4);
+  X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
+  X.o_partials = take((size_t)4096 * 2 * 8);
+  X.o_counter = take(8);
+  X.total_bytes = o;
+  return OPTIMUS_OK;
+}
+
+}  // namespace
+
+struct optimus_ctx {
+  Prep X;
+  Cfg cfg;
+  char* ws = nullptr;
+  int sms = 0;
+  int grid = 0;
+  int build_launches = 0, eval_launches = 0;
+};
+
+namespace {
+
+Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
+  Cfg c;
+  memset(&c, 0, sizeof c);
+  c.p = X.p; c.t = X.t; c.v = X.v; c.n = X.n; c.lc = X.lc; c.policy = pb->warmup_policy;
+  c.nb = X.nb; c.ntp = X.ntp; c.E = (int)X.plans.size(); c.nops = X.nops;
+  c.icapc = X.icapc; c.icapm = X.icapm; c.kmax_all = X.kmax_all;
+  c.T_ag = pb->dp_allgather_ns; c.T_rs = pb->dp_reducescatter_ns; c.pp_p2p = pb->pp_p2p_ns;
+  c.enc_p2p = pb->enc_p2p_ns; c.L = pb->enc_llm_p2p_ns;
+  c.lkind = (const int32_t*)(ws + X.o_lkind);
+  c.lns = (const int64_t*)(ws + X.o_lns);
+  c.loff = (const int32_t*)(ws + X.o_loff);
+  c.blayers = (const int32_t*)(ws + X.o_blayers);
+  c.binom = (const uint64_t*)(ws + X.o_binom);
+  c.plans = (const PlanDesc*)(ws + X.o_plans);
+  c.W = (int32_t*)(ws + X.o_W);
+  c.Wdef = (int32_t*)(ws + X.o_Wdef);
+  c.scal = (int64_t*)(ws + X.o_scal);
+  c.F = (int64_t*)(ws + X.o_F);
+  c.B = (int64_t*)(ws + X.o_B);
+  c.w = (int64_t*)(ws + X.o_w);
+  c.z = (int64_t*)(ws + X.o_z);
+  c.opstart = (int64_t*)(ws + X.o_opstart);
+  c.ncomp = (int32_t*)(ws + X.o_ncomp);
+  c.ncomm = (int32_t*)(ws + X.o_ncomm);
+  c.comp_lo = (int64_t*)(ws + X.o_comp_lo);
+  c.comp_hi = (int64_t*)(ws + X.o_comp_hi);
+  c.comm_lo = (int64_t*)(ws + X.o_comm_lo);
+  c.comm_hi = (int64_t*)(ws + X.o_comm_hi);
+  c.sim = (int64_t*)(ws + X.o_sim);
+  c.tables = (int64_t*)(ws + X.o_tables);
+  c.snap = (int64_t*)(ws + X.o_snap);
+  c.bfill = (int64_t*)(ws + X.o_bfill);
+  c.snap_hw = (int32_t*)(ws + X.o_snap_hw);
+  return c;
+}
+
+int build(optimus_ctx* c, cudaStream_t st) {
+  c->build_launches = 0;
+  CK(launch_template(c->cfg, st, &c->build_launches));
+  CK(launch_plan_tables(c->cfg, st, &c->build_launches));
+  CK(launch_chain_tables(c->cfg, c->X.fwd_units, c->X.bwd_units, st, &c->build_launches));
+  return OPTIMUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* optimus_last_error(void) { return g_err.c_str(); }
+
+int optimus_workspace_bytes(const optimus_problem* pb, size_t* bytes) {
+  if (!bytes) return fail(OPTIMUS_EINVAL, "bytes is NULL");
+  Prep X;
+  int rc = prepare(pb, X);
+  if (rc) return rc;
+  *bytes = X.total_bytes;
+  return OPTIMUS_OK;
+}
+
+int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t bytes, void* cuda_stream,
+                       optimus_ctx** out) {
+  if (!out) return fail(OPTIMUS_EINVAL, "out is NULL");
+  *out = nullptr;
+  optimus_ctx* c = new optimus_ctx;
+  int rc = prepare(pb, c->X);
+  if (rc) { delete c; return rc; }
+  const Prep& X = c->X;
+  if (c->X.total == 0) { delete c; return fail(OPTIMUS_EINFEASIBLE, "no feasible plan"); }
+  if (!d_workspace || ((uintptr_t)d_workspace & 255)) { delete c; return fail(OPTIMUS_EINVAL, "workspace must be a 256-byte aligned device pointer"); }
+  if (bytes < X.total_bytes) {
+    delete c;
+    return fail(OPTIMUS_ENOSPACE, "workspace has %zu bytes, needs %zu", bytes, X.total_bytes);
+  }
+  int dev = 0;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+  if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
+  c->sms = prop.multiProcessorCount;
+  c->grid = std::min(4096, eval_grid(c->sms));
+  c->ws = (char*)d_workspace;
+  c->cfg = make_cfg(X, pb, c->ws);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  // one host->device copy of the packed inputs (the problem's cost tables)
+  std::vector<char> h(X.inputs_bytes, 0);
+  memcpy(h.data() + X.o_lkind, X.lkind.data(), X.lkind.size() * 4);
+  memcpy(h.data() + X.o_lns, X.lns.data(), X.lns.size() * 8);
+  memcpy(h.data() + X.o_loff, X.loff.data(), X.loff.size() * 4);
+  memcpy(h.data() + X.o_blayers, X.blayers.data(), X.blayers.size() * 4);
+  memcpy(h.data() + X.o_binom, X.binom.data(), X.binom.size() * 8);
+  for (size_t i = 0; i < X.plans.size(); ++i) memcpy(h.data() + X.o_plans + i * sizeof(PlanDesc), &X.plans[i].d, sizeof(PlanDesc));
+  e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
+  if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
+  rc = build(c, st);
+  if (rc) { delete c; return rc; }
+  *out = c;
+  return OPTIMUS_OK;
+}
+
+int optimus_plan_only(const optimus_problem* pb, optimus_ctx** out) {
+  if (!out) return fail(OPTIMUS_EINVAL, "out is NULL");
+  *out = nullptr;
+  optimus_ctx* c = new optimus_ctx;
+  int rc = prepare(pb, c->X);
+  if (rc) { delete c; return rc; }
+  *out = c;
+  return OPTIMUS_OK;
+}
+
+int optimus_rebuild(optimus_ctx* c, void* cuda_stream) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  return build(c, (cudaStream_t)cuda_stream);
+}
+
+int optimus_num_candidates(const optimus_ctx* c, uint64_t* total, int32_t* n_plans) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (total) *total = c->X.total;
+  if (n_plans) *n_plans = (int32_t)c->X.plans.size();
+  return OPTIMUS_OK;
+}
+
+int optimus_get_plan(const optimus_ctx* c, int32_t i, optimus_plan* enc, int32_t* m, uint64_t* first, uint64_t* count) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (i < 0 || i >= (int)c->X.plans.size()) return fail(OPTIMUS_ERANGE, "plan %d out of range", i);
+  const HostPlan& hp = c->X.plans[i];
+  if (enc) { enc->dp = (int32_t)hp.dp_enc; enc->pp = hp.d.P; enc->tp = hp.d.T; enc->v = 1; }
+  if (m) *m = hp.d.m;
+  if (first) *first = hp.d.first;
+  if (count) *count = hp.d.count;
+  return OPTIMUS_OK;
+}
+
+static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
+  a.partials = (int64_t*)(c->ws + c->X.o_partials);
+  a.counter = (unsigned long long*)(c->ws + c->X.o_counter);
+  a.total = c->X.total;
+  a.grid = c->grid;
+  c->eval_launches = 0;
+  CK(launch_eval(c->cfg, a, st, &c->eval_launches));
+  return OPTIMUS_OK;
+}
+
+int optimus_eval_candidates(optimus_ctx* c, uint64_t begin, uint64_t end, uint32_t rank, uint32_t world, uint32_t block,
+                            int64_t* d_lat_out, int64_t* d_best2, void* cuda_stream) {
+  if (!c || !d_best2) return fail(OPTIMUS_EINVAL, "ctx/best2 is NULL");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  if (begin > end || end > c->X.total)
+    return fail(OPTIMUS_ERANGE, "range [%llu, %llu) outside [0, %llu)", (unsigned long long)begin,
+                (unsigned long long)end, (unsigned long long)c->X.total);
+  if (world == 0 || rank >= world) return fail(OPTIMUS_EINVAL, "rank %u / world %u", rank, world);
+  if (block == 0) block = 4096;
+  if (block % 64) return fail(OPTIMUS_EINVAL, "block must be a multiple of 64");
+  EvalArgs a;
+  memset(&a, 0, sizeof a);
+  a.begin = begin; a.end = end; a.rank = rank; a.world = world; a.block = block;
+  const uint64_t nblocks = (end - begin + block - 1) / block;
+  a.count = rank < nblocks ? ((nblocks - 1 - rank) / world + 1) * (uint64_t)block : 0;
+  a.lat_out = d_lat_out;
+  a.best2 = d_best2;
+  return eval_common(c, a, (cudaStream_t)cuda_stream);
+}
+
+int optimus_eval_indices(optimus_ctx* c, const uint64_t* d_index, uint64_t count, int64_t* d_lat_out, int64_t* d_best2,
+                         void* cuda_stream) {
+  if (!c || !d_best2 || (!d_index && count)) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  EvalArgs a;
+  memset(&a, 0, sizeof a);
+  a.index = d_index;
+  a.count = count;
+  a.lat_out = d_lat_out;
+  a.best2 = d_best2;
+  a.end = c->X.total;
+  a.world = 1;
+  a.block = 64;
+  if (!d_index) {  // count == 0: nothing to do but a valid empty answer
+    a.index = (const uint64_t*)(c->ws + c->X.o_counter);
+  }
+  return eval_common(c, a, (cudaStream_t)cuda_stream);
+}
+
+int optimus_best_plan(const optimus_ctx* c, const int64_t* h_best2_all_ranks, int32_t world, optimus_result* out,
+                      int32_t* counts_out) {
+  if (!c || !h_best2_all_ranks || !out || world < 1) return fail(OPTIMUS_EINVAL, "NULL argument");
+  int64_t bl = INT64_MAX;
+  uint64_t bg = 0;
+  bool any = false;
+  for (int r = 0; r < world; ++r) {
+    const int64_t l = h_best2_all_ranks[2 * r];
+    const int64_t g = h_best2_all_ranks[2 * r + 1];
+    if (l == INT64_MAX || g < 0) continue;
+    if (!any || l < bl || (l == bl && (uint64_t)g < bg)) { bl = l; bg = (uint64_t)g; any = true; }
+  }
+  if (!any) return fail(OPTIMUS_EINVAL, "no rank reported a candidate");
+  if (bg >= c->X.total) return fail(OPTIMUS_ERANGE, "index %llu >= total", (unsigned long long)bg);
+  for (const HostPlan& hp : c->X.plans) {
+    if (!hp.d.count || bg < hp.d.first || bg >= hp.d.first + hp.d.count) continue;
+    out->lat_ns = bl;
+    out->index = bg;
+    out->enc.dp = (int32_t)hp.dp_enc; out->enc.pp = hp.d.P; out->enc.tp = hp.d.T; out->enc.v = 1;
+    out->m = hp.d.m;
+    if (counts_out) {  // lexicographic unranking of the composition (R17)
+      uint64_t rank = bg - hp.d.first;
+      int rem = c->X.n;
+      for (int j = 0; j < hp.d.m - 1; ++j) {
+        const int parts = hp.d.m - j;
+        int x = 1;
+        for (; x <= rem - (parts - 1); ++x) {
+          const uint64_t cnt = binom_sat(rem - x - 1, parts - 2);
+          if (rank < cnt) break;
+          rank -= cnt;
+        }
+        counts_out[j] = x;
+        rem -= x;
+      }
+      counts_out[hp.d.m - 1] = rem;
+    }
+    return OPTIMUS_OK;
+  }
+  return fail(OPTIMUS_ERANGE, "index not in any plan");
+}
+
+int optimus_debug_template(const optimus_ctx* c, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream) {
+  if (!c || !h_out || !len) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  const Prep& X = c->X;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  CK(cudaStreamSynchronize(st));
+  const int p = X.p, n = X.n;
+  std::vector<int32_t> W(p), nc(p), nm(p);
+  std::vector<int64_t> scal(4), F(n), B(n), w(p), z(p);
+  CK(cudaMemcpy(W.data(), c->cfg.W, p * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(nc.data(), c->cfg.ncomp, p * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(nm.data(), c->cfg.ncomm, p * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(scal.data(), c->cfg.scal, 4 * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(F.data(), c->cfg.F, n * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(B.data(), c->cfg.B, n * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(w.data(), c->cfg.w, p * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(z.data(), c->cfg.z, p * 8, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> o;
+  o.push_back(p); o.push_back(n); o.push_back(scal[1]); o.push_back(scal[0]);
+  for (int s = 0; s < p; ++s) o.push_back(W[s]);
+  for (int i = 0; i < n; ++i) o.push_back(F[i]);
+  for (int i = 0; i < n; ++i) o.push_back(B[i]);
+  for (int s = 0; s < p; ++s) o.push_back(w[s]);
+  for (int s = 0; s < p; ++s) o.push_back(z[s]);
+  for (int s = 0; s < p; ++s) o.push_back(nc[s]);
+  for (int s = 0; s < p; ++s) o.push_back(nm[s]);
+  for (int s = 0; s < p; ++s) {
+    if (nc[s] < 0 || nc[s] > X.icapc || nm[s] < 0 || nm[s] > X.icapm) return fail(OPTIMUS_ERANGE, "interval count out of range");
+    std::vector<int64_t> a(nc[s]), b(nc[s]), cc(nm[s]), d(nm[s]);
+    CK(cudaMemcpy(a.data(), c->cfg.comp_lo + (size_t)s * X.icapc, nc[s] * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(b.data(), c->cfg.comp_hi + (size_t)s * X.icapc, nc[s] * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cc.data(), c->cfg.comm_lo + (size_t)s * X.icapm, nm[s] * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(d.data(), c->cfg.comm_hi + (size_t)s * X.icapm, nm[s] * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < nc[s]; ++i) { o.push_back(a[i]); o.push_back(b[i]); }
+    for (int i = 0; i < nm[s]; ++i) { o.push_back(cc[i]); o.push_back(d[i]); }
+  }
+  *len = o.size();
+  if (o.size() > cap) return fail(OPTIMUS_ERANGE, "need %zu int64", o.size());
+  memcpy(h_out, o.data(), o.size() * 8);
+  return OPTIMUS_OK;
+}
+
+int optimus_debug_plan_tables(const optimus_ctx* c, int32_t i, int64_t* h_out, size_t cap, size_t* len,
+                              void* cuda_stream) {
+  if (!c || !h_out || !len) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (i < 0 || i >= (int)c->X.plans.size()) return fail(OPTIMUS_ERANGE, "plan %d out of range", i);
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  const PlanDesc& d = c->X.plans[i].d;
+  if (!d.count) { *len = 0; return OPTIMUS_OK; }
+  CK(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+  const int64_t np1 = c->X.n + 1;
+  auto get = [&](int64_t off, int64_t cnt, std::vector<int64_t>& o) -> cudaError_t {
+    std::vector<int64_t> tmp(cnt);
+    cudaError_t e = cudaMemcpy(tmp.data(), c->cfg.tables + off, cnt * 8, cudaMemcpyDeviceToHost);
+    o.insert(o.end(), tmp.begin(), tmp.end());
+    return e;
+  };
+  std::vector<int64_t> o{d.rp, d.kmax};
+  CK(get(d.lenF, d.rp, o));
+  CK(get(d.inbF, (int64_t)d.rp * d.kmax, o));
+  CK(get(d.lenB, (int64_t)d.rp * (d.kmax + 1), o));
+  CK(get(d.inbB, (int64_t)d.rp * (d.kmax + 1) * d.kmax, o));
+  CK(get(d.preF, d.P * np1, o));
+  CK(get(d.preB, d.P * np1, o));
+  *len = o.size();
+  if (o.size() > cap) return fail(OPTIMUS_ERANGE, "need %zu int64", o.size());
+  memcpy(h_out, o.data(), o.size() * 8);
+  return OPTIMUS_OK;
+}
+
+int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t* eval_launches) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (build_launches) *build_launches = c->build_launches;
+  if (eval_launches) *eval_launches = c->eval_launches;
+  return OPTIMUS_OK;
+}
+
+void optimus_free(optimus_ctx* c) { delete c; }
+
+}  // extern "C"

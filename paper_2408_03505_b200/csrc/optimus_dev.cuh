@@ -1,0 +1,110 @@
+// optimus_dev.cuh — device-side layout shared by the liboptimus kernels.
+// (Product code.  Nothing here is shared with oracle/.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace optimus {
+
+constexpr int64_t kInf = INT64_MAX / 4;   // "no finite shift" / +infinity
+constexpr int64_t kNegInf = -(INT64_MAX / 4);
+constexpr int kMaxP = 32;                 // LLM pipeline stages handled (one lane per stage in K0)
+constexpr int kMaxN = 32;                 // microbatches per LLM pipeline in K2 (one lane per slot)
+constexpr int kSimWarps = 32;             // warps of the K0 warm-up search block
+
+// List ids in the packed input: 0 = LLM layer fwd, 1 = LLM layer bwd,
+// 2 + 2*(branch*ntp + ti) = encoder layer fwd at TP option ti, +1 = bwd.
+__host__ __device__ inline int enc_list_id(int b, int ti, int ntp, int bwd) { return 2 + 2 * (b * ntp + ti) + bwd; }
+
+// Per-plan descriptor (host-built at load, copied to the workspace).
+struct PlanDesc {
+  int32_t P, T, ti, m, rp, rt, kmax, pad;
+  uint64_t first, count;
+  // offsets, in int64 elements, of this plan's tables from Cfg::tables
+  int64_t preF, preB, devF, devB, inbF, lenF, inbB, lenB;
+  int64_t slot_base;  // first K1 scratch slot of this plan
+};
+
+// Everything a kernel needs: scalars + device pointers into the workspace.
+struct Cfg {
+  int32_t p, t, v, n, lc, policy, nb, ntp, E;
+  int32_t nops;          // 2*n*v ops per stage
+  int32_t icapc, icapm;  // interval capacity per stage: compute-free, comm-free
+  int32_t kmax_all;      // max kmax over plans
+  int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
+  // packed inputs
+  const int32_t* lkind;   // kernel kinds, all lists concatenated
+  const int64_t* lns;     // kernel durations
+  const int32_t* loff;    // list id -> [loff[id], loff[id+1])
+  const int32_t* blayers; // [nb] encoder layers per branch
+  // template (K0)
+  int32_t* W;             // [p] adjusted warm-up counts (policy 1) or defaults
+  int32_t* Wdef;          // [p]
+  int64_t* scal;          // [0] span_def, [1] T_end, [2] ok flag
+  int64_t* F;             // [n]
+  int64_t* B;             // [n]
+  int64_t* w;             // [p] first LLM compute instant
+  int64_t* z;             // [p] last LLM compute end
+  int64_t* opstart;       // [p][nops]
+  int32_t* ncomp;         // [p]
+  int32_t* ncomm;         // [p]
+  int64_t* comp_lo;       // [p][icapc] compute-free interval starts
+  int64_t* comp_hi;       // [p][icapc] compute-free interval ends
+  int64_t* comm_lo;       // [p][icapm]
+  int64_t* comm_hi;       // [p][icapm]
+  int64_t* sim;           // [kSimWarps][p*2*v*n] K0 scratch
+  // plans + tables (K1)
+  const PlanDesc* plans;  // [E]
+  int64_t* tables;
+  int64_t* snap;          // [slots][icapc+icapm] forward fill snapshots (slot k=0 is the working copy)
+  int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
+  int32_t* snap_hw;       // [slots][2] valid prefix of each snapshot slot
+  const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
+};
+
+// Per-op identity in the Megatron interleaved 1F1B order (R2).
+struct OpRef {
+  int fwd, chunk, mb;
+};
+
+__host__ __device__ inline OpRef op_at(int p, int v, int n, int W, int pos) {
+  int nv = n * v, k, fwd;
+  if (pos < W) {
+    k = pos;
+    fwd = 1;
+  } else {
+    int r = pos - W;
+    if (r < 2 * (nv - W)) {
+      k = (r & 1) ? r / 2 : W + r / 2;
+      fwd = (r & 1) ? 0 : 1;
+    } else {
+      k = (nv - W) + (r - 2 * (nv - W));
+      fwd = 0;
+    }
+  }
+  int ch = (k % (p * v)) / p;
+  int mb = (k / (p * v)) * p + (k % p);
+  return OpRef{fwd, fwd ? ch : v - 1 - ch, mb};
+}
+
+}  // namespace optimus
+
+// Host launchers (defined in the .cu files).
+namespace optimus {
+cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
+cudaError_t launch_plan_tables(const Cfg& c, cudaStream_t st, int* launches);
+cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st, int* launches);
+struct EvalArgs {
+  uint64_t begin, end;       // global index range (eval_candidates)
+  uint32_t rank, world, block;
+  const uint64_t* index;     // explicit indices (eval_indices) or nullptr
+  uint64_t count;            // number of indices (explicit) / this rank's candidates
+  int64_t* lat_out;          // nullable
+  int64_t* best2;            // [2]
+  int64_t* partials;         // [grid][2]
+  unsigned long long* counter;
+  uint64_t total;
+  int grid;
+};
+cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
+}  // namespace optimus

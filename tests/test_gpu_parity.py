@@ -1,0 +1,216 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle (-m gpu).
+
+Bit-exact integer equality on every compared value: the template (F, B, w, z,
+T_end, warm-up counts, every compute-free / comm-free interval), the per-row
+chain tables, every candidate's lat and the argmin (lat, index).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from workload import config_problem, random_problem, sample_indices, toy_problem
+
+pytestmark = pytest.mark.gpu
+
+THREADS = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build()
+    torch.cuda.set_device(0)
+    return torch
+
+
+def _load(prob):
+    from paper_2408_03505_b200 import optimus_load_costs
+    return optimus_load_costs(prob)
+
+
+SMALL = [toy_problem(), config_problem(1), config_problem(2)] + [random_problem(s) for s in range(40)]
+BIG = [config_problem(3), config_problem(4), config_problem(5, 16), config_problem(5, 32)]
+
+
+@pytest.mark.parametrize("prob", SMALL[:8] + BIG, ids=lambda p: p["name"])
+def test_template_parity(dev, oracle_mod, prob):
+    ctx = _load(prob)
+    g = ctx.debug_template()
+    o = oracle_mod.template(prob)
+    for k in ("T_end", "W", "F", "B", "w", "z"):
+        assert g[k] == o[k], k
+    assert g["span_def"] == o["span_def"]
+    for s in range(prob["llm"]["pp"]):
+        assert g["comp_free"][s] == [tuple(x) for x in o["comp_free"][s]], f"stage {s} compute-free"
+        assert g["comm_free"][s] == [tuple(x) for x in o["comm_free"][s]], f"stage {s} comm-free"
+
+
+@pytest.mark.parametrize("prob", [toy_problem(), config_problem(2), config_problem(4)] +
+                         [random_problem(s) for s in range(12)], ids=lambda p: p["name"])
+def test_chain_tables_parity(dev, oracle_mod, prob):
+    ctx = _load(prob)
+    o = oracle_mod.Oracle(prob)
+    _, n_plans = ctx.num_candidates()
+    checked = 0
+    for e in range(n_plans):
+        t = ctx.debug_plan_tables(e)
+        if t is None:
+            continue
+        assert t["PRE_F"][-1][1:] == [oracle_mod.gpipe(_taus(prob, ctx.get_plan(e), 0), prob["enc_p2p_ns"],
+                                                       prob["n_mb"])[-1][x] for x in range(1, prob["n_mb"] + 1)]
+        for a in range(t["rp"]):
+            assert t["INB_F"][a] == o.row_chains(e, a, -1, t["kmax"]), (e, a)
+            for kf in range(t["lenF"][a] + 1):
+                assert t["INB_B"][a][kf] == o.row_chains(e, a, kf, t["kmax"]), (e, a, kf)
+                checked += 1
+    assert checked > 0
+
+
+def _taus(prob, plan, bwd):
+    """Stage sums of the encoder work (test-side restatement of R8)."""
+    P, T = plan["pp"], plan["tp"]
+    ti = prob["tp_opts"].index(T)
+    out = []
+    for s in range(P):
+        tot = 0
+        for b in prob["branches"]:
+            L = b["layers"]
+            nl = (s + 1) * L // P - s * L // P
+            tot += nl * sum(ns for _, ns in (b["bwd"] if bwd else b["fwd"])[ti])
+        out.append(tot)
+    return out
+
+
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p["name"])
+def test_full_space_parity(dev, oracle_mod, prob):
+    torch = dev
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    lat = torch.full((total,), -7, dtype=torch.int64, device="cuda")
+    best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, best2, lat_out=lat)
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(prob)
+    ref = o.eval(np.arange(total, dtype=np.uint64), threads=THREADS)
+    got = lat.cpu().numpy()
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first g={bad[:5].tolist()} got={got[bad[:5]].tolist()} ref={ref[bad[:5]].tolist()}"
+    b = best2.cpu().numpy()
+    assert (int(b[0]), int(b[1])) == (int(ref.min()), int(np.argmin(ref)))
+
+
+@pytest.mark.parametrize("prob", BIG, ids=lambda p: p["name"])
+def test_sampled_parity_full_size(dev, oracle_mod, prob):
+    """BASELINE sizes: 4096 seeded indices per config through eval_indices."""
+    torch = dev
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    idx = np.array(sample_indices(20241018, 4096, total), dtype=np.uint64)
+    di = torch.from_numpy(idx.astype(np.int64)).cuda()
+    lat = torch.empty(len(idx), dtype=torch.int64, device="cuda")
+    best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_indices(di, best2, lat_out=lat)
+    torch.cuda.synchronize()
+    ref = oracle_mod.Oracle(prob).eval(idx, threads=THREADS)
+    got = lat.cpu().numpy()
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first idx={idx[bad[:5]].tolist()}"
+    b = best2.cpu().numpy()
+    j = min(range(len(idx)), key=lambda i: (ref[i], idx[i]))
+    assert (int(b[0]), int(b[1])) == (int(ref[j]), int(idx[j]))
+
+
+@pytest.mark.parametrize("prob", [config_problem(4), config_problem(2)], ids=lambda p: p["name"])
+def test_contiguous_ranges_full_size(dev, oracle_mod, prob):
+    """The launch configuration bench.py times (eval_candidates over ranges),
+    checked on a ragged window that straddles plan boundaries."""
+    torch = dev
+    ctx = _load(prob)
+    total, n_plans = ctx.num_candidates()
+    firsts = [ctx.get_plan(i)["first"] for i in range(n_plans) if ctx.get_plan(i)["count"]]
+    for f in firsts[1:4]:
+        begin, end = max(0, f - 1000), min(total, f + 1337)
+        lat = torch.empty(end - begin, dtype=torch.int64, device="cuda")
+        best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(begin, end, best2, lat_out=lat)
+        torch.cuda.synchronize()
+        ref = oracle_mod.Oracle(prob).eval_range(begin, end, threads=THREADS)
+        assert np.array_equal(lat.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_rank_sharding(dev, oracle_mod, world):
+    """Block-cyclic sharding: every rank's best, gathered and decoded, equals the
+    single-rank answer; lat dumps of all ranks tile the space exactly once."""
+    torch = dev
+    prob = config_problem(2)
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    lat = torch.full((total,), -1, dtype=torch.int64, device="cuda")
+    gathered = []
+    for r in range(world):
+        b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(0, total, b2, lat_out=lat, rank=r, world=world, block=128)
+        gathered.append(b2)
+    torch.cuda.synchronize()
+    assert int((lat < 0).sum()) == 0
+    one = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, one)
+    g = torch.stack(gathered).cpu().numpy()
+    res = ctx.best_plan(g)
+    o1 = one.cpu().numpy()
+    assert (res["lat_ns"], res["index"]) == (int(o1[0]), int(o1[1]))
+    ref = oracle_mod.Oracle(prob).eval(np.array([res["index"]], dtype=np.uint64))[0]
+    assert ref == res["lat_ns"]
+
+
+def test_edge_cases(dev, oracle_mod):
+    torch = dev
+    from paper_2408_03505_b200 import OptimusError
+    prob = toy_problem()
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(5, 5, b2)  # empty range
+    torch.cuda.synchronize()
+    assert b2.cpu().tolist() == [2**63 - 1, -1]
+    with pytest.raises(OptimusError):
+        ctx.eval_candidates(0, total + 1, b2)
+    ctx.eval_candidates(total - 1, total, b2)  # one candidate
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(prob)
+    assert b2.cpu().tolist() == [int(o.eval([total - 1])[0]), total - 1]
+    # rebuild from device-resident inputs is idempotent
+    ctx.rebuild()
+    lat = torch.empty(total, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, b2, lat_out=lat)
+    torch.cuda.synchronize()
+    assert np.array_equal(lat.cpu().numpy(), o.eval(np.arange(total, dtype=np.uint64)))
+
+
+def test_degenerate_problems(dev, oracle_mod):
+    """Zero-kernel encoder, N_mb = PP (all warm-up), m = N_mb plans, v = 1."""
+    torch = dev
+    probs = []
+    p = toy_problem()
+    p["branches"][0]["fwd"] = [[], []]
+    p["branches"][0]["bwd"] = [[], []]
+    probs.append(p)
+    for s in range(200, 260):
+        q = random_problem(s, max_n=6)
+        if q["n_mb"] == q["llm"]["pp"] or q["llm"]["v"] == 1:
+            probs.append(q)
+    assert len(probs) > 5
+    for prob in probs:
+        ctx = _load(prob)
+        total, _ = ctx.num_candidates()
+        lat = torch.empty(total, dtype=torch.int64, device="cuda")
+        b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(0, total, b2, lat_out=lat)
+        torch.cuda.synchronize()
+        ref = oracle_mod.Oracle(prob).eval(np.arange(total, dtype=np.uint64))
+        assert np.array_equal(lat.cpu().numpy(), ref), prob["name"]
