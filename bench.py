@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark: candidate schedules evaluated/sec of the Optimus bubble-scheduling
+search (arXiv 2408.03505) on B200, SURVEY.md §8(d).
+
+A step is one pass of the whole hot path over the headline search space
+(BASELINE config 4: ViT-22B + GPT-175B on 3072 simulated GPUs, PP=12 TP=8 V=2,
+24 microbatches, all 20 memory-feasible encoder plans, 5,845,247 candidates):
+  optimus_rebuild         K0 template + K1 plan/chain tables (inputs in HBM)
+  optimus_eval_candidates K2 per-candidate evaluation + K3 argmin (this rank's
+                          block-cyclic shard)
+  all_gather (N > 1)      16 B (lat, index) per rank over NCCL
+value = candidates of the whole space / device time per step (max over ranks).
+e2e   = the same through the public API from host inputs every step: problem
+        marshalling, load (validation, plan enumeration, H2D copy, build),
+        eval, gather, D2H of the result, best_plan decode.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl optimus|reference]
+  N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate schedules evaluated/sec"
+UNIT = "candidates/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["optimus", "reference"], default="optimus")
+    ap.add_argument("--config", type=int, default=4, help="BASELINE.json config (1-5)")
+    ap.add_argument("--n-mb", type=int, default=None, help="microbatches (config 5 sweep)")
+    ap.add_argument("--block", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/cpu/e2e legs")
+    a = ap.parse_args()
+    a.warmup = max(3, a.warmup)
+    return a
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.lines = []
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception as e:  # pragma: no cover
+            log("clock sampler unavailable:", e)
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict | None:
+        if not self.p:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=2)
+        except Exception:
+            self.p.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, rank: int, world: int, prob: dict, name: str):
+    """The oracle (oracle/, plain C++), as it stands, on this box's host cores."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import oracle as O
+    from workload import sample_indices
+    O.build()
+    orc = O.Oracle(prob)
+    cores = os.cpu_count() or 1
+    # calibrate a per-step sample of ~3 s
+    probe = np.array(sample_indices(7, 2000, orc.total), dtype=np.uint64)
+    t0 = time.perf_counter()
+    orc.eval(probe, threads=cores)
+    rate = len(probe) / (time.perf_counter() - t0)
+    per_step = int(max(1000, min(orc.total, rate * 3.0)))
+    times = []
+    for s in range(args.warmup + args.steps):
+        idx = np.array(sample_indices(1000 + s, per_step, orc.total), dtype=np.uint64)
+        t0 = time.perf_counter()
+        orc.eval(idx, threads=cores)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1000 * sum(times) / len(times)
+    value = per_step / (ms / 1000)
+    sample = (f"{per_step} seeded splitmix64 indices of the {orc.total}-candidate space per step, "
+              f"oracle C++ -O2, {cores} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": workload_config(prob, name, world, args, orc.total),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }), flush=True)
+
+
+def workload_config(prob, name, world, args, total):
+    llm = prob["llm"]
+    return {"workload": name, "candidates": int(total), "n_mb": prob["n_mb"],
+            "llm_plan": f"DP{llm['dp']} PP{llm['pp']} TP{llm['tp']} V{llm['v']}",
+            "simulated_gpus": prob["n_gpu"], "encoders": [b["layers"] for b in prob["branches"]],
+            "l2": "flushed before every timed step (256 MiB memset, outside the step events)",
+            "sharding": f"block-cyclic, block={args.block}", "parallelism": f"candidates-dp{world}"}
+
+
+# ---------------------------------------------------------------- cpu leg
+def cpu_baseline(ctx, prob, torch):
+    """Oracle on this box's host cores over a bounded sample of the same space
+    (~10-20 s), plus a GPU-vs-oracle parity spot check on that sample."""
+    import numpy as np
+    from oracle import oracle as O
+    from workload import sample_indices
+    O.build()
+    orc = O.Oracle(prob)
+    cores = os.cpu_count() or 1
+    probe = np.array(sample_indices(11, 2000, orc.total), dtype=np.uint64)
+    t0 = time.perf_counter()
+    orc.eval(probe, threads=cores)
+    rate = len(probe) / (time.perf_counter() - t0)
+    count = int(max(2000, min(orc.total, rate * 12.0)))
+    idx = np.array(sample_indices(12, count, orc.total), dtype=np.uint64)
+    t0 = time.perf_counter()
+    ref = orc.eval(idx, threads=cores)
+    dt = time.perf_counter() - t0
+    di = torch.from_numpy(idx.astype(np.int64)).cuda()
+    lat = torch.empty(count, dtype=torch.int64, device="cuda")
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_indices(di, b2, lat_out=lat)
+    torch.cuda.synchronize()
+    mism = int((lat.cpu().numpy() != ref).sum())
+    return ({"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+             "sample": f"{count} seeded splitmix64 indices of the {orc.total}-candidate space, oracle C++ -O2, "
+                       f"{cores} threads, {dt:.1f} s"},
+            {"sample": count, "mismatches": mism})
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world == 1 and "RANK" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000), *sys.argv]
+        sys.exit(subprocess.call(cmd))
+
+    from workload import config_problem
+    prob = config_problem(args.config, args.n_mb)
+    name = prob["name"]
+    if args.impl == "reference":
+        run_reference(args, rank, world, prob, name)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if dist:
+        dist.barrier()
+    from paper_2408_03505_b200 import optimus as OP
+    from paper_2408_03505_b200.dist import gather_best
+
+    stream = torch.cuda.current_stream()
+    P = OP.Problem(prob)
+    ws = torch.empty(OP.optimus_workspace_bytes(P), dtype=torch.uint8, device="cuda")
+    ctx = OP.Ctx(P, ws, stream)
+    total, n_plans = ctx.num_candidates()
+    ctx.set_timing(True)
+    best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        ctx.rebuild(stream)
+        ctx.eval_candidates(0, total, best2, rank=rank, world=world, block=args.block, stream=stream)
+        if world > 1:
+            return gather_best(best2)
+        return best2.view(1, 2)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    stats0 = ctx.eval_stats()
+
+    sampler = ClockSampler(local) if (not args.profile) else None
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    step_ms, k2_ms, build_ms = [], [], []
+    g = None
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g = step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        b, k = ctx.last_timing()
+        build_ms.append(b)
+        k2_ms.append(k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    stats1 = ctx.eval_stats()
+    nb, ne = ctx.launch_count()
+    best = ctx.best_plan(g.cpu().numpy())
+
+    sum_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(sum_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(sum_ms.item()) / args.steps
+    value = total / (ms_per_step / 1000.0)
+
+    # ---- e2e through the public API from host inputs, every step
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        h2d, d2h = ctx.io_bytes()
+        times = []
+        for s in range(args.warmup + args.steps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            c2 = OP.Ctx(OP.Problem(prob), ws, stream)          # H2D copy + build
+            b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+            c2.eval_candidates(0, total, b2, rank=rank, world=world, block=args.block, stream=stream)
+            gg = gather_best(b2) if world > 1 else b2.view(1, 2)
+            res = c2.best_plan(gg.cpu().numpy())                # D2H + decode
+            c2.free()
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                times.append(dt)
+            assert res["index"] == best["index"]
+        tt = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item()) / args.steps
+        e2e = {"value": total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": e2e_s * 1000}
+
+    # ---- roofline of the dominant kernel (K2), alu-bound
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak_gops = sms * 4 * 32 * sm_mhz * 1e6 / 1e9
+    ops_per_launch = (stats1["ops"] - stats0["ops"]) / args.steps
+    k2_avg = sum(k2_ms) / len(k2_ms)
+    achieved = ops_per_launch / (k2_avg / 1000.0) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            if tj.get("workload") == name:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    roofline = {"bound": "alu", "kernel": "k2_eval", "achieved": achieved, "peak": peak_gops,
+                "unit": "Gop/s (32-bit integer lane-ops)", "frac": achieved / peak_gops, "traffic": traffic,
+                "peak_basis": f"{sms} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                "k2_ms": k2_avg, "k2_share_of_step": k2_avg / (sum(step_ms) / len(step_ms)),
+                "build_ms": sum(build_ms) / len(build_ms),
+                "ops_per_candidate": ops_per_launch / max(1, (stats1["candidates"] - stats0["candidates"]) / args.steps)}
+
+    cpu = parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu, parity = cpu_baseline(ctx, prob, torch)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": workload_config(prob, name, world, args, total),
+            "e2e": e2e, "gpu_launches": (nb + ne) * args.steps, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks,
+            "best": {"lat_ns": best["lat_ns"], "index": best["index"], "enc_plan": best["enc"], "m": best["m"],
+                     "partition": best["counts"]},
+            "parity_spot_check": parity,
+        }
+        print(json.dumps(out), flush=True)
+    ctx.free()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

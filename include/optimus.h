@@ -171,6 +171,23 @@ int optimus_debug_plan_tables(const optimus_ctx* c, int32_t i, int64_t* h_out, s
 /* Kernel launches the last build / eval enqueued (for launch accounting). */
 int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t* eval_launches);
 
+/* Per-kernel timing: when on, the library records CUDA events around each
+ * build (K0+K1 launches) and around the K2 evaluation kernel on the stream
+ * it launches them on; optimus_last_timing waits for them and returns the
+ * elapsed milliseconds of the most recent build / K2 launch. */
+int optimus_set_timing(optimus_ctx* c, int on);
+int optimus_last_timing(const optimus_ctx* c, float* build_ms, float* eval_ms);
+
+/* Cumulative K2 work counters since load (synchronises the stream):
+ * h_out[6] = candidates evaluated, algorithmic 32-bit integer lane-ops
+ * (DESIGN.md §5), forward loop iterations, forward move attempts, backward
+ * iterations, backward attempts. */
+int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream);
+
+/* Bytes load copies host->device (the packed problem) and one evaluation
+ * returns device->host through best2 (16). */
+int optimus_io_bytes(const optimus_ctx* c, uint64_t* h2d, uint64_t* d2h);
+
 void optimus_free(optimus_ctx* c);
 
 const char* optimus_last_error(void);

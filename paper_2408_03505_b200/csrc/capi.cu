@@ -5,6 +5,7 @@
 // host->device copy of the packed problem, and the launches of the build
 // kernels (template.cu, chains.cu) and the evaluation kernels (eval.cu).
 // No search step runs on the host; there is no CPU fallback.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -58,10 +59,11 @@ struct Prep {
   uint64_t total = 0;
   int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0;
   int kmax_all = 0;
+  int nk_max = 0;
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_sim, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, total_bytes;
+      o_comm_hi, o_sim, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, o_stats, total_bytes;
   int grid;
 };
 
@@ -164,6 +166,22 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.loff.push_back((int32_t)X.lkind.size());
   if (X.lkind.empty()) { X.lkind.push_back(0); X.lns.push_back(0); }
   X.blayers.assign(pb->branch_layers, pb->branch_layers + X.nb);
+  for (int ti = 0; ti < X.ntp; ++ti) {  // encoder kernels per chain (K1 stages them in shared memory)
+    int64_t nk = 0;
+    for (int b = 0; b < X.nb; ++b)
+      nk += (int64_t)pb->branch_layers[b] *
+            std::max(pb->enc_fwd_layer[b * X.ntp + ti].len, pb->enc_bwd_layer[b * X.ntp + ti].len);
+    if (nk > 8192) return fail(OPTIMUS_ERANGE, "encoder has %lld kernels per microbatch (> 8192 supported)", (long long)nk);
+    X.nk_max = std::max<int>(X.nk_max, (int)nk);
+  }
+  if ((size_t)X.p * 2 * X.v * X.n * 8 + (size_t)X.p * X.nops * 8 > 200 * 1024)
+    return fail(OPTIMUS_ERANGE, "PP*V*N_mb too large for the K0 shared-memory simulation");
+  {
+    const size_t ci = (size_t)(std::max(X.icapc, X.icapm) + 31) / 32;
+    const size_t per = (size_t)X.nk_max * 9 + 64 + (size_t)(3 * X.p + 1) * 4 + (size_t)X.p * 2 * ci * 8 +
+                       (size_t)X.p * (X.n + 1) * 12 + 64;
+    if (per > 200 * 1024) return fail(OPTIMUS_ERANGE, "K1 shared-memory footprint %zu B exceeds 200 KB", per);
+  }
   X.binom.assign((kMaxN + 1) * (kMaxN + 1), 0);
   for (int a = 0; a <= kMaxN; ++a)
     for (int b = 0; b <= kMaxN; ++b) X.binom[a * (kMaxN + 1) + b] = binom_sat(a, b);
@@ -240,7 +258,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_comp_hi = take((size_t)X.p * X.icapc * 8);
   X.o_comm_lo = take((size_t)X.p * X.icapm * 8);
   X.o_comm_hi = take((size_t)X.p * X.icapm * 8);
-  X.o_sim = take((size_t)kSimWarps * X.p * 2 * X.v * X.n * 8);
+  X.o_sim = take((size_t)X.p * 4);
   X.o_tables = take((size_t)X.n_tables * 8);
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
@@ -248,6 +266,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
+  X.o_stats = take(8 * 8);
   X.total_bytes = o;
   return OPTIMUS_OK;
 }
@@ -261,6 +280,12 @@ struct optimus_ctx {
   int sms = 0;
   int grid = 0;
   int build_launches = 0, eval_launches = 0;
+  bool timing = false;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // build start/end, K2 start/end
+  ~optimus_ctx() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 namespace {
@@ -270,7 +295,7 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   memset(&c, 0, sizeof c);
   c.p = X.p; c.t = X.t; c.v = X.v; c.n = X.n; c.lc = X.lc; c.policy = pb->warmup_policy;
   c.nb = X.nb; c.ntp = X.ntp; c.E = (int)X.plans.size(); c.nops = X.nops;
-  c.icapc = X.icapc; c.icapm = X.icapm; c.kmax_all = X.kmax_all;
+  c.icapc = X.icapc; c.icapm = X.icapm; c.kmax_all = X.kmax_all; c.nk_max = std::max(1, X.nk_max);
   c.T_ag = pb->dp_allgather_ns; c.T_rs = pb->dp_reducescatter_ns; c.pp_p2p = pb->pp_p2p_ns;
   c.enc_p2p = pb->enc_p2p_ns; c.L = pb->enc_llm_p2p_ns;
   c.lkind = (const int32_t*)(ws + X.o_lkind);
@@ -293,7 +318,7 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.comp_hi = (int64_t*)(ws + X.o_comp_hi);
   c.comm_lo = (int64_t*)(ws + X.o_comm_lo);
   c.comm_hi = (int64_t*)(ws + X.o_comm_hi);
-  c.sim = (int64_t*)(ws + X.o_sim);
+  c.bestw = (int32_t*)(ws + X.o_sim);
   c.tables = (int64_t*)(ws + X.o_tables);
   c.snap = (int64_t*)(ws + X.o_snap);
   c.bfill = (int64_t*)(ws + X.o_bfill);
@@ -303,9 +328,11 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
 
 int build(optimus_ctx* c, cudaStream_t st) {
   c->build_launches = 0;
+  if (c->timing) CK(cudaEventRecord(c->ev[0], st));
   CK(launch_template(c->cfg, st, &c->build_launches));
   CK(launch_plan_tables(c->cfg, st, &c->build_launches));
   CK(launch_chain_tables(c->cfg, c->X.fwd_units, c->X.bwd_units, st, &c->build_launches));
+  if (c->timing) CK(cudaEventRecord(c->ev[1], st));
   return OPTIMUS_OK;
 }
 
@@ -358,6 +385,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   for (size_t i = 0; i < X.plans.size(); ++i) memcpy(h.data() + X.o_plans + i * sizeof(PlanDesc), &X.plans[i].d, sizeof(PlanDesc));
   e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);
@@ -405,6 +433,9 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.counter = (unsigned long long*)(c->ws + c->X.o_counter);
   a.total = c->X.total;
   a.grid = c->grid;
+  a.stats = (unsigned long long*)(c->ws + c->X.o_stats);
+  a.ev0 = c->timing ? c->ev[2] : nullptr;
+  a.ev1 = c->timing ? c->ev[3] : nullptr;
   c->eval_launches = 0;
   CK(launch_eval(c->cfg, a, st, &c->eval_launches));
   return OPTIMUS_OK;
@@ -564,6 +595,41 @@ int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t*
   if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
   if (build_launches) *build_launches = c->build_launches;
   if (eval_launches) *eval_launches = c->eval_launches;
+  return OPTIMUS_OK;
+}
+
+int optimus_set_timing(optimus_ctx* c, int on) {
+  if (!c || !c->ws) return fail(OPTIMUS_EINVAL, "ctx is NULL or host-only");
+  if (on && !c->ev[0])
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  c->timing = on != 0;
+  return OPTIMUS_OK;
+}
+
+int optimus_last_timing(const optimus_ctx* c, float* build_ms, float* eval_ms) {
+  if (!c || !c->timing) return fail(OPTIMUS_EINVAL, "timing is off (optimus_set_timing)");
+  if (build_ms) {
+    CK(cudaEventSynchronize(c->ev[1]));
+    CK(cudaEventElapsedTime(build_ms, c->ev[0], c->ev[1]));
+  }
+  if (eval_ms) {
+    CK(cudaEventSynchronize(c->ev[3]));
+    CK(cudaEventElapsedTime(eval_ms, c->ev[2], c->ev[3]));
+  }
+  return OPTIMUS_OK;
+}
+
+int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream) {
+  if (!c || !c->ws || !h_out) return fail(OPTIMUS_EINVAL, "NULL argument or host-only ctx");
+  CK(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+  CK(cudaMemcpy(h_out, c->ws + c->X.o_stats, 6 * 8, cudaMemcpyDeviceToHost));
+  return OPTIMUS_OK;
+}
+
+int optimus_io_bytes(const optimus_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (h2d) *h2d = c->X.inputs_bytes;
+  if (d2h) *d2h = 16;
   return OPTIMUS_OK;
 }
 

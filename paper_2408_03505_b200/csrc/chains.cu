@@ -20,6 +20,8 @@
 //   of forward snapshot kf.
 // First fit is warp-cooperative: a window of 32 consecutive intervals lives
 // in registers (lane i = interval base+i), one ballot tests all 32.
+#include <algorithm>
+
 #include "optimus_dev.cuh"
 
 namespace optimus {
@@ -82,95 +84,76 @@ __global__ void k_plan_tables(Cfg c) {
 }
 
 // ------------------------------------------------------ first-fit machinery
-// View of one (LLM stage, resource) interval list for one unit.
-struct View {
-  int count;
-  bool mirror;
-  const int64_t* S;   // template interval starts
-  const int64_t* H;   // template interval ends
-  int64_t* fill;      // this unit's fill pointers (own direction)
-  int* hw;            // valid prefix of `fill` (lives in shared memory)
-  const int64_t* snapf;  // mirror only: forward fill snapshot
-  int hwf;               // mirror only: valid prefix of the snapshot
+// Register view of one (LLM stage, resource) interval list of one unit.
+// Forward (M = false): intervals as in the template; fill = this unit's fill
+// pointers, valid below hw.  Mirrored (M = true, R15): interval i' is real
+// interval count-1-i' in time t -> T_end - t; its end is T_end minus the
+// forward fill pointer of forward snapshot kf (valid below hwf).
+template <bool M>
+struct VR {
+  int count, hw, hwf;
+  const int64_t* S;
+  const int64_t* H;
+  int64_t* fill;
+  const int64_t* snapf;
   int64_t T_end;
-};
-
-// forward fill pointer of REAL interval r (mirror view)
-__device__ __forceinline__ int64_t fwd_lo(const View& V, int r) { return r < V.hwf ? V.snapf[r] : V.S[r]; }
-
-__device__ __forceinline__ int64_t view_hi(const View& V, int i) {
-  if (!V.mirror) return V.H[i];
-  return V.T_end - fwd_lo(V, V.count - 1 - i);  // mirrored end = T_end - forward fill pointer (R15)
-}
-__device__ __forceinline__ int64_t view_start(const View& V, int i) {
-  if (!V.mirror) return V.S[i];
-  return V.T_end - V.H[V.count - 1 - i];
-}
-
-struct Window {
-  int base;
-  bool loaded, dirty;
-  int64_t lo, hi;  // interval base+lane
-};
-
-__device__ __forceinline__ void win_load(const View& V, Window& w) {
-  const int i = w.base + (threadIdx.x & 31);
-  if (i < V.count) {
-    w.hi = view_hi(V, i);
-    w.lo = i < *V.hw ? V.fill[i] : view_start(V, i);
-  } else {
-    w.hi = kNegInf;
-    w.lo = 0;
+  __device__ __forceinline__ int64_t hi_at(int i) const {
+    if (!M) return H[i];
+    const int r = count - 1 - i;
+    return T_end - (r < hwf ? snapf[r] : S[r]);
   }
-  w.loaded = true;
-  w.dirty = false;
+  __device__ __forceinline__ int64_t start_at(int i) const { return M ? T_end - H[count - 1 - i] : S[i]; }
+  __device__ __forceinline__ int64_t lo_at(int i) const { return i < hw ? fill[i] : start_at(i); }
+};
+
+// A window of 32 consecutive intervals in registers (lane l = interval
+// base+l) plus the prefetched next window.
+struct Win {
+  int base;
+  bool dirty;
+  int64_t lo, hi, nlo, nhi;
+};
+
+template <bool M>
+__device__ __forceinline__ void win_fetch(const VR<M>& V, int b, int64_t& lo, int64_t& hi) {
+  const int i = b + (threadIdx.x & 31);
+  if (i < V.count) {
+    hi = V.hi_at(i);
+    lo = V.lo_at(i);
+  } else {
+    hi = kNegInf;
+    lo = 0;
+  }
 }
 
-__device__ __forceinline__ void win_writeback(const View& V, Window& w) {
-  if (!w.loaded || !w.dirty) return;
+template <bool M>
+__device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
+  w.base = b;
+  w.dirty = false;
+  win_fetch(V, b, w.lo, w.hi);
+  win_fetch(V, b + 32, w.nlo, w.nhi);
+}
+
+template <bool M>
+__device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
+  if (!w.dirty) return;
   const int lane = threadIdx.x & 31;
-  const int hw = *V.hw;
-  for (int i = hw + lane; i < w.base; i += 32) V.fill[i] = view_start(V, i);  // gap fill
+  for (int i = V.hw + lane; i < w.base; i += 32) V.fill[i] = V.start_at(i);  // gap fill
   const int i = w.base + lane;
   if (i < V.count) V.fill[i] = w.lo;
-  __syncwarp();
-  if (lane == 0) *V.hw = max(hw, min(V.count, w.base + 32));
-  __syncwarp();
+  V.hw = max(V.hw, min(V.count, w.base + 32));
   w.dirty = false;
+  __syncwarp();
 }
 
-// first interval index with end > ready (ends are non-decreasing)
-__device__ int first_end_after(const View& V, int64_t ready) {
-  const int lane = threadIdx.x & 31;
-  int lo = 0, hi = V.count;
-  while (hi - lo > 32) {
-    const int step = (hi - lo + 31) / 32;
-    const int i = lo + lane * step;
-    const bool le = i < hi && view_hi(V, i) <= ready;
-    const int cnt = __popc(__ballot_sync(FULL, le));
-    if (cnt == 0) return lo;
-    const int nlo = lo + (cnt - 1) * step + 1;
-    hi = min(hi, lo + cnt * step);
-    lo = nlo;
-  }
-  const int i = lo + lane;
-  const unsigned b = __ballot_sync(FULL, i < hi && view_hi(V, i) > ready);
-  return b ? lo + __ffs(b) - 1 : hi;
-}
-
-// Place one kernel of duration d at or after `ready` (R12): scan intervals
-// in time order from the first with end > ready, take the first where
-// max(ready, lo) + d <= end; lo <- x + d.
-__device__ __forceinline__ bool place_kernel(const View& V, Window& w, int64_t d, int64_t& ready) {
+// Place one kernel of duration d at or after `ready` (R12): the first
+// interval (time order) with end > ready and max(ready, lo) + d <= end.
+template <bool M>
+__device__ __forceinline__ bool place(VR<M>& V, Win& w, int64_t d, int64_t& ready) {
   const int lane = threadIdx.x & 31;
   for (;;) {
-    if (!w.loaded) {
-      if (w.base >= V.count) return false;
-      win_load(V, w);
-    }
     const int64_t x = max(ready, w.lo);
-    const bool ok = w.hi > ready && x + d <= w.hi;
-    const unsigned b = __ballot_sync(FULL, ok);
+    const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
     if (b) {
       const int f = __ffs(b) - 1;
       const int64_t xf = __shfl_sync(FULL, x, f);
@@ -179,54 +162,151 @@ __device__ __forceinline__ bool place_kernel(const View& V, Window& w, int64_t d
       ready = xf + d;
       return true;
     }
-    win_writeback(V, w);
+    win_flush(V, w);
+    if (w.base + 32 >= V.count) return false;
     w.base += 32;
-    w.loaded = false;
+    w.lo = w.nlo;
+    w.hi = w.nhi;
+    win_fetch(V, w.base + 32, w.nlo, w.nhi);
   }
 }
 
-struct Row {
-  int P, ti, a;
+// Per-warp shared memory of a K1 unit.
+struct UnitSm {
+  int64_t* seq_d;     // [NK] flattened kernel durations of the whole encoder, stage-major
+  uint8_t* seq_k;     // [NK] kinds
+  int* soff;          // [P+1] stage offsets into seq
+  int* hw;            // [2P] valid fill prefix per (stage, resource)
+  int64_t* ci;        // [P][2][CI] coarse index: end of the last interval of each 32-block
+  int CI;
 };
 
-// One chain over stages 0..P-1 (R12; mirrored lists and w' for backward, R15).
-// views[2*s + r]; returns false on failure (caller stops the unit).
-__device__ bool place_chain(const Cfg& c, const Row& R, View* views, bool mirror, int64_t& EF) {
-  const int64_t T_end = c.scal[1];
-  int64_t ready = 0, prev = 0;
-  for (int s = 0; s < R.P; ++s) {
-    const int q = R.a * R.P + s;
-    const int64_t ws = mirror ? T_end - c.z[q] : c.w[q];
-    ready = (s == 0) ? ws : max(prev + c.enc_p2p, ws);
-    Window w0, w1;  // compute-free / comm-free windows of this stage
-    w0.base = first_end_after(views[2 * s + 0], ready);
-    w1.base = first_end_after(views[2 * s + 1], ready);
-    w0.loaded = w0.dirty = w1.loaded = w1.dirty = false;
-    for (int b = 0; b < c.nb; ++b) {
-      const int L = c.blayers[b];
-      const int l0 = s * L / R.P, l1 = (s + 1) * L / R.P;
-      const int id = enc_list_id(b, R.ti, c.ntp, mirror ? 1 : 0);
-      const int off = c.loff[id], len = c.loff[id + 1] - off;
-      for (int l = l0; l < l1; ++l)
-        for (int k = 0; k < len; ++k) {
-          // mirrored time runs each layer's backward list in reverse (R15)
-          const int kk = mirror ? off + len - 1 - k : off + k;
-          const int kind = __ldg(&c.lkind[kk]);
-          const int64_t d = __ldg(&c.lns[kk]);
-          const bool ok = kind == 0 ? place_kernel(views[2 * s + 0], w0, d, ready)
-                                    : place_kernel(views[2 * s + 1], w1, d, ready);
-          if (!ok) return false;
-        }
-    }
-    win_writeback(views[2 * s + 0], w0);
-    win_writeback(views[2 * s + 1], w1);
-    prev = ready;
-  }
-  EF = ready;
-  return true;
+__host__ __device__ inline size_t unit_smem_bytes(int NK, int P, int CI) {
+  return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)NK + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
+         ((size_t)2 * P * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8;
 }
 
-constexpr int kK1Warps = 4;
+__device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
+  UnitSm u;
+  u.seq_d = (int64_t*)p;
+  p += ((size_t)NK * 8 + 15) / 16 * 16;
+  u.seq_k = p;
+  p += ((size_t)NK + 15) / 16 * 16;
+  u.soff = (int*)p;
+  p += ((size_t)(P + 1) * 4 + 15) / 16 * 16;
+  u.hw = (int*)p;
+  p += ((size_t)2 * P * 4 + 15) / 16 * 16;
+  u.ci = (int64_t*)p;
+  u.CI = CI;
+  return u;
+}
+
+// Flatten the encoder's stage kernel lists (R8; §4.4 branches in order,
+// P:478) for plan pd: stage s = for each branch its layers
+// [floor(sL/P), floor((s+1)L/P)); mirrored time runs each layer's backward
+// list in reverse (R15).
+__device__ void build_seq(const Cfg& c, const PlanDesc& pd, bool mirror, UnitSm& U) {
+  const int lane = threadIdx.x & 31, P = pd.P;
+  int pos = 0;
+  for (int s = 0; s < P; ++s) {
+    if (lane == 0) U.soff[s] = pos;
+    for (int b = 0; b < c.nb; ++b) {
+      const int L = c.blayers[b];
+      const int l0 = s * L / P, l1 = (s + 1) * L / P;
+      const int id = enc_list_id(b, pd.ti, c.ntp, mirror ? 1 : 0);
+      const int off = c.loff[id], len = c.loff[id + 1] - off;
+      const int cnt = (l1 - l0) * len;
+      for (int x = lane; x < cnt; x += 32) {
+        const int k = x % len;
+        const int kk = mirror ? off + len - 1 - k : off + k;
+        U.seq_d[pos + x] = c.lns[kk];
+        U.seq_k[pos + x] = (uint8_t)c.lkind[kk];
+      }
+      pos += cnt;
+    }
+  }
+  if (lane == 0) U.soff[P] = pos;
+  __syncwarp();
+}
+
+template <bool M>
+__device__ VR<M> make_view(const Cfg& c, const PlanDesc& pd, int a, int s, int r, int64_t* fill,
+                           const int64_t* snapf, int hwf, int hw) {
+  const int q = a * pd.P + s;
+  VR<M> V;
+  V.count = r == 0 ? c.ncomp[q] : c.ncomm[q];
+  V.S = r == 0 ? c.comp_lo + (int64_t)q * c.icapc : c.comm_lo + (int64_t)q * c.icapm;
+  V.H = r == 0 ? c.comp_hi + (int64_t)q * c.icapc : c.comm_hi + (int64_t)q * c.icapm;
+  V.fill = fill;
+  V.snapf = snapf;
+  V.hwf = hwf;
+  V.hw = hw;
+  V.T_end = c.scal[1];
+  return V;
+}
+
+// coarse index of one view: ci[k] = end of interval min(count-1, 32k+31)
+template <bool M>
+__device__ void build_ci(const VR<M>& V, int64_t* ci, int CI) {
+  const int nblk = (V.count + 31) / 32;
+  for (int k = threadIdx.x & 31; k < CI; k += 32)
+    ci[k] = k < nblk ? V.hi_at(min(V.count - 1, 32 * k + 31)) : kInf;
+  __syncwarp();
+}
+
+// first 32-block whose last interval ends after `ready`
+__device__ __forceinline__ int ci_search(const int64_t* ci, int CI, int64_t ready) {
+  const int lane = threadIdx.x & 31;
+  for (int b = 0; b < CI; b += 32) {
+    const int k = b + lane;
+    const unsigned m = __ballot_sync(FULL, k < CI && ci[k] > ready);
+    if (m) return 32 * (b + __ffs(m) - 1);
+  }
+  return 32 * CI;
+}
+
+struct UnitCtx {
+  int P, a;
+  int64_t* fill;        // this unit's fill state, slot-major: [P][icapc + icapm]
+  const int64_t* snap;  // mirror: forward snapshot kf, same layout
+  const int* snap_hw;   // mirror: [P][2] (nullptr -> all 0)
+};
+
+// Place stage s of one chain starting at `ready` (R12; mirrored lists and
+// w' = T_end - z for backward, R15).  On success *end = the stage's last
+// kernel end.  On failure the stage's fill state may be partly modified
+// (the unit stops).
+template <bool M>
+__device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, UnitSm& U, int s, int64_t ready,
+                            int64_t* end) {
+  const int icap = c.icapc + c.icapm;
+  int64_t* f0 = X.fill + (int64_t)s * icap;
+  const int64_t* s0 = M ? X.snap + (int64_t)s * icap : nullptr;
+  VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, s0, X.snap_hw ? X.snap_hw[2 * s] : 0, U.hw[2 * s]);
+  VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0 + c.icapc, M ? s0 + c.icapc : nullptr,
+                          X.snap_hw ? X.snap_hw[2 * s + 1] : 0, U.hw[2 * s + 1]);
+  Win w0, w1;  // compute-free / comm-free windows of this stage
+  win_open(V0, w0, ci_search(U.ci + (2 * s) * U.CI, U.CI, ready));
+  win_open(V1, w1, ci_search(U.ci + (2 * s + 1) * U.CI, U.CI, ready));
+  const int i0 = U.soff[s], i1 = U.soff[s + 1];
+  bool ok = true;
+  int64_t d = i0 < i1 ? U.seq_d[i0] : 0;
+  int kind = i0 < i1 ? U.seq_k[i0] : 0;
+  for (int i = i0; i < i1 && ok; ++i) {
+    const int64_t dn = U.seq_d[min(i + 1, i1 - 1)];  // prefetch the next kernel
+    const int kn = U.seq_k[min(i + 1, i1 - 1)];
+    ok = kind == 0 ? place(V0, w0, d, ready) : place(V1, w1, d, ready);
+    d = dn;
+    kind = kn;
+  }
+  if (!ok) return false;
+  win_flush(V0, w0);
+  win_flush(V1, w1);
+  if ((threadIdx.x & 31) == 0) { U.hw[2 * s] = V0.hw; U.hw[2 * s + 1] = V1.hw; }
+  __syncwarp();
+  *end = ready;
+  return true;
+}
 
 __device__ bool decode_row_unit(const Cfg& c, int64_t u, bool with_kf, int& e, int& a, int& kf) {
   for (e = 0; e < c.E; ++e) {
@@ -243,92 +323,105 @@ __device__ bool decode_row_unit(const Cfg& c, int64_t u, bool with_kf, int& e, i
   return false;
 }
 
-__global__ void __launch_bounds__(kK1Warps * 32) k1_forward(Cfg c, int64_t units) {
-  __shared__ int hw_sm[kK1Warps][2 * kMaxP];
-  __shared__ View views_sm[kK1Warps][2 * kMaxP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t u = (int64_t)blockIdx.x * kK1Warps + warp;
-  if (u >= units) return;
-  int e, a, kf;
-  if (!decode_row_unit(c, u, false, e, a, kf)) return;
-  const PlanDesc pd = c.plans[e];
-  const int P = pd.P, icap = c.icapc + c.icapm;
-  View* V = views_sm[warp];
-  int* hw = hw_sm[warp];
-  auto slot = [&](int k, int s) { return pd.slot_base + ((int64_t)k * pd.rp + a) * P + s; };
-  if (lane < 2 * P) {
-    const int s = lane >> 1, r = lane & 1, q = a * P + s;
-    View& v = V[lane];
-    v.count = r == 0 ? c.ncomp[q] : c.ncomm[q];
-    v.mirror = false;
-    v.S = r == 0 ? c.comp_lo + (int64_t)q * c.icapc : c.comm_lo + (int64_t)q * c.icapm;
-    v.H = r == 0 ? c.comp_hi + (int64_t)q * c.icapc : c.comm_hi + (int64_t)q * c.icapm;
-    v.fill = c.snap + slot(0, s) * icap + (r == 0 ? 0 : c.icapc);
-    v.hw = &hw[lane];
-    v.snapf = nullptr;
-    v.hwf = 0;
-    v.T_end = c.scal[1];
-    hw[lane] = 0;
-  }
-  __syncwarp();
-  int k = 0;
-  for (; k < pd.kmax; ++k) {
-    int64_t EF;
-    if (!place_chain(c, Row{P, pd.ti, a}, V, false, EF)) break;
-    if (lane == 0) c.tables[pd.inbF + (int64_t)a * pd.kmax + k] = EF;
-    // snapshot the fill state after k+1 chains for the backward units
-    if (k + 1 <= pd.kmax) {
-      for (int sr = 0; sr < 2 * P; ++sr) {
-        const int s = sr >> 1, r = sr & 1;
-        const int h = hw[sr];
-        const int64_t* src = V[sr].fill;
-        int64_t* dst = c.snap + slot(k + 1, s) * icap + (r == 0 ? 0 : c.icapc);
-        for (int i = lane; i < h; i += 32) dst[i] = src[i];
-        if (lane == 0) c.snap_hw[slot(k + 1, s) * 2 + r] = h;
-      }
-    }
-    __syncwarp();
-  }
-  if (lane == 0) c.tables[pd.lenF + a] = k;
+struct K1Launch {
+  int NK, Pmax, CI, KM;  // KM = max kmax
+};
+
+__host__ __device__ inline size_t k1_smem_bytes(const K1Launch& L) {
+  return unit_smem_bytes(L.NK, L.Pmax, L.CI) + (size_t)L.Pmax * L.KM * (8 + 4) + 16;
 }
 
-__global__ void __launch_bounds__(kK1Warps * 32) k1_backward(Cfg c, int64_t units) {
-  __shared__ int hw_sm[kK1Warps][2 * kMaxP];
-  __shared__ View views_sm[kK1Warps][2 * kMaxP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t u = (int64_t)blockIdx.x * kK1Warps + warp;
-  if (u >= units) return;
+// One K1 unit per block, one warp per encoder stage s (a wavefront over
+// chains): chain k of stage s starts when chain k of stage s-1 has ended
+// (shared-memory flags) and chain k-1 of stage s is done (program order).
+// Forward (M = false): successive chains on fresh instances, fill state of
+// every stage snapshotted after every chain.  Backward (M = true): mirrored
+// chains on top of forward snapshot kf.  Both stop at the first failure.
+template <bool M>
+__global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ int stop_at;  // first chain index known to fail (chains >= it are void)
+  const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int e, a, kf;
-  if (!decode_row_unit(c, u, true, e, a, kf)) return;
+  if (!decode_row_unit(c, blockIdx.x, M, e, a, kf)) return;  // uniform over the block
   const PlanDesc pd = c.plans[e];
-  const int lenF = (int)c.tables[pd.lenF + a];
-  if (kf > lenF) return;  // no pipeline of this row can have kf forward chains
   const int P = pd.P, icap = c.icapc + c.icapm;
-  View* V = views_sm[warp];
-  int* hw = hw_sm[warp];
-  auto slot = [&](int k, int s) { return pd.slot_base + ((int64_t)k * pd.rp + a) * P + s; };
-  if (lane < 2 * P) {
-    const int s = lane >> 1, r = lane & 1, q = a * P + s;
-    View& v = V[lane];
-    v.count = r == 0 ? c.ncomp[q] : c.ncomm[q];
-    v.mirror = true;
-    v.S = r == 0 ? c.comp_lo + (int64_t)q * c.icapc : c.comm_lo + (int64_t)q * c.icapm;
-    v.H = r == 0 ? c.comp_hi + (int64_t)q * c.icapc : c.comm_hi + (int64_t)q * c.icapm;
-    v.fill = c.bfill + slot(kf, s) * icap + (r == 0 ? 0 : c.icapc);
-    v.hw = &hw[lane];
-    v.snapf = c.snap + slot(kf, s) * icap + (r == 0 ? 0 : c.icapc);
-    v.hwf = kf == 0 ? 0 : c.snap_hw[slot(kf, s) * 2 + r];
-    v.T_end = c.scal[1];
-    hw[lane] = 0;
+  if (M && kf > (int)c.tables[pd.lenF + a]) return;  // uniform: no pipeline of this row has kf forward chains
+  const bool active = s < P;  // warps beyond this plan's P only join the barriers
+  UnitSm U = carve(dsm, L.NK, L.Pmax, L.CI);
+  const size_t ub = unit_smem_bytes(L.NK, L.Pmax, L.CI);
+  volatile int* status = (volatile int*)(dsm + ub);  // [P][KM]: 0 pending, 1 done, 2 failed
+  volatile int64_t* endv = (volatile int64_t*)(dsm + ub + (((size_t)L.Pmax * L.KM * 4 + 15) & ~size_t(15)));
+  volatile int* stop = &stop_at;
+  auto slot = [&](int k, int st) { return pd.slot_base + ((int64_t)k * pd.rp + a) * P + st; };
+  if (s == 0) build_seq(c, pd, M, U);
+  for (int i = threadIdx.x; i < P * L.KM; i += blockDim.x) status[i] = 0;
+  if (threadIdx.x == 0) stop_at = pd.kmax;
+  const int64_t* snap = M ? c.snap + slot(kf, 0) * icap : nullptr;
+  const int* snap_hw = (M && kf > 0) ? c.snap_hw + slot(kf, 0) * 2 : nullptr;
+  if (active) {
+    if (lane < 2) U.hw[2 * s + lane] = 0;
+    for (int r = 0; r < 2; ++r) {
+      VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, M ? snap + (int64_t)s * icap + (r ? c.icapc : 0) : nullptr,
+                             snap_hw ? snap_hw[2 * s + r] : 0, 0);
+      build_ci(V, U.ci + (2 * s + r) * U.CI, U.CI);
+    }
   }
-  __syncwarp();
-  int k = 0;
-  for (; k < pd.kmax; ++k) {
-    int64_t EF;
-    if (!place_chain(c, Row{P, pd.ti, a}, V, true, EF)) break;
-    if (lane == 0) c.tables[pd.inbB + ((int64_t)a * (pd.kmax + 1) + kf) * pd.kmax + k] = EF;
+  __syncthreads();
+  if (active) {
+    const UnitCtx X{P, a, (M ? c.bfill : c.snap) + slot(M ? kf : 0, 0) * icap, snap, snap_hw};
+    const int64_t T_end = c.scal[1];
+    const int q = a * P + s;
+    const int64_t ws = M ? T_end - c.z[q] : c.w[q];
+    for (int k = 0; k < pd.kmax; ++k) {
+      if (k >= *stop) break;
+      int64_t ready = ws;
+      if (s > 0) {  // wait for chain k of the upstream stage
+        int st;
+        bool quit = false;
+        while ((st = status[(s - 1) * L.KM + k]) == 0) {
+          if (k >= *stop) { quit = true; break; }
+          __nanosleep(20);
+        }
+        if (quit || st == 2) break;
+        ready = max(endv[(s - 1) * L.KM + k] + c.enc_p2p, ws);
+      }
+      int64_t end;
+      if (!place_stage<M>(c, pd, X, U, s, ready, &end)) {
+        if (lane == 0) {
+          atomicMin(&stop_at, k);
+          status[s * L.KM + k] = 2;
+        }
+        break;
+      }
+      if (!M) {  // snapshot this stage after k+1 chains
+        for (int r = 0; r < 2; ++r) {
+          const int h = U.hw[2 * s + r];
+          const int64_t* src = X.fill + (int64_t)s * icap + (r ? c.icapc : 0);
+          int64_t* dst = c.snap + slot(k + 1, s) * icap + (r ? c.icapc : 0);
+          for (int i = lane; i < h; i += 32) dst[i] = src[i];
+          if (lane == 0) c.snap_hw[slot(k + 1, s) * 2 + r] = h;
+        }
+      }
+      if (lane == 0) {
+        endv[s * L.KM + k] = end;
+        __threadfence_block();
+        status[s * L.KM + k] = 1;
+        if (s == P - 1) {
+          if (M) c.tables[pd.inbB + ((int64_t)a * (pd.kmax + 1) + kf) * pd.kmax + k] = end;
+          else c.tables[pd.inbF + (int64_t)a * pd.kmax + k] = end;
+        }
+      }
+      __syncwarp();
+    }
   }
-  if (lane == 0) c.tables[pd.lenB + (int64_t)a * (pd.kmax + 1) + kf] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // chains completed by every stage
+    int k = 0;
+    while (k < pd.kmax && status[(P - 1) * L.KM + k] == 1) ++k;
+    if (M) c.tables[pd.lenB + (int64_t)a * (pd.kmax + 1) + kf] = k;
+    else c.tables[pd.lenF + a] = k;
+  }
 }
 
 }  // namespace
@@ -341,8 +434,18 @@ cudaError_t launch_plan_tables(const Cfg& c, cudaStream_t st, int* launches) {
 
 cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st,
                                 int* launches) {
-  if (fwd_units > 0) k1_forward<<<(unsigned)((fwd_units + kK1Warps - 1) / kK1Warps), kK1Warps * 32, 0, st>>>(c, fwd_units);
-  if (bwd_units > 0) k1_backward<<<(unsigned)((bwd_units + kK1Warps - 1) / kK1Warps), kK1Warps * 32, 0, st>>>(c, bwd_units);
+  K1Launch L;
+  L.NK = c.nk_max;
+  L.Pmax = c.p;
+  L.CI = (std::max(c.icapc, c.icapm) + 31) / 32;
+  L.KM = std::max(1, c.kmax_all);
+  const size_t smem = k1_smem_bytes(L);
+  if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
+  cudaFuncSetAttribute(k1_chains<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k1_chains<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // one block per unit, one warp per stage of the widest plan
+  if (fwd_units > 0) k1_chains<false><<<(unsigned)fwd_units, 32 * c.p, smem, st>>>(c, fwd_units, L);
+  if (bwd_units > 0) k1_chains<true><<<(unsigned)bwd_units, 32 * c.p, smem, st>>>(c, bwd_units, L);
   if (launches) *launches += (fwd_units > 0) + (bwd_units > 0);
   return cudaGetLastError();
 }

@@ -37,6 +37,8 @@ __device__ __forceinline__ unsigned lanemask_gt(int k) { return ~lanemask_le(k);
 
 struct PlanCache {
   int e, P, rt, m, kmax;
+  int aj;         // lane j: its PP row a = j div r_t (R7)
+  bool strict;    // PRE_EF strictly increasing (pre entries order by (t, j))
   uint64_t first, count;
   const int64_t* devF;
   const int64_t* devB;
@@ -67,6 +69,9 @@ __device__ void load_plan(const Cfg& c, int e, PlanCache& pc) {
   const int t = min(lane + 1, n);
   pc.preEF = c.tables[pd.preF + (int64_t)(pd.P - 1) * (n + 1) + t];
   pc.preBEF = c.tables[pd.preB + (int64_t)(pd.P - 1) * (n + 1) + t];
+  pc.aj = lane / pd.rt;
+  const int64_t prev = __shfl_up_sync(FULL, pc.preEF, 1);
+  pc.strict = __all_sync(FULL, lane == 0 || lane >= n || pc.preEF > prev);
 }
 
 __device__ int find_plan(const Cfg& c, uint64_t g) {
@@ -117,68 +122,75 @@ __device__ bool next_composition(int m, int& N) {
   return true;
 }
 
-// Forward dependency shift (R10) for the current H (lane t-1: H(t)), Qc.
-__device__ __forceinline__ int64_t dep_fwd(int n, int H, int Qc, int sumc, int64_t G, int64_t preEF) {
+// Level-boundary mask of the pre multiset: level t (lane t-1 holds H(t) =
+// sum_j min(c_j, t) and cnt = #{j : c_j >= t}) occupies the 0-based sorted
+// positions [H(t-1), H(t)); the levels 1..max c are all non-empty.
+__device__ __forceinline__ unsigned level_mask(int H, int cnt) {
+  return __reduce_or_sync(FULL, cnt > 0 ? 1u << (H - cnt) : 0u);
+}
+
+// Forward dependency shift (R10): need_i = i - #{moved EF <= G_i}; INF if
+// need_i > sum c; else max over need_i > 0 of PRE_EF(t_i) - G_i, with t_i
+// the level holding sorted position need_i - 1.
+__device__ __forceinline__ int64_t dep_fwd(int n, unsigned B, int Qc, int sumc, int64_t G, int64_t preEF) {
   const int lane = threadIdx.x & 31;
   const int need = lane + 1 - Qc;
-  // t = min{t : H(t) >= need}: binary search over lanes
-  int pos = 0;
-#pragma unroll
-  for (int step = 16; step > 0; step >>= 1) {
-    const int h = __shfl_sync(FULL, H, pos + step - 1);
-    if (pos + step <= n && h < need) pos += step;
-  }
-  const int64_t pe = __shfl_sync(FULL, preEF, pos);  // PRE_EF(pos+1)
-  const bool act = lane < n && need > 0;
-  const bool inf = lane < n && need > sumc;
-  if (__any_sync(FULL, inf)) return kInf;
-  return warp_max64(act ? pe - G : kNegInf);
+  if (__any_sync(FULL, lane < n && need > sumc)) return kInf;
+  const int t = __popc(B & lanemask_le(max(need - 1, 0)));
+  const int64_t pe = __shfl_sync(FULL, preEF, max(t - 1, 0));  // PRE_EF(t)
+  return warp_max64(lane < n && need > 0 ? pe - G : kNegInf);
 }
 
 // Backward dependency shift (R15): slot i with owner o, rank r within o.
 __device__ __forceinline__ int64_t dep_bwd(int n, int r, int Qcb, int cbo, int64_t D, int64_t preBEF) {
   const int lane = threadIdx.x & 31;
   const int need = r - Qcb;
+  if (__any_sync(FULL, lane < n && need > cbo)) return kInf;
   const int64_t pe = __shfl_sync(FULL, preBEF, max(need, 1) - 1);  // PREB_EF(need)
-  const bool inf = lane < n && need > cbo;
-  if (__any_sync(FULL, inf)) return kInf;
   return warp_max64(lane < n && need > 0 ? pe - D : kNegInf);
 }
 
+// Per-warp work counters (warp-uniform), flushed with one atomic per warp.
+struct Stats {
+  unsigned long long cand, ops, itf, atf, itb, atb;
+};
+
 // One candidate: returns lat (uniform across the warp).
-__device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G, int64_t D, int64_t T_end) {
+__device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G, int64_t D, int64_t T_end,
+                            Stats& st) {
+  __shared__ int hist_sm[kEvalThreads / 32][kMaxN + 2];
   const int lane = threadIdx.x & 31;
-  const int n = c.n, m = pc.m, rt = pc.rt, kmax = pc.kmax, np1 = n + 1;
+  const int n = c.n, m = pc.m, kmax = pc.kmax, np1 = n + 1;
   const bool isp = lane < m;
-  const int aj = lane / rt;
+  const int aj = pc.aj;
+  int* sm = hist_sm[threadIdx.x >> 5];
 
   // ---------------- coarse init + forward OptimizeSchedule -------------
   int cj = isp ? Nj : 0, kf = 0;
   int64_t dv = isp ? __ldg(&pc.devF[aj * np1 + cj]) : kNegInf;
-  // H(t) = sum_j min(c_j, t) from the histogram of c_j
-  __shared__ int hist_sm[kEvalThreads / 32][kMaxN + 2];
-  int* hist = hist_sm[threadIdx.x >> 5];
-  hist[lane] = 0;
-  if (lane < 2) hist[32 + lane] = 0;
+  // cnt(t) = #{j : c_j >= t} and H(t) = sum_j min(c_j, t), lane t-1
+  sm[lane] = 0;
+  if (lane < 2) sm[32 + lane] = 0;
   __syncwarp();
-  if (isp) atomicAdd(&hist[cj], 1);
+  if (isp) atomicAdd(&sm[cj], 1);
   __syncwarp();
-  // cnt_ge(t) = #{j : c_j >= t} for t = lane+1 (suffix sum of hist over u >= t)
-  int suf = hist[lane + 1];
+  int cnt = sm[lane + 1];
   for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_down_sync(FULL, suf, o);
-    if (lane + o < 32) suf += y;
+    const int y = __shfl_down_sync(FULL, cnt, o);
+    if (lane + o < 32) cnt += y;
   }
-  // suf at lane t-1 = #{j: c_j >= t} for t in 1..32 (c_j <= n <= 32)
-  int H = suf;
+  int H = cnt;
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(FULL, H, o);
     if (lane >= o) H += y;
   }
+  unsigned B = level_mask(H, cnt);
   int sumc = n, Qc = 0;
-  int64_t dep = dep_fwd(n, H, Qc, sumc, G, pc.preEF);
+  int64_t dep = dep_fwd(n, B, Qc, sumc, G, pc.preEF);
   int64_t Delta;
+  int itf = 0, atf = 0, itb = 0, atb = 0;
   for (;;) {
+    ++itf;
     const bool valid = isp && cj > 0;
     const int64_t dvv = valid ? dv : kNegInf;
     const int64_t dev = warp_max64(dvv);
@@ -186,14 +198,19 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
     if (Delta == 0 || sumc == 0) break;
     const int js = __ffs(__ballot_sync(FULL, valid && dvv == dev)) - 1;  // findCritical, ties -> lowest j (R11)
     const int kfj = __shfl_sync(FULL, kf, js), cjs = __shfl_sync(FULL, cj, js);
-    const int as = js / rt;
-    if (kfj >= (int)__ldg(&pc.lenF[as])) break;         // ScheduleKernels fails (R12)
+    const int as = __shfl_sync(FULL, aj, js);
+    if (kfj >= (int)__ldg(&pc.lenF[as])) break;  // ScheduleKernels fails (R12)
     const int64_t EF = __ldg(&pc.inbF[as * kmax + kfj]);
+    ++atf;
     const int H2 = H - (lane + 1 >= cjs ? 1 : 0);
+    const int cnt2 = cnt - (lane + 1 == cjs ? 1 : 0);
+    const unsigned B2 = level_mask(H2, cnt2);
     const int Qc2 = Qc + (EF <= G ? 1 : 0);
-    const int64_t dep2 = dep_fwd(n, H2, Qc2, sumc - 1, G, pc.preEF);
-    if (dep2 > Delta) break;                             // checkEncLLMDep (R13)
+    const int64_t dep2 = dep_fwd(n, B2, Qc2, sumc - 1, G, pc.preEF);
+    if (dep2 > Delta) break;  // checkEncLLMDep (R13)
     H = H2;
+    cnt = cnt2;
+    B = B2;
     Qc = Qc2;
     dep = dep2;
     --sumc;
@@ -206,46 +223,65 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
   const int64_t Df = Delta;
 
   // ---------------- global ordering (R14) -------------------------------
-  int incl = isp ? Nj : 0;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int off = incl - (isp ? Nj : 0);
-  const unsigned segs = __reduce_or_sync(FULL, isp ? (1u << off) : 0u);
-  int64_t key = INT64_MAX;
-  {
-    const int j = __popc(segs & lanemask_le(lane)) - 1;
-    const int jj = max(j, 0);
-    const int offj = __shfl_sync(FULL, off, jj);
-    const int cjj = __shfl_sync(FULL, cj, jj);
-    const int local = lane - offj;
-    const int64_t pre = __shfl_sync(FULL, pc.preEF, max(local, 0) % 32);  // PRE_EF(local+1)
-    if (lane < n) {
-      const int64_t val = local < cjj ? pre - Df : __ldg(&pc.inbF[(jj / rt) * kmax + (local - cjj)]);
-      key = val * 65536 + (int64_t)(jj << 8) + local;
+  // owner[i] and r[i] = rank of slot i's deadline within its owner's sorted
+  // deadlines = #{later slots of the same owner} + 1
+  int owner, r;
+  if (sumc == n && pc.strict) {
+    // no chain moved: entries are the pre levels, ordered by (t, j)
+    const int maxc = __reduce_max_sync(FULL, cj);
+    for (int t = 1; t <= maxc; ++t) {
+      const unsigned mk = __ballot_sync(FULL, isp && cj >= t);
+      const int Hp = t == 1 ? 0 : __shfl_sync(FULL, H, t - 2);
+      if (isp && cj >= t) sm[Hp + __popc(mk & (lane ? (0xffffffffu >> (32 - lane)) : 0u))] = lane | ((cj - t + 1) << 8);
     }
-  }
-  // bitonic sort of the 32 keys, ascending
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const int64_t other = __shfl_xor_sync(FULL, key, j);
-      const bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
-      key = keep_min ? min(key, other) : max(key, other);
+    __syncwarp();
+    const int vv = sm[lane];
+    __syncwarp();
+    owner = lane < n ? (vv & 0xff) : 64 + lane;
+    r = vv >> 8;
+  } else {
+    int incl = isp ? Nj : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
     }
-  const int owner = lane < n ? (int)((key >> 8) & 0xff) : 64 + lane;
+    const int off = incl - (isp ? Nj : 0);
+    const unsigned segs = __reduce_or_sync(FULL, isp ? (1u << off) : 0u);
+    int64_t key = INT64_MAX;
+    {
+      const int jj = max(__popc(segs & lanemask_le(lane)) - 1, 0);
+      const int offj = __shfl_sync(FULL, off, jj);
+      const int cjj = __shfl_sync(FULL, cj, jj);
+      const int ajj = __shfl_sync(FULL, aj, jj);
+      const int local = lane - offj;
+      const int64_t pre = __shfl_sync(FULL, pc.preEF, max(local, 0) & 31);  // PRE_EF(local+1)
+      if (lane < n) {
+        const int64_t val = local < cjj ? pre - Df : __ldg(&pc.inbF[ajj * kmax + (local - cjj)]);
+        key = val * 65536 + (int64_t)(jj << 8) + local;
+      }
+    }
+    // bitonic sort of the 32 keys, ascending
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const int64_t other = __shfl_xor_sync(FULL, key, j);
+        const bool up = ((lane & j) == 0) == ((lane & k) == 0);  // keep the smaller key
+        if ((other < key) == up) key = other;
+      }
+    owner = lane < n ? (int)((key >> 8) & 0xff) : 64 + lane;
+    const unsigned same = __match_any_sync(FULL, owner);
+    r = __popc(same & lanemask_gt(lane)) + 1;
+  }
 
   // ---------------- backward OptimizeSchedule (R15) ----------------------
-  const unsigned same = __match_any_sync(FULL, owner);
-  const int r = __popc(same & lanemask_gt(lane)) + 1;  // rank of D_i within its owner
   int cb = isp ? Nj : 0, kb = 0;
   int64_t dvb = isp ? __ldg(&pc.devB[aj * np1 + cb]) : kNegInf;
   int Qcb = 0, sumcb = n;
   int cbo = __shfl_sync(FULL, cb, owner & 31);
   int64_t depb = dep_bwd(n, r, Qcb, cbo, D, pc.preBEF);
   for (;;) {
+    ++itb;
     const bool valid = isp && cb > 0;
     const int64_t dvv = valid ? dvb : kNegInf;
     const int64_t dev = warp_max64(dvv);
@@ -253,10 +289,11 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
     if (Delta == 0 || sumcb == 0) break;
     const int js = __ffs(__ballot_sync(FULL, valid && dvv == dev)) - 1;
     const int kfj = __shfl_sync(FULL, kf, js), kbj = __shfl_sync(FULL, kb, js);
-    const int as = js / rt;
+    const int as = __shfl_sync(FULL, aj, js);
     const int64_t rowoff = (int64_t)as * (kmax + 1) + kfj;
     if (kbj >= (int)__ldg(&pc.lenB[rowoff])) break;
     const int64_t EFb = __ldg(&pc.inbB[rowoff * kmax + kbj]);
+    ++atb;
     const bool mine = owner == js;
     const int Qcb2 = Qcb + (mine && EFb <= D ? 1 : 0);
     const int cbo2 = cbo - (mine ? 1 : 0);
@@ -272,6 +309,18 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
       dvb = cb > 0 ? __ldg(&pc.devB[aj * np1 + cb]) : kNegInf;
     }
   }
+  // algorithmic work of this candidate in 32-bit integer lane-ops (int64 add,
+  // compare, max count 2): DESIGN.md §5 defines each term.
+  const int lg = 32 - __clz(max(n - 1, 1));
+  st.cand += 1;
+  st.ops += (unsigned long long)(2 * n + 2 * m) + (unsigned long long)itf * (2 * m + 4) +
+            (unsigned long long)(1 + atf) * 6 * n + (unsigned long long)atf * (4 * n + 4) + 2 * n + 2 * n * lg + n +
+            (unsigned long long)itb * (2 * m + 4) + (unsigned long long)(1 + atb) * 6 * n +
+            (unsigned long long)atb * (3 * n + 4) + 4;
+  st.itf += itf;
+  st.atf += atf;
+  st.itb += itb;
+  st.atb += atb;
   return T_end + Df + Delta;  // R16
 }
 
@@ -290,6 +339,7 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
   uint64_t bg = UINT64_MAX;
   PlanCache pc;
   pc.e = -1;
+  Stats st = {0, 0, 0, 0, 0, 0};
   const uint64_t nchunks = (A.count + kChunk - 1) / kChunk;
   for (;;) {
     unsigned long long ch = 0;
@@ -304,7 +354,7 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
         if (e < 0) continue;
         if (e != pc.e) load_plan(c, e, pc);
         const int Nj = unrank_lane(c, n, pc.m, g - pc.first);
-        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end);
+        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end, st);
         if (A.lat_out && lane == 0) A.lat_out[i] = lat;
         better(lat, g, bl, bg);
       }
@@ -319,7 +369,7 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
       if (e != pc.e) load_plan(c, e, pc);
       int Nj = unrank_lane(c, n, pc.m, g - pc.first);
       for (;;) {
-        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end);
+        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end, st);
         if (A.lat_out && lane == 0) A.lat_out[g - A.begin] = lat;
         better(lat, g, bl, bg);
         if (++g >= gend) break;
@@ -332,6 +382,14 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
         }
       }
     }
+  }
+  if (lane == 0 && A.stats) {
+    atomicAdd(&A.stats[0], st.cand);
+    atomicAdd(&A.stats[1], st.ops);
+    atomicAdd(&A.stats[2], st.itf);
+    atomicAdd(&A.stats[3], st.atf);
+    atomicAdd(&A.stats[4], st.itb);
+    atomicAdd(&A.stats[5], st.atb);
   }
   // block argmin -> partials
   __shared__ long long bl_sm[kEvalThreads / 32];
@@ -382,8 +440,10 @@ int eval_grid(int sms) {
 }
 
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches) {
+  if (a.ev0) cudaEventRecord(a.ev0, st);
   if (a.index) k2_eval<true><<<a.grid, kEvalThreads, 0, st>>>(c, a);
   else k2_eval<false><<<a.grid, kEvalThreads, 0, st>>>(c, a);
+  if (a.ev1) cudaEventRecord(a.ev1, st);
   k3_reduce<<<1, 256, 0, st>>>(a);
   if (launches) *launches += 2;
   return cudaGetLastError();

@@ -31,6 +31,7 @@ struct Cfg {
   int32_t nops;          // 2*n*v ops per stage
   int32_t icapc, icapm;  // interval capacity per stage: compute-free, comm-free
   int32_t kmax_all;      // max kmax over plans
+  int32_t nk_max;        // max over TP options of the encoder's total kernel count (all layers, all branches)
   int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
   // packed inputs
   const int32_t* lkind;   // kernel kinds, all lists concatenated
@@ -52,7 +53,7 @@ struct Cfg {
   int64_t* comp_hi;       // [p][icapc] compute-free interval ends
   int64_t* comm_lo;       // [p][icapm]
   int64_t* comm_hi;       // [p][icapm]
-  int64_t* sim;           // [kSimWarps][p*2*v*n] K0 scratch
+  int32_t* bestw;         // [p] K0 warm-up search: smallest successful w per stage
   // plans + tables (K1)
   const PlanDesc* plans;  // [E]
   int64_t* tables;
@@ -105,6 +106,8 @@ struct EvalArgs {
   unsigned long long* counter;
   uint64_t total;
   int grid;
+  cudaEvent_t ev0, ev1;       // optional: recorded around K2 for per-kernel timing
+  unsigned long long* stats;  // [6] cumulative: candidates, algorithmic ops, fwd iters, fwd attempts, bwd iters, bwd attempts
 };
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
 }  // namespace optimus

@@ -16,6 +16,8 @@
 //   each compute kernel (compute-free interval) and after each comm kernel
 //   clipped to [w, z] (comm-free interval), and compact them in time order
 //   with a block scan.
+#include <algorithm>
+
 #include <cub/block/block_scan.cuh>
 
 #include "optimus_dev.cuh"
@@ -23,8 +25,9 @@
 namespace optimus {
 namespace {
 
-__device__ __forceinline__ int64_t ldv(const int64_t* p) { return *(volatile const int64_t*)p; }
-__device__ __forceinline__ void stv(int64_t* p, int64_t v) { *(volatile int64_t*)p = v; }
+// K0 dynamic shared memory (declared at namespace scope so that every access
+// compiles to LDS/STS, not to generic strong loads/stores)
+extern __shared__ __align__(16) unsigned char k0_dsm[];
 
 __device__ int64_t list_sum(const Cfg& c, int id) {
   int64_t s = 0;
@@ -37,127 +40,214 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
   return v;
 }
 
-// Simulate the interleaved 1F1B pipeline with per-stage warm-up counts W
-// (lane s reads W[s]).  done: this warp's scratch [p][2][v][n] of op end
-// times.  record: also write op starts, F, B.  Returns ok (deadlock-free)
-// and the span (max last-op end).
-__device__ void warp_simulate(const Cfg& c, const int* W, int64_t* done, bool record, int64_t dur_f,
-                              int64_t dur_b, int64_t* span, int* ok) {
+// K0 per-warp shared memory: [optab: p*nops int64][done: p*2*v*n int64].
+// optab[s][pos] packs the op at position pos of stage s for the warp's
+// current warm-up vector: bits 0-23 its own slot in done, 24-47 the slot of
+// its dependency (0xFFFFFF = none), 48 forward, 49 cross-stage dependency.
+constexpr uint64_t kNoDep = 0xFFFFFF;
+constexpr int kFinalWarps = 8;
+
+__host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int nops, int v, int n) {
+  return (size_t)p * nops * 8 + (size_t)p * 2 * v * n * 8;
+}
+
+// Fill the warp's optab for the warm-up vector W (lane-parallel).
+__device__ void build_optab(const Cfg& c, const int* W, size_t base) {
+  uint64_t* tab = reinterpret_cast<uint64_t*>(k0_dsm + base);
+  const int p = c.p, v = c.v, n = c.n, nops = c.nops;
+  for (int i = threadIdx.x & 31; i < p * nops; i += 32) {
+    const int s = i / nops, pos = i % nops;
+    const OpRef op = op_at(p, v, n, W[s], pos);  // Megatron interleaved order (R2)
+    int ds = -1, df = 0, dc = 0;                 // dependency (R2)
+    if (op.fwd) {
+      if (s > 0) { ds = s - 1; df = 1; dc = op.chunk; }
+      else if (op.chunk > 0) { ds = p - 1; df = 1; dc = op.chunk - 1; }
+    } else {
+      if (s < p - 1) { ds = s + 1; df = 0; dc = op.chunk; }
+      else if (op.chunk < v - 1) { ds = 0; df = 0; dc = op.chunk + 1; }
+      else { ds = p - 1; df = 1; dc = v - 1; }
+    }
+    const uint64_t self = ((s * 2 + op.fwd) * v + op.chunk) * n + op.mb;
+    const uint64_t dep = ds < 0 ? kNoDep : (uint64_t)(((ds * 2 + df) * v + dc) * n + op.mb);
+    tab[i] = self | (dep << 24) | ((uint64_t)op.fwd << 48) | ((uint64_t)(ds >= 0 && ds != s) << 49);
+  }
+  __syncwarp();
+}
+
+// ASAP list schedule of the pipeline in optab's fixed per-stage order (R2,
+// R3), one warp, lane = stage.  A trial stops as soon as an op ends after
+// span_limit.  record: also write op starts, F, B.  Returns ok
+// (deadlock-free and within the limit) and the span (max last-op end).
+__device__ void warp_simulate(const Cfg& c, size_t base, bool record, int64_t dur_f, int64_t dur_b,
+                              int64_t span_limit, int64_t* span, int* ok) {
+  const uint64_t* tab = reinterpret_cast<const uint64_t*>(k0_dsm + base);
+  volatile int64_t* done = reinterpret_cast<volatile int64_t*>(k0_dsm + base + (size_t)c.p * c.nops * 8);
   const int lane = threadIdx.x & 31;
   const int p = c.p, v = c.v, n = c.n, nops = c.nops;
   const int sz = p * 2 * v * n;
-  for (int i = lane; i < sz; i += 32) stv(&done[i], -1);
+  for (int i = lane; i < sz; i += 32) done[i] = -1;
   __syncwarp();
-  auto idx = [&](int s, int f, int ch, int mb) { return ((s * 2 + f) * v + ch) * n + mb; };
   int pos = 0;
-  int64_t fr = 0;
-  const int Ws = lane < p ? W[lane] : 0;
+  int64_t fr = max((int64_t)0, c.T_ag);  // every op starts after the DP all-gather (R3)
+  const int64_t pp2p = c.pp_p2p;
+  bool over = false;
+  const uint64_t* row = tab + (size_t)min(lane, p - 1) * nops;
   for (;;) {
     bool prog = false;
     if (lane < p) {
       while (pos < nops) {
-        OpRef op = op_at(p, v, n, Ws, pos);
-        int ds = -1, df = 0, dc = 0;  // dependency (R2)
-        if (op.fwd) {
-          if (lane > 0) { ds = lane - 1; df = 1; dc = op.chunk; }
-          else if (op.chunk > 0) { ds = p - 1; df = 1; dc = op.chunk - 1; }
-        } else {
-          if (lane < p - 1) { ds = lane + 1; df = 0; dc = op.chunk; }
-          else if (op.chunk < v - 1) { ds = 0; df = 0; dc = op.chunk + 1; }
-          else { ds = p - 1; df = 1; dc = v - 1; }
+        const uint64_t e = row[pos];
+        const int dep = (int)((e >> 24) & kNoDep);
+        int64_t t = fr;
+        if (dep != (int)kNoDep) {
+          const int64_t de = done[dep];
+          if (de < 0) break;
+          t = max(t, de + ((e >> 49) & 1 ? pp2p : 0));
         }
-        int64_t t = max(fr, c.T_ag);  // every op starts after the DP all-gather (R3)
-        if (ds >= 0) {
-          int64_t e = ldv(&done[idx(ds, df, dc, op.mb)]);
-          if (e < 0) break;
-          t = max(t, e + (ds != lane ? c.pp_p2p : 0));
-        }
-        const int64_t d = op.fwd ? dur_f : dur_b;
-        stv(&done[idx(lane, op.fwd, op.chunk, op.mb)], t + d);
+        const bool fwd = (e >> 48) & 1;
+        const int64_t fin = t + (fwd ? dur_f : dur_b);
+        if (fin > span_limit) { over = true; break; }
+        const int self = (int)(e & kNoDep);
+        done[self] = fin;
         if (record) {
           c.opstart[(int64_t)lane * nops + pos] = t;
-          if (lane == 0 && op.chunk == 0) {
-            if (op.fwd) c.F[op.mb] = t;       // F_i: start of F(stage 0, chunk 0, i) (R4)
-            else c.B[op.mb] = t + d;          // B_i: end of B(stage 0, chunk 0, i)
+          const int mb = self % n, ch = (self / n) % v;
+          if (lane == 0 && ch == 0) {
+            if (fwd) c.F[mb] = t;    // F_i: start of F(stage 0, chunk 0, i) (R4)
+            else c.B[mb] = fin;      // B_i: end of B(stage 0, chunk 0, i)
           }
         }
-        fr = t + d;
+        fr = fin;
         ++pos;
         prog = true;
       }
     }
     __syncwarp();
-    if (!__any_sync(0xffffffffu, prog)) break;
+    if (__any_sync(0xffffffffu, over) || !__any_sync(0xffffffffu, prog)) break;
   }
-  *ok = __all_sync(0xffffffffu, lane >= p || pos == nops);
+  *ok = __all_sync(0xffffffffu, lane >= p || pos == nops) && !__any_sync(0xffffffffu, over);
   *span = warp_max64(lane < p ? fr : 0);
 }
 
-__global__ void __launch_bounds__(kSimWarps * 32) k0_template(Cfg c) {
-  __shared__ int Wsm[kSimWarps][kMaxP];
+__device__ __forceinline__ int default_w(int p, int v, int n, int s) {  // Megatron default warm-up (R2)
+  if (v == 1) return min(n, p - 1 - s);
+  if (n == p) return n * v;
+  return min(n * v, 2 * (p - 1 - s) + (v - 1) * p);
+}
+
+// Speculative guess for the adjusted warm-up of stage s (only used to run
+// the stage phases of R5 in parallel; every guess is verified).
+__device__ __forceinline__ int guess_w(int p, int v, int n, int s) {
+  return v == 1 ? default_w(p, v, n, s) : min(n * v, (v - 1) * p + (p - 1 - s));
+}
+
+__device__ __forceinline__ void dur_fb(const Cfg& c, int64_t& f, int64_t& b) {
+  f = (int64_t)c.lc * list_sum(c, 0);
+  b = (int64_t)c.lc * list_sum(c, 1);
+}
+
+// K0a: default warm-up, default schedule (span to preserve), reset of the search.
+__global__ void __launch_bounds__(32) k0_default(Cfg c) {
+  __shared__ int Wsm[kMaxP];
+  const int lane = threadIdx.x;
+  int64_t df, db;
+  dur_fb(c, df, db);
+  if (lane < c.p) {
+    const int w = default_w(c.p, c.v, c.n, lane);
+    c.Wdef[lane] = w;
+    c.W[lane] = w;
+    c.bestw[lane] = INT32_MAX;
+    Wsm[lane] = w;
+  }
+  __syncwarp();
+  build_optab(c, Wsm, 0);
+  int64_t sp;
+  int ok;
+  warp_simulate(c, 0, false, df, db, INT64_MAX, &sp, &ok);
+  if (lane == 0) { c.scal[0] = sp; c.scal[2] = ok; }
+}
+
+// K0b: GetEncLLMDep's warm-up adjustment (R5) is, for s = p-1 .. 0,
+// the smallest w in [0, Wdef_s] keeping the schedule deadlock-free with the
+// default span.  All stage phases run here at once, one trial (s, w) per
+// block, each assuming the later stages take their guessed value; K0c
+// verifies (a stage's result is exact when every later guess was right).
+__global__ void __launch_bounds__(32) k0_wave(Cfg c) {
+  __shared__ int Wsm[kMaxP];
+  const int lane = threadIdx.x, p = c.p, v = c.v, n = c.n;
+  if (c.policy != 1 || c.scal[2] == 0) return;
+  int s = 0, w = blockIdx.x;
+  while (s < p && w > default_w(p, v, n, s)) { w -= default_w(p, v, n, s) + 1; ++s; }
+  if (s >= p) return;
+  int64_t df, db;
+  dur_fb(c, df, db);
+  if (lane < p) Wsm[lane] = lane < s ? default_w(p, v, n, lane) : lane == s ? w : guess_w(p, v, n, lane);
+  __syncwarp();
+  build_optab(c, Wsm, 0);
+  int64_t sp;
+  int ok;
+  warp_simulate(c, 0, false, df, db, c.scal[0], &sp, &ok);
+  if (lane == 0 && ok && sp == c.scal[0]) atomicMin(&c.bestw[s], w);
+}
+
+// K0c: verify the wave from the last stage down, redo the phases below the
+// first wrong guess exactly (kFinalWarps trials at a time), then the final
+// schedule with its op starts, F_i, B_i and T_end.
+__global__ void __launch_bounds__(kFinalWarps * 32) k0_final(Cfg c) {
   __shared__ int Wcur[kMaxP];
-  __shared__ int Wd[kMaxP];
-  __shared__ long long span_def;
-  __shared__ int ok_def, best_w;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int p = c.p, v = c.v, n = c.n;
-  const int64_t dur_f = (int64_t)c.lc * list_sum(c, 0);
-  const int64_t dur_b = (int64_t)c.lc * list_sum(c, 1);
-  int64_t* scratch = c.sim + (int64_t)warp * p * 2 * v * n;
-  if (threadIdx.x < p) {  // Megatron default warm-up (R2)
-    int s = threadIdx.x, w;
-    if (v == 1) w = min(n, p - 1 - s);
-    else if (n == p) w = n * v;
-    else w = min(n * v, 2 * (p - 1 - s) + (v - 1) * p);
-    Wd[s] = w;
-    Wcur[s] = w;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    int64_t sp;
-    int ok;
-    warp_simulate(c, Wd, scratch, false, dur_f, dur_b, &sp, &ok);
-    if (lane == 0) { span_def = sp; ok_def = ok; }
-  }
-  __syncthreads();
-  if (!ok_def) {
-    if (threadIdx.x == 0) c.scal[2] = 0;
-    return;
-  }
+  __shared__ int Wsm[kFinalWarps][kMaxP];
+  __shared__ int best_sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, p = c.p, v = c.v, n = c.n;
+  const int nwarps = blockDim.x >> 5;
+  if (c.scal[2] == 0) return;  // default schedule deadlocks: template fails
+  const size_t base = (size_t)warp * k0_warp_bytes(p, c.nops, v, n);
+  int64_t df, db;
+  dur_fb(c, df, db);
+  const int64_t span_def = c.scal[0];
+  int s0 = -1;
   if (c.policy == 1) {
-    // R5: for s = p-1 .. 0, the smallest w in [0, Wdef_s] keeping the
-    // schedule deadlock-free with the default span
-    for (int s = p - 1; s >= 0; --s) {
-      for (int base = 0; base <= Wd[s]; base += kSimWarps) {
-        if (threadIdx.x == 0) best_w = INT32_MAX;
-        const int w = base + warp;
-        if (lane < p) Wsm[warp][lane] = (lane == s) ? w : Wcur[lane];
+    int s = p - 1;
+    while (s >= 0 && c.bestw[s] == guess_w(p, v, n, s)) --s;
+    s0 = s;  // stages > s0 verified; stage s0 exact (its later stages were right)
+  }
+  if (threadIdx.x < p) {
+    const int t = threadIdx.x;
+    Wcur[t] = c.policy != 1 ? default_w(p, v, n, t)
+                            : t > s0 ? guess_w(p, v, n, t) : t == s0 ? c.bestw[t] : default_w(p, v, n, t);
+  }
+  __syncthreads();
+  for (int s = s0 - 1; s >= 0; --s) {  // exact sequential phases (rarely needed)
+    const int wd = default_w(p, v, n, s);
+    for (int b = 0; b <= wd; b += nwarps) {
+      if (threadIdx.x == 0) best_sm = INT32_MAX;
+      __syncthreads();
+      const int w = b + warp;
+      if (w <= wd) {
+        if (lane < p) Wsm[warp][lane] = lane == s ? w : Wcur[lane];
+        __syncwarp();
+        build_optab(c, Wsm[warp], base);
+        int64_t sp;
+        int ok;
+        warp_simulate(c, base, false, df, db, span_def, &sp, &ok);
+        if (lane == 0 && ok && sp == span_def) atomicMin(&best_sm, w);
+      }
+      __syncthreads();
+      const int bw = best_sm;
+      __syncthreads();
+      if (bw != INT32_MAX) {
+        if (threadIdx.x == 0) Wcur[s] = bw;
         __syncthreads();
-        if (w <= Wd[s]) {
-          int64_t sp;
-          int ok;
-          warp_simulate(c, Wsm[warp], scratch, false, dur_f, dur_b, &sp, &ok);
-          if (lane == 0 && ok && sp == span_def) atomicMin(&best_w, w);
-        }
-        __syncthreads();
-        const int bw = best_w;
-        __syncthreads();
-        if (bw != INT32_MAX) {
-          if (threadIdx.x == 0) Wcur[s] = bw;
-          __syncthreads();
-          break;
-        }
+        break;
       }
     }
   }
-  __syncthreads();
   if (warp == 0) {
+    build_optab(c, Wcur, 0);
     int64_t sp;
     int ok;
-    warp_simulate(c, Wcur, scratch, true, dur_f, dur_b, &sp, &ok);
-    if (lane < p) { c.W[lane] = Wcur[lane]; c.Wdef[lane] = Wd[lane]; }
+    warp_simulate(c, 0, true, df, db, INT64_MAX, &sp, &ok);
+    if (lane < p) c.W[lane] = Wcur[lane];
     if (lane == 0) {
-      c.scal[0] = span_def;
       c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
       c.scal[2] = ok;
     }
@@ -299,9 +389,22 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
 }  // namespace
 
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
-  k0_template<<<1, kSimWarps * 32, 0, st>>>(c);
+  const size_t per = k0_warp_bytes(c.p, c.nops, c.v, c.n);
+  if (per > 200 * 1024) return cudaErrorInvalidConfiguration;
+  const int fw = (int)std::max<size_t>(1, std::min<size_t>(kFinalWarps, (200 * 1024) / per));
+  cudaFuncSetAttribute(k0_default, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
+  cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
+  cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * fw));
+  int trials = 0;
+  for (int s = 0; s < c.p; ++s) {
+    const int p = c.p, v = c.v, n = c.n;
+    trials += (v == 1 ? std::min(n, p - 1 - s) : n == p ? n * v : std::min(n * v, 2 * (p - 1 - s) + (v - 1) * p)) + 1;
+  }
+  k0_default<<<1, 32, per, st>>>(c);
+  k0_wave<<<std::max(1, trials), 32, per, st>>>(c);
+  k0_final<<<1, 32 * fw, per * fw, st>>>(c);
   k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int), st>>>(c);
-  if (launches) *launches += 2;
+  if (launches) *launches += 4;
   return cudaGetLastError();
 }
 

@@ -21,8 +21,8 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_free",
-    "optimus_last_error",
+    "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_set_timing",
+    "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
 ]
 
 
@@ -86,6 +86,10 @@ def lib():
             "optimus_debug_template": [vp, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
+            "optimus_set_timing": [vp, ctypes.c_int],
+            "optimus_last_timing": [vp, P(ctypes.c_float), P(ctypes.c_float)],
+            "optimus_eval_stats": [vp, P(ctypes.c_uint64), vp],
+            "optimus_io_bytes": [vp, P(ctypes.c_uint64), P(ctypes.c_uint64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -275,6 +279,26 @@ class Ctx:
         b, e = ctypes.c_int32(), ctypes.c_int32()
         _check(lib().optimus_launch_count(self.h, ctypes.byref(b), ctypes.byref(e)))
         return b.value, e.value
+
+    def set_timing(self, on: bool = True):
+        _check(lib().optimus_set_timing(self.h, 1 if on else 0))
+
+    def last_timing(self):
+        """(build_ms, k2_ms) of the most recent build / K2 launch (events on the launch stream)."""
+        b, e = ctypes.c_float(), ctypes.c_float()
+        _check(lib().optimus_last_timing(self.h, ctypes.byref(b), ctypes.byref(e)))
+        return b.value, e.value
+
+    def eval_stats(self, stream=None) -> dict:
+        a = (ctypes.c_uint64 * 6)()
+        _check(lib().optimus_eval_stats(self.h, a, ctypes.c_void_p(_stream(stream))))
+        keys = ("candidates", "ops", "iters_f", "attempts_f", "iters_b", "attempts_b")
+        return dict(zip(keys, list(a)))
+
+    def io_bytes(self):
+        h, d = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().optimus_io_bytes(self.h, ctypes.byref(h), ctypes.byref(d)))
+        return h.value, d.value
 
     def free(self):
         if getattr(self, "h", None):
