@@ -171,6 +171,11 @@ int optimus_debug_plan_tables(const optimus_ctx* c, int32_t i, int64_t* h_out, s
 /* Kernel launches the last build / eval enqueued (for launch accounting). */
 int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t* eval_launches);
 
+/* K2 variant used by the eval calls: 1 (default) = one candidate per thread
+ * (eval_thread.cu), 0 = one candidate per warp (eval.cu).  Both compute the
+ * same lat for every candidate (bit-exact); they differ only in speed. */
+int optimus_set_eval_mode(optimus_ctx* c, int mode);
+
 /* Per-kernel timing: when on, the library records CUDA events around each
  * build (K0+K1 launches) and around the K2 evaluation kernel on the stream
  * it launches them on; optimus_last_timing waits for them and returns the

@@ -15,10 +15,6 @@
 #include "../../include/optimus.h"
 #include "optimus_dev.cuh"
 
-namespace optimus {
-int eval_grid(int sms);
-}
-
 using namespace optimus;
 
 namespace {
@@ -278,7 +274,8 @@ struct optimus_ctx {
   Cfg cfg;
   char* ws = nullptr;
   int sms = 0;
-  int grid = 0;
+  int grid = 0, grid_thread = 0;
+  int mode = 1;  // K2 variant: 1 = one candidate per thread (default), 0 = one per warp
   int build_launches = 0, eval_launches = 0;
   bool timing = false;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // build start/end, K2 start/end
@@ -372,6 +369,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = prop.multiProcessorCount;
   c->grid = std::min(4096, eval_grid(c->sms));
+  c->grid_thread = std::min(4096, eval_thread_grid(c->sms));
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
   cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -432,7 +430,8 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.partials = (int64_t*)(c->ws + c->X.o_partials);
   a.counter = (unsigned long long*)(c->ws + c->X.o_counter);
   a.total = c->X.total;
-  a.grid = c->grid;
+  a.mode = c->mode;
+  a.grid = c->mode == 1 ? c->grid_thread : c->grid;
   a.stats = (unsigned long long*)(c->ws + c->X.o_stats);
   a.ev0 = c->timing ? c->ev[2] : nullptr;
   a.ev1 = c->timing ? c->ev[3] : nullptr;
@@ -598,6 +597,12 @@ int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t*
   return OPTIMUS_OK;
 }
 
+int optimus_set_eval_mode(optimus_ctx* c, int mode) {
+  if (!c || (mode != 0 && mode != 1)) return fail(OPTIMUS_EINVAL, "mode must be 0 (warp per candidate) or 1 (thread per candidate)");
+  c->mode = mode;
+  return OPTIMUS_OK;
+}
+
 int optimus_set_timing(optimus_ctx* c, int on) {
   if (!c || !c->ws) return fail(OPTIMUS_EINVAL, "ctx is NULL or host-only");
   if (on && !c->ev[0])
@@ -622,7 +627,20 @@ int optimus_last_timing(const optimus_ctx* c, float* build_ms, float* eval_ms) {
 int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream) {
   if (!c || !c->ws || !h_out) return fail(OPTIMUS_EINVAL, "NULL argument or host-only ctx");
   CK(cudaStreamSynchronize((cudaStream_t)cuda_stream));
-  CK(cudaMemcpy(h_out, c->ws + c->X.o_stats, 6 * 8, cudaMemcpyDeviceToHost));
+  uint64_t v[8];
+  CK(cudaMemcpy(v, c->ws + c->X.o_stats, 8 * 8, cudaMemcpyDeviceToHost));
+  // algorithmic 32-bit lane-ops per candidate (int64 add/compare/max = 2):
+  // (17n + 4 + 2n lg) + 2m + 2 m it_f + 4 it_f + (10n+4) at_f + 2 m it_b + 4 it_b + (9n+4) at_b
+  const uint64_t n = (uint64_t)c->X.n;
+  uint64_t lg = 0;
+  while ((1ull << lg) < std::max<uint64_t>(n, 2)) ++lg;
+  h_out[0] = v[0];
+  h_out[1] = v[0] * (17 * n + 4 + 2 * n * lg) + 2 * v[1] + 2 * v[2] + 4 * v[3] + (10 * n + 4) * v[4] + 2 * v[5] +
+             4 * v[6] + (9 * n + 4) * v[7];
+  h_out[2] = v[3];
+  h_out[3] = v[4];
+  h_out[4] = v[6];
+  h_out[5] = v[7];
   return OPTIMUS_OK;
 }
 

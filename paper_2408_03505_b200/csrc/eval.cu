@@ -150,29 +150,34 @@ __device__ __forceinline__ int64_t dep_bwd(int n, int r, int Qcb, int cbo, int64
   return warp_max64(lane < n && need > 0 ? pe - D : kNegInf);
 }
 
-// Per-warp work counters (warp-uniform), flushed with one atomic per warp.
+// Per-warp work counters (warp-uniform), flushed with one atomic per warp:
+// candidates, sum m, sum m*iters_f, iters_f, attempts_f, sum m*iters_b,
+// iters_b, attempts_b.  The host turns them into algorithmic lane-ops
+// (optimus_eval_stats).
 struct Stats {
-  unsigned long long cand, ops, itf, atf, itb, atb;
+  unsigned v[8];
 };
 
-// One candidate: returns lat (uniform across the warp).
-__device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G, int64_t D, int64_t T_end,
-                            Stats& st) {
-  __shared__ int hist_sm[kEvalThreads / 32][kMaxN + 2];
-  const int lane = threadIdx.x & 31;
-  const int n = c.n, m = pc.m, kmax = pc.kmax, np1 = n + 1;
-  const bool isp = lane < m;
-  const int aj = pc.aj;
-  int* sm = hist_sm[threadIdx.x >> 5];
+// Base state of the current composition N, carried across lexicographic
+// successors: lane j: N_j and its DEV values; lane t-1: cnt(t) = #{j : N_j
+// >= t}, H(t) = sum_j min(N_j, t).
+struct Comp {
+  int N, cnt, H;
+  int64_t dvF, dvB;
+};
 
-  // ---------------- coarse init + forward OptimizeSchedule -------------
-  int cj = isp ? Nj : 0, kf = 0;
-  int64_t dv = isp ? __ldg(&pc.devF[aj * np1 + cj]) : kNegInf;
-  // cnt(t) = #{j : c_j >= t} and H(t) = sum_j min(c_j, t), lane t-1
+__device__ void comp_init(const Cfg& c, const PlanCache& pc, int N, Comp& s) {
+  __shared__ int hist_sm[kEvalThreads / 32][kMaxN + 2];
+  const int lane = threadIdx.x & 31, np1 = c.n + 1;
+  int* sm = hist_sm[threadIdx.x >> 5];
+  const bool isp = lane < pc.m;
+  s.N = isp ? N : 0;
+  s.dvF = isp ? __ldg(&pc.devF[pc.aj * np1 + N]) : kNegInf;
+  s.dvB = isp ? __ldg(&pc.devB[pc.aj * np1 + N]) : kNegInf;
   sm[lane] = 0;
   if (lane < 2) sm[32 + lane] = 0;
   __syncwarp();
-  if (isp) atomicAdd(&sm[cj], 1);
+  if (isp) atomicAdd(&sm[N], 1);
   __syncwarp();
   int cnt = sm[lane + 1];
   for (int o = 1; o < 32; o <<= 1) {
@@ -184,6 +189,49 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
     const int y = __shfl_up_sync(FULL, H, o);
     if (lane >= o) H += y;
   }
+  s.cnt = cnt;
+  s.H = H;
+  __syncwarp();
+}
+
+// Lexicographic successor with the base state kept up to date; the common
+// step (last part > 1) moves one microbatch from part m-1 to part m-2.
+__device__ bool comp_next(const Cfg& c, const PlanCache& pc, Comp& s) {
+  const int lane = threadIdx.x & 31, m = pc.m, np1 = c.n + 1;
+  if (m < 2) return false;
+  const int y = __shfl_sync(FULL, s.N, m - 1);
+  if (y > 1) {
+    const int x = __shfl_sync(FULL, s.N, m - 2);
+    s.cnt += (lane == x ? 1 : 0) - (lane == y - 1 ? 1 : 0);  // cnt(x+1) += 1, cnt(y) -= 1
+    s.H += (lane >= x ? 1 : 0) - (lane >= y - 1 ? 1 : 0);
+    if (lane == m - 2 || lane == m - 1) {
+      s.N += lane == m - 2 ? 1 : -1;
+      s.dvF = __ldg(&pc.devF[pc.aj * np1 + s.N]);
+      s.dvB = __ldg(&pc.devB[pc.aj * np1 + s.N]);
+    }
+    return true;
+  }
+  int N = s.N;
+  if (!next_composition(m, N)) return false;
+  comp_init(c, pc, N, s);
+  return true;
+}
+
+// One candidate: returns lat (uniform across the warp).
+__device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, const Comp& base, int64_t G, int64_t D, int64_t T_end,
+                            Stats& st) {
+  __shared__ int ord_sm[kEvalThreads / 32][kMaxN + 2];
+  const int lane = threadIdx.x & 31;
+  const int n = c.n, m = pc.m, kmax = pc.kmax, np1 = n + 1;
+  const bool isp = lane < m;
+  const int aj = pc.aj;
+  const int Nj = base.N;
+  int* sm = ord_sm[threadIdx.x >> 5];
+
+  // ---------------- coarse init + forward OptimizeSchedule -------------
+  int cj = Nj, kf = 0;
+  int64_t dv = base.dvF;
+  int cnt = base.cnt, H = base.H;
   unsigned B = level_mask(H, cnt);
   int sumc = n, Qc = 0;
   int64_t dep = dep_fwd(n, B, Qc, sumc, G, pc.preEF);
@@ -275,8 +323,8 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
   }
 
   // ---------------- backward OptimizeSchedule (R15) ----------------------
-  int cb = isp ? Nj : 0, kb = 0;
-  int64_t dvb = isp ? __ldg(&pc.devB[aj * np1 + cb]) : kNegInf;
+  int cb = Nj, kb = 0;
+  int64_t dvb = base.dvB;
   int Qcb = 0, sumcb = n;
   int cbo = __shfl_sync(FULL, cb, owner & 31);
   int64_t depb = dep_bwd(n, r, Qcb, cbo, D, pc.preBEF);
@@ -309,18 +357,14 @@ __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, int Nj, int64_t G
       dvb = cb > 0 ? __ldg(&pc.devB[aj * np1 + cb]) : kNegInf;
     }
   }
-  // algorithmic work of this candidate in 32-bit integer lane-ops (int64 add,
-  // compare, max count 2): DESIGN.md §5 defines each term.
-  const int lg = 32 - __clz(max(n - 1, 1));
-  st.cand += 1;
-  st.ops += (unsigned long long)(2 * n + 2 * m) + (unsigned long long)itf * (2 * m + 4) +
-            (unsigned long long)(1 + atf) * 6 * n + (unsigned long long)atf * (4 * n + 4) + 2 * n + 2 * n * lg + n +
-            (unsigned long long)itb * (2 * m + 4) + (unsigned long long)(1 + atb) * 6 * n +
-            (unsigned long long)atb * (3 * n + 4) + 4;
-  st.itf += itf;
-  st.atf += atf;
-  st.itb += itb;
-  st.atb += atb;
+  st.v[0] += 1;
+  st.v[1] += m;
+  st.v[2] += m * itf;
+  st.v[3] += itf;
+  st.v[4] += atf;
+  st.v[5] += m * itb;
+  st.v[6] += itb;
+  st.v[7] += atb;
   return T_end + Df + Delta;  // R16
 }
 
@@ -339,7 +383,8 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
   uint64_t bg = UINT64_MAX;
   PlanCache pc;
   pc.e = -1;
-  Stats st = {0, 0, 0, 0, 0, 0};
+  Stats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
+  Comp cs;
   const uint64_t nchunks = (A.count + kChunk - 1) / kChunk;
   for (;;) {
     unsigned long long ch = 0;
@@ -353,8 +398,8 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
         const int e = find_plan(c, g);
         if (e < 0) continue;
         if (e != pc.e) load_plan(c, e, pc);
-        const int Nj = unrank_lane(c, n, pc.m, g - pc.first);
-        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end, st);
+        comp_init(c, pc, unrank_lane(c, n, pc.m, g - pc.first), cs);
+        const int64_t lat = eval_one(c, pc, cs, G, D, T_end, st);
         if (A.lat_out && lane == 0) A.lat_out[i] = lat;
         better(lat, g, bl, bg);
       }
@@ -367,29 +412,25 @@ __global__ void __launch_bounds__(kEvalThreads) k2_eval(Cfg c, EvalArgs A) {
       if (g >= gend) continue;
       int e = find_plan(c, g);
       if (e != pc.e) load_plan(c, e, pc);
-      int Nj = unrank_lane(c, n, pc.m, g - pc.first);
+      comp_init(c, pc, unrank_lane(c, n, pc.m, g - pc.first), cs);
       for (;;) {
-        const int64_t lat = eval_one(c, pc, Nj, G, D, T_end, st);
+        const int64_t lat = eval_one(c, pc, cs, G, D, T_end, st);
         if (A.lat_out && lane == 0) A.lat_out[g - A.begin] = lat;
         better(lat, g, bl, bg);
         if (++g >= gend) break;
         if (g >= pc.first + pc.count) {  // next plan with candidates
           e = find_plan(c, g);
           load_plan(c, e, pc);
-          Nj = unrank_lane(c, n, pc.m, 0);
+          comp_init(c, pc, unrank_lane(c, n, pc.m, 0), cs);
         } else {
-          next_composition(pc.m, Nj);
+          comp_next(c, pc, cs);
         }
       }
     }
   }
   if (lane == 0 && A.stats) {
-    atomicAdd(&A.stats[0], st.cand);
-    atomicAdd(&A.stats[1], st.ops);
-    atomicAdd(&A.stats[2], st.itf);
-    atomicAdd(&A.stats[3], st.atf);
-    atomicAdd(&A.stats[4], st.itb);
-    atomicAdd(&A.stats[5], st.atb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) atomicAdd(&A.stats[i], (unsigned long long)st.v[i]);
   }
   // block argmin -> partials
   __shared__ long long bl_sm[kEvalThreads / 32];
@@ -441,8 +482,14 @@ int eval_grid(int sms) {
 
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches) {
   if (a.ev0) cudaEventRecord(a.ev0, st);
-  if (a.index) k2_eval<true><<<a.grid, kEvalThreads, 0, st>>>(c, a);
-  else k2_eval<false><<<a.grid, kEvalThreads, 0, st>>>(c, a);
+  if (a.mode == 1) {
+    const cudaError_t e = launch_eval_thread(c, a, st);
+    if (e != cudaSuccess) return e;
+  } else if (a.index) {
+    k2_eval<true><<<a.grid, kEvalThreads, 0, st>>>(c, a);
+  } else {
+    k2_eval<false><<<a.grid, kEvalThreads, 0, st>>>(c, a);
+  }
   if (a.ev1) cudaEventRecord(a.ev1, st);
   k3_reduce<<<1, 256, 0, st>>>(a);
   if (launches) *launches += 2;

@@ -1,0 +1,441 @@
+// eval_thread.cu — K2t: one candidate per THREAD (32 candidates per warp).
+//
+// Same computation as eval.cu's one-candidate-per-warp K2 (Alg. 2's
+// per-partition body, over the exact chain tables of
+// R-FACT; readings R9-R18), restructured so that a warp instruction does
+// useful work for 32 candidates instead of spreading one candidate's n slots
+// over lanes: every per-slot / per-pipeline loop is a short sequential loop
+// in one thread, with the thread's small arrays (counts, owners, ranks) in
+// shared memory at an odd word stride (lanes touching the same index hit
+// distinct banks).  Each thread walks a run of consecutive candidate
+// indices, carrying the composition from one lexicographic successor to the
+// next.
+#include "optimus_dev.cuh"
+
+namespace optimus {
+namespace {
+
+constexpr int kTThreads = 128;
+constexpr int kTRun = 16;                 // consecutive candidates per thread
+constexpr int kTStrideW = 81;             // per-thread scratch: 81 words (odd)
+constexpr int kTStride = kTStrideW * 4;   // = 324 bytes
+
+// Per-thread scratch layout (bytes): N[32] c[32] cnt[34] Qc[32] own[32] rk[32]
+// cb[32] kb[32] Qcb[32] seen[32]  (= 322 <= 324)
+struct TS {
+  uint8_t* N;     // composition N_j
+  uint8_t* c;     // coarse (not yet moved) forward microbatches c_j
+  uint8_t* cnt;   // cnt[t] = #{j : c_j >= t}, t = 1..n (cnt[n+1] = 0)
+  uint8_t* Qc;    // Qc[i] = #{moved forward EF <= G_i}
+  uint8_t* own;   // owner pipeline of LLM microbatch slot i (global ordering)
+  uint8_t* rk;    // rank of D_i within its owner's sorted deadlines
+  uint8_t* cb;    // coarse backward microbatches per pipeline
+  uint8_t* kb;    // committed backward chains per pipeline
+  uint8_t* Qcb;   // Qcb[i] = #{owner's moved backward EF <= D_i}
+  uint8_t* seen;  // ordering: slots already given to pipeline j
+};
+
+__device__ __forceinline__ TS ts_at(unsigned char* base) {
+  TS s;
+  s.N = base;
+  s.c = base + 32;
+  s.cnt = base + 64;
+  s.Qc = base + 98;
+  s.own = base + 130;
+  s.rk = base + 162;
+  s.cb = base + 194;
+  s.kb = base + 226;
+  s.Qcb = base + 258;
+  s.seen = base + 290;
+  return s;
+}
+
+struct TPlan {
+  int e, P, rt, m, kmax, np1;
+  uint64_t first, count;
+  const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
+  const int64_t* preBEF;  // PREB_EF(t)
+  const int64_t* devF;
+  const int64_t* devB;
+  const int64_t* inbF;
+  const int64_t* lenF;
+  const int64_t* inbB;
+  const int64_t* lenB;
+};
+
+__device__ void tplan(const Cfg& c, int e, TPlan& p) {
+  const PlanDesc& d = c.plans[e];
+  p.e = e;
+  p.P = d.P;
+  p.rt = d.rt;
+  p.m = d.m;
+  p.kmax = d.kmax;
+  p.np1 = c.n + 1;
+  p.first = d.first;
+  p.count = d.count;
+  p.preEF = c.tables + d.preF + (int64_t)(d.P - 1) * (c.n + 1);
+  p.preBEF = c.tables + d.preB + (int64_t)(d.P - 1) * (c.n + 1);
+  p.devF = c.tables + d.devF;
+  p.devB = c.tables + d.devB;
+  p.inbF = c.tables + d.inbF;
+  p.lenF = c.tables + d.lenF;
+  p.inbB = c.tables + d.inbB;
+  p.lenB = c.tables + d.lenB;
+}
+
+__device__ int tfind_plan(const Cfg& c, uint64_t g) {
+  for (int e = 0; e < c.E; ++e) {
+    const PlanDesc& d = c.plans[e];
+    if (d.count && g >= d.first && g < d.first + d.count) return e;
+  }
+  return -1;
+}
+
+// Lexicographic unranking (R17) into N[0..m).
+__device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
+  int rem = n;
+  for (int j = 0; j < m - 1; ++j) {
+    const int parts = m - j;
+    int x = 1;
+    for (; x <= rem - (parts - 1); ++x) {
+      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (kMaxN + 1) + (parts - 2)]);
+      if (rank < cnt) break;
+      rank -= cnt;
+    }
+    s.N[j] = (uint8_t)x;
+    rem -= x;
+  }
+  s.N[m - 1] = (uint8_t)rem;
+}
+
+// Lexicographic successor of N (m parts); false past the last composition.
+__device__ bool tnext(int m, TS& s) {
+  if (m < 2) return false;
+  const int last = s.N[m - 1];
+  if (last > 1) {  // common step: one microbatch from part m-1 to part m-2
+    s.N[m - 2] += 1;
+    s.N[m - 1] = (uint8_t)(last - 1);
+    return true;
+  }
+  int S = last, jj = m - 2;
+  for (; jj >= 0; --jj) {  // largest jj whose suffix can still give one away
+    if (S > m - 1 - jj) break;
+    S += s.N[jj];
+  }
+  if (jj < 0) return false;
+  s.N[jj] += 1;
+  for (int j = jj + 1; j < m - 1; ++j) s.N[j] = 1;
+  s.N[m - 1] = (uint8_t)(S - 1 - (m - 2 - jj));
+  return true;
+}
+
+// Forward dependency shift (R10) of the current state; pend = a trial EF
+// not yet counted in Qc (kInf: none).  need_i = i - #{moved EF <= G_i}; INF
+// if need_i > sum c; else max over need_i > 0 of PRE_EF(level of sorted
+// position need_i) - G_i.
+__device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, int n, int sumc, int64_t pend,
+                                            const TS& s) {
+  int t = 0, lend = 0;
+  int64_t best = kNegInf;
+  for (int i = 1; i <= n; ++i) {
+    const int64_t g = G[i - 1];
+    const int need = i - s.Qc[i - 1] - (pend <= g ? 1 : 0);
+    if (need > sumc) return kInf;
+    if (need <= 0) continue;
+    while (lend < need) lend += s.cnt[++t];
+    while (lend - s.cnt[t] >= need) lend -= s.cnt[t--];
+    best = max(best, __ldg(&p.preEF[t]) - g);
+  }
+  return best;
+}
+
+// Backward dependency shift (R15) after the ordering; trial pipeline js
+// (-1: none) with trial chain end efb.
+__device__ int64_t tdep_bwd(const TPlan& p, const int64_t* D, int n, int js, int64_t efb, const TS& s) {
+  int64_t best = kNegInf;
+  for (int i = 0; i < n; ++i) {
+    const int o = s.own[i];
+    const int64_t d = D[i];
+    const int cbo = s.cb[o] - (o == js ? 1 : 0);
+    const int need = s.rk[i] - s.Qcb[i] - (o == js && efb <= d ? 1 : 0);
+    if (need > cbo) return kInf;
+    if (need > 0) best = max(best, __ldg(&p.preBEF[need]) - d);
+  }
+  return best;
+}
+
+struct TStats {
+  unsigned v[8];
+};
+
+// One candidate, sequentially in this thread.
+__device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
+                         TStats& st) {
+  const int n = c.n, m = p.m, rt = p.rt, np1 = p.np1, kmax = p.kmax;
+  // ---------------- coarse init (R9) -------------------------------------
+  for (int t = 0; t <= n + 1; ++t) s.cnt[t] = 0;
+  for (int j = 0; j < m; ++j) {
+    s.c[j] = s.N[j];
+    s.cnt[s.N[j]] += 1;
+  }
+  for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
+  for (int i = 0; i < n; ++i) s.Qc[i] = 0;
+  int sumc = n, itf = 0, atf = 0, itb = 0, atb = 0;
+  // ---------------- forward OptimizeSchedule (R10-R13) --------------------
+  int64_t dep = tdep_fwd(p, G, n, sumc, kInf, s);
+  int64_t Delta;
+  for (;;) {
+    ++itf;
+    int64_t dev = kNegInf;
+    int js = -1;
+    for (int j = 0, a = 0, r = 0; j < m; ++j) {  // findCritical, ties -> lowest j (R11)
+      const int cj = s.c[j];
+      if (cj > 0) {
+        const int64_t v = __ldg(&p.devF[a * np1 + cj]);
+        if (v > dev) { dev = v; js = j; }
+      }
+      if (++r == rt) { r = 0; ++a; }
+    }
+    Delta = max((int64_t)0, max(dev, dep));
+    if (Delta == 0 || sumc == 0) break;
+    const int as = js / rt, cjs = s.c[js], kfj = s.N[js] - cjs;
+    if (kfj >= (int)__ldg(&p.lenF[as])) break;  // ScheduleKernels fails (R12)
+    const int64_t EF = __ldg(&p.inbF[as * kmax + kfj]);
+    ++atf;
+    s.c[js] = (uint8_t)(cjs - 1);  // trial move
+    s.cnt[cjs] -= 1;
+    const int64_t dep2 = tdep_fwd(p, G, n, sumc - 1, EF, s);
+    if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
+      s.c[js] = (uint8_t)cjs;
+      s.cnt[cjs] += 1;
+      break;
+    }
+    for (int i = 0; i < n; ++i) s.Qc[i] += EF <= G[i] ? 1 : 0;
+    dep = dep2;
+    --sumc;
+  }
+  const int64_t Df = Delta;
+  // ---------------- global ordering (R14): merge pre levels and moved EFs --
+  // pre entries (value PRE_EF(t) - Df, j, t-1), levels of equal value
+  // grouped; moved entries (INB_F[a_j][k], j, c_j + k) extracted in key
+  // order by repeated minimum search above the last key taken.
+  int maxc = 0;
+  for (int j = 0; j < m; ++j) {
+    maxc = max(maxc, (int)s.c[j]);
+    s.seen[j] = 0;
+  }
+  int slot = 0;
+  int64_t dep_b = kNegInf;
+  int64_t lastv = kNegInf;
+  int lastk = -1;
+  int64_t mv = kInf;
+  int mk = 0, mj = -1;
+  auto next_moved = [&]() {  // smallest moved key above (lastv, lastk)
+    mv = kInf;
+    mj = -1;
+    if (sumc == n) return;
+    for (int j = 0, a = 0, r = 0; j < m; ++j) {
+      const int cj = s.c[j], kfj = s.N[j] - cj;
+      for (int k = 0; k < kfj; ++k) {
+        const int64_t v = __ldg(&p.inbF[a * kmax + k]);
+        const int key = (j << 8) | (cj + k);
+        if ((v > lastv || (v == lastv && key > lastk)) && (v < mv || (v == mv && key < mk))) {
+          mv = v;
+          mk = key;
+          mj = j;
+        }
+      }
+      if (++r == rt) { r = 0; ++a; }
+    }
+  };
+  auto assign = [&](int j) {  // slot -> pipeline j (R14); rank of its deadline (R15)
+    const int r = s.N[j] - s.seen[j];
+    s.seen[j] += 1;
+    s.own[slot] = (uint8_t)j;
+    s.rk[slot] = (uint8_t)r;
+    dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);  // initial backward shift, no moves yet
+    ++slot;
+  };
+  next_moved();
+  for (int t1 = 1; t1 <= maxc;) {
+    int t2 = t1;
+    const int64_t pv = __ldg(&p.preEF[t1]);
+    while (t2 < maxc && __ldg(&p.preEF[t2 + 1]) == pv) ++t2;
+    const int64_t v = pv - Df;
+    for (int j = 0; j < m; ++j)
+      for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
+        const int key = (j << 8) | (t - 1);
+        while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
+          assign(mj);
+          lastv = mv;
+          lastk = mk;
+          next_moved();
+        }
+        assign(j);
+        lastv = v;
+        lastk = key;
+      }
+    t1 = t2 + 1;
+  }
+  while (mj >= 0) {
+    assign(mj);
+    lastv = mv;
+    lastk = mk;
+    next_moved();
+  }
+  // ---------------- backward OptimizeSchedule (R15) ------------------------
+  int sumcb = n;
+  bool init_b = false;
+  for (;;) {
+    ++itb;
+    int64_t dev = kNegInf;
+    int js = -1;
+    for (int j = 0, a = 0, r = 0; j < m; ++j) {
+      const int cbj = init_b ? s.cb[j] : s.N[j];
+      if (cbj > 0) {
+        const int64_t v = __ldg(&p.devB[a * np1 + cbj]);
+        if (v > dev) { dev = v; js = j; }
+      }
+      if (++r == rt) { r = 0; ++a; }
+    }
+    Delta = max((int64_t)0, max(dev, dep_b));
+    if (Delta == 0 || sumcb == 0) break;
+    const int as = js / rt, kfj = s.N[js] - s.c[js];
+    const int kbj = init_b ? s.kb[js] : 0;
+    const int64_t rowoff = (int64_t)as * (kmax + 1) + kfj;
+    if (kbj >= (int)__ldg(&p.lenB[rowoff])) break;
+    const int64_t EFb = __ldg(&p.inbB[rowoff * kmax + kbj]);
+    ++atb;
+    if (!init_b) {  // backward moves are rare: per-pipeline state on first use
+      for (int j = 0; j < m; ++j) { s.cb[j] = s.N[j]; s.kb[j] = 0; }
+      for (int i = 0; i < n; ++i) s.Qcb[i] = 0;
+      init_b = true;
+    }
+    const int64_t dep2 = tdep_bwd(p, D, n, js, EFb, s);
+    if (dep2 > Delta) break;
+    for (int i = 0; i < n; ++i) s.Qcb[i] += (s.own[i] == js && EFb <= D[i]) ? 1 : 0;
+    s.cb[js] -= 1;
+    s.kb[js] += 1;
+    dep_b = dep2;
+    --sumcb;
+  }
+  st.v[0] += 1;
+  st.v[1] += m;
+  st.v[2] += m * itf;
+  st.v[3] += itf;
+  st.v[4] += atf;
+  st.v[5] += m * itb;
+  st.v[6] += itb;
+  st.v[7] += atb;
+  return T_end + Df + Delta;  // R16
+}
+
+__device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, uint64_t& bg) {
+  if (lat < bl || (lat == bl && g < bg)) { bl = lat; bg = g; }
+}
+
+template <bool EXPLICIT>
+__global__ void __launch_bounds__(kTThreads) k2_eval_thread(Cfg c, EvalArgs A) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  __shared__ int64_t G[kMaxN], D[kMaxN];
+  __shared__ long long bl_sm[kTThreads / 32];
+  __shared__ unsigned long long bg_sm[kTThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = c.n;
+  const int64_t T_end = c.scal[1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    G[i] = c.F[i] - c.L;          // EF_i + L <= F_i
+    D[i] = T_end - c.B[i] - c.L;  // EB_i >= B_i + L (mirrored)
+  }
+  __syncthreads();
+  TS s = ts_at(tsm + (size_t)threadIdx.x * kTStride);
+  TPlan p;
+  p.e = -1;
+  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
+  int64_t bl = INT64_MAX;
+  uint64_t bg = UINT64_MAX;
+  const uint64_t per_warp = 32ull * (EXPLICIT ? 1 : kTRun);
+  const uint64_t nchunks = (A.count + per_warp - 1) / per_warp;
+  for (;;) {
+    unsigned long long ch = 0;
+    if (lane == 0) ch = atomicAdd(A.counter, 1ull);
+    ch = __shfl_sync(0xffffffffu, ch, 0);
+    if (ch >= nchunks) break;
+    if (EXPLICIT) {
+      const uint64_t i = ch * per_warp + lane;
+      if (i < A.count) {
+        const uint64_t g = A.index[i];
+        const int e = tfind_plan(c, g);
+        if (e >= 0) {
+          if (e != p.e) tplan(c, e, p);
+          tunrank(c, n, p.m, g - p.first, s);
+          const int64_t lat = teval(c, p, G, D, T_end, s, st);
+          if (A.lat_out) A.lat_out[i] = lat;
+          tbetter(lat, g, bl, bg);
+        }
+      }
+    } else {
+      // this rank's positions [pos, pos + kTRun) -> global indices (block-cyclic over ranks)
+      const uint64_t pos = ch * per_warp + (uint64_t)lane * kTRun;
+      const uint64_t rb = pos / A.block, offb = pos % A.block;
+      uint64_t g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + offb;
+      const uint64_t gend = min(g + kTRun, A.end);
+      if (g < gend) {
+        int e = tfind_plan(c, g);
+        if (e != p.e) tplan(c, e, p);
+        tunrank(c, n, p.m, g - p.first, s);
+        for (;;) {
+          const int64_t lat = teval(c, p, G, D, T_end, s, st);
+          if (A.lat_out) A.lat_out[g - A.begin] = lat;
+          tbetter(lat, g, bl, bg);
+          if (++g >= gend) break;
+          if (g >= p.first + p.count) {
+            tplan(c, tfind_plan(c, g), p);
+            tunrank(c, n, p.m, 0, s);
+          } else {
+            tnext(p.m, s);
+          }
+        }
+      }
+    }
+  }
+  // warp + block argmin -> partials; counters
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+    const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+    tbetter(ol, og, bl, bg);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned v = st.v[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && A.stats) atomicAdd(&A.stats[i], (unsigned long long)v);
+  }
+  if (lane == 0) { bl_sm[warp] = bl; bg_sm[warp] = bg; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t l = INT64_MAX;
+    uint64_t gg = UINT64_MAX;
+    for (int w = 0; w < kTThreads / 32; ++w) tbetter(bl_sm[w], bg_sm[w], l, gg);
+    A.partials[2 * blockIdx.x] = l;
+    A.partials[2 * blockIdx.x + 1] = (int64_t)gg;
+  }
+}
+
+}  // namespace
+
+int eval_thread_grid(int sms) {
+  int per = 0;
+  cudaFuncSetAttribute(k2_eval_thread<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
+  cudaFuncSetAttribute(k2_eval_thread<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false>, kTThreads, kTThreads * kTStride);
+  return max(1, per) * sms;
+}
+
+cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)kTThreads * kTStride;
+  if (a.index) k2_eval_thread<true><<<a.grid, kTThreads, smem, st>>>(c, a);
+  else k2_eval_thread<false><<<a.grid, kTThreads, smem, st>>>(c, a);
+  return cudaGetLastError();
+}
+
+}  // namespace optimus

@@ -106,8 +106,12 @@ struct EvalArgs {
   unsigned long long* counter;
   uint64_t total;
   int grid;
+  int mode;                   // 0: one candidate per warp (eval.cu), 1: one per thread (eval_thread.cu)
   cudaEvent_t ev0, ev1;       // optional: recorded around K2 for per-kernel timing
   unsigned long long* stats;  // [6] cumulative: candidates, algorithmic ops, fwd iters, fwd attempts, bwd iters, bwd attempts
 };
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
+cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
+int eval_grid(int sms);
+int eval_thread_grid(int sms);
 }  // namespace optimus

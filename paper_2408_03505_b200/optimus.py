@@ -21,7 +21,8 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_set_timing",
+    "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_set_eval_mode",
+    "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
 ]
 
@@ -87,6 +88,7 @@ def lib():
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_set_timing": [vp, ctypes.c_int],
+            "optimus_set_eval_mode": [vp, ctypes.c_int],
             "optimus_last_timing": [vp, P(ctypes.c_float), P(ctypes.c_float)],
             "optimus_eval_stats": [vp, P(ctypes.c_uint64), vp],
             "optimus_io_bytes": [vp, P(ctypes.c_uint64), P(ctypes.c_uint64)],
@@ -279,6 +281,10 @@ class Ctx:
         b, e = ctypes.c_int32(), ctypes.c_int32()
         _check(lib().optimus_launch_count(self.h, ctypes.byref(b), ctypes.byref(e)))
         return b.value, e.value
+
+    def set_eval_mode(self, mode: int):
+        """1 = one candidate per thread (default), 0 = one candidate per warp."""
+        _check(lib().optimus_set_eval_mode(self.h, mode))
 
     def set_timing(self, on: bool = True):
         _check(lib().optimus_set_timing(self.h, 1 if on else 0))

@@ -27,9 +27,14 @@ def dev():
     return torch
 
 
-def _load(prob):
+def _load(prob, mode=1):
     from paper_2408_03505_b200 import optimus_load_costs
-    return optimus_load_costs(prob)
+    ctx = optimus_load_costs(prob)
+    ctx.set_eval_mode(mode)
+    return ctx
+
+
+MODES = pytest.mark.parametrize("mode", [0, 1], ids=["warp_per_cand", "thread_per_cand"])
 
 
 SMALL = [toy_problem(), config_problem(1), config_problem(2)] + [random_problem(s) for s in range(40)]
@@ -85,10 +90,11 @@ def _taus(prob, plan, bwd):
     return out
 
 
+@MODES
 @pytest.mark.parametrize("prob", SMALL, ids=lambda p: p["name"])
-def test_full_space_parity(dev, oracle_mod, prob):
+def test_full_space_parity(dev, oracle_mod, prob, mode):
     torch = dev
-    ctx = _load(prob)
+    ctx = _load(prob, mode)
     total, _ = ctx.num_candidates()
     lat = torch.full((total,), -7, dtype=torch.int64, device="cuda")
     best2 = torch.empty(2, dtype=torch.int64, device="cuda")
@@ -103,11 +109,12 @@ def test_full_space_parity(dev, oracle_mod, prob):
     assert (int(b[0]), int(b[1])) == (int(ref.min()), int(np.argmin(ref)))
 
 
+@MODES
 @pytest.mark.parametrize("prob", BIG, ids=lambda p: p["name"])
-def test_sampled_parity_full_size(dev, oracle_mod, prob):
+def test_sampled_parity_full_size(dev, oracle_mod, prob, mode):
     """BASELINE sizes: 4096 seeded indices per config through eval_indices."""
     torch = dev
-    ctx = _load(prob)
+    ctx = _load(prob, mode)
     total, _ = ctx.num_candidates()
     idx = np.array(sample_indices(20241018, 4096, total), dtype=np.uint64)
     di = torch.from_numpy(idx.astype(np.int64)).cuda()
@@ -124,12 +131,13 @@ def test_sampled_parity_full_size(dev, oracle_mod, prob):
     assert (int(b[0]), int(b[1])) == (int(ref[j]), int(idx[j]))
 
 
+@MODES
 @pytest.mark.parametrize("prob", [config_problem(4), config_problem(2)], ids=lambda p: p["name"])
-def test_contiguous_ranges_full_size(dev, oracle_mod, prob):
+def test_contiguous_ranges_full_size(dev, oracle_mod, prob, mode):
     """The launch configuration bench.py times (eval_candidates over ranges),
     checked on a ragged window that straddles plan boundaries."""
     torch = dev
-    ctx = _load(prob)
+    ctx = _load(prob, mode)
     total, n_plans = ctx.num_candidates()
     firsts = [ctx.get_plan(i)["first"] for i in range(n_plans) if ctx.get_plan(i)["count"]]
     for f in firsts[1:4]:
@@ -142,13 +150,14 @@ def test_contiguous_ranges_full_size(dev, oracle_mod, prob):
         assert np.array_equal(lat.cpu().numpy(), ref)
 
 
+@MODES
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_rank_sharding(dev, oracle_mod, world):
+def test_rank_sharding(dev, oracle_mod, world, mode):
     """Block-cyclic sharding: every rank's best, gathered and decoded, equals the
     single-rank answer; lat dumps of all ranks tile the space exactly once."""
     torch = dev
     prob = config_problem(2)
-    ctx = _load(prob)
+    ctx = _load(prob, mode)
     total, _ = ctx.num_candidates()
     lat = torch.full((total,), -1, dtype=torch.int64, device="cuda")
     gathered = []
@@ -168,11 +177,12 @@ def test_rank_sharding(dev, oracle_mod, world):
     assert ref == res["lat_ns"]
 
 
-def test_edge_cases(dev, oracle_mod):
+@MODES
+def test_edge_cases(dev, oracle_mod, mode):
     torch = dev
     from paper_2408_03505_b200 import OptimusError
     prob = toy_problem()
-    ctx = _load(prob)
+    ctx = _load(prob, mode)
     total, _ = ctx.num_candidates()
     b2 = torch.empty(2, dtype=torch.int64, device="cuda")
     ctx.eval_candidates(5, 5, b2)  # empty range
@@ -192,7 +202,8 @@ def test_edge_cases(dev, oracle_mod):
     assert np.array_equal(lat.cpu().numpy(), o.eval(np.arange(total, dtype=np.uint64)))
 
 
-def test_degenerate_problems(dev, oracle_mod):
+@MODES
+def test_degenerate_problems(dev, oracle_mod, mode):
     """Zero-kernel encoder, N_mb = PP (all warm-up), m = N_mb plans, v = 1."""
     torch = dev
     probs = []
@@ -206,7 +217,7 @@ def test_degenerate_problems(dev, oracle_mod):
             probs.append(q)
     assert len(probs) > 5
     for prob in probs:
-        ctx = _load(prob)
+        ctx = _load(prob, mode)
         total, _ = ctx.num_candidates()
         lat = torch.empty(total, dtype=torch.int64, device="cuda")
         b2 = torch.empty(2, dtype=torch.int64, device="cuda")
