@@ -52,6 +52,7 @@ __device__ __forceinline__ TS ts_at(unsigned char* base) {
 
 struct TPlan {
   int e, P, rt, m, kmax, np1;
+  bool strict;            // PRE_EF strictly increasing: pre entries order by (t, j)
   uint64_t first, count;
   const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
   const int64_t* preBEF;  // PREB_EF(t)
@@ -81,6 +82,8 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.lenF = c.tables + d.lenF;
   p.inbB = c.tables + d.inbB;
   p.lenB = c.tables + d.lenB;
+  p.strict = true;
+  for (int t = 1; t < c.n; ++t) p.strict = p.strict && __ldg(&p.preEF[t + 1]) > __ldg(&p.preEF[t]);
 }
 
 __device__ int tfind_plan(const Cfg& c, uint64_t g) {
@@ -149,6 +152,126 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
   return best;
 }
 
+// tdep_fwd while no forward chain has been committed (Qc = 0).  Position p
+// (1-based) of the sorted pre multiset is first reached by slot p, or p+1
+// once the trial EF counts (slots >= i0, G ascending); within a level the
+// term PRE_EF(t) - G_slot is largest at its first position, so one term per
+// level suffices.  INF when slot n still needs n pre entries (the trial EF
+// meets no deadline) but only n-1 remain.
+__device__ __forceinline__ int64_t tdep_fwd0(const TPlan& p, const int64_t* G, int n, int sumc, int64_t pend,
+                                             const TS& s) {
+  int i0 = n + 1;
+  if (pend != kInf) {
+    int lo = 0, hi = n;  // first slot index (0-based) with G >= pend
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (G[mid] >= pend) hi = mid; else lo = mid + 1;
+    }
+    i0 = lo + 1;
+  }
+  if (n - (i0 <= n ? 1 : 0) > sumc) return kInf;  // slot n needs more pre entries than remain
+  int64_t best = kNegInf;
+  for (int t = 1, pos = 0; pos < sumc; ++t) {
+    const int start = pos + 1;
+    const int slot = start < i0 ? start : start + 1;
+    best = max(best, __ldg(&p.preEF[t]) - G[slot - 1]);
+    pos += s.cnt[t];
+  }
+  return best;
+}
+
+// Global ordering (R14) in the general case: merge the pre levels (value
+// PRE_EF(t) - Df, key (j, t-1); levels of equal value grouped) with the
+// moved EFs (INB_F[a_j][k], key (j, c_j + k)) extracted in key order by
+// repeated minimum search above the last key taken.  Fills own[] / rk[]
+// and returns the initial backward shift max_i PREB_EF(rk_i) - D_i.
+__device__ int64_t order_general(const TPlan& p, const int64_t* D, int n, int m, int64_t Df, bool moved, TS& s) {
+  const int rt = p.rt, kmax = p.kmax;
+  int maxc = 0;
+  for (int j = 0; j < m; ++j) {
+    maxc = max(maxc, (int)s.c[j]);
+    s.seen[j] = 0;
+  }
+  int slot = 0;
+  int64_t dep_b = kNegInf, lastv = kNegInf, mv = kInf;
+  int lastk = -1, mk = 0, mj = -1;
+  auto next_moved = [&]() {
+    mv = kInf;
+    mj = -1;
+    if (!moved) return;
+    for (int j = 0, a = 0, r = 0; j < m; ++j) {
+      const int cj = s.c[j], kfj = s.N[j] - cj;
+      for (int k = 0; k < kfj; ++k) {
+        const int64_t v = __ldg(&p.inbF[a * kmax + k]);
+        const int key = (j << 8) | (cj + k);
+        if ((v > lastv || (v == lastv && key > lastk)) && (v < mv || (v == mv && key < mk))) {
+          mv = v;
+          mk = key;
+          mj = j;
+        }
+      }
+      if (++r == rt) { r = 0; ++a; }
+    }
+  };
+  auto assign = [&](int j) {  // slot -> pipeline j; rank of its deadline (R15)
+    const int r = s.N[j] - s.seen[j];
+    s.seen[j] += 1;
+    s.own[slot] = (uint8_t)j;
+    s.rk[slot] = (uint8_t)r;
+    dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);
+    ++slot;
+  };
+  next_moved();
+  for (int t1 = 1; t1 <= maxc;) {
+    int t2 = t1;
+    const int64_t pv = __ldg(&p.preEF[t1]);
+    while (t2 < maxc && __ldg(&p.preEF[t2 + 1]) == pv) ++t2;
+    const int64_t v = pv - Df;
+    for (int j = 0; j < m; ++j)
+      for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
+        const int key = (j << 8) | (t - 1);
+        while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
+          assign(mj);
+          lastv = mv;
+          lastk = mk;
+          next_moved();
+        }
+        assign(j);
+        lastv = v;
+        lastk = key;
+      }
+    t1 = t2 + 1;
+  }
+  while (mj >= 0) {
+    assign(mj);
+    lastv = mv;
+    lastk = mk;
+    next_moved();
+  }
+  (void)n;
+  return dep_b;
+}
+
+// Initial backward shift when no forward chain moved and PRE_EF is strict:
+// the order is (t, j), slot of (t, j) gets rank N_j - t + 1; active
+// pipelines compacted level by level (own/rk are not materialised).
+__device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, int m, TS& s) {
+  uint8_t* act = s.seen;
+  for (int j = 0; j < m; ++j) act[j] = (uint8_t)j;
+  int na = m, pos = 0;
+  int64_t best = kNegInf;
+  for (int t = 1; na > 0; ++t) {
+    int nn = 0;
+    for (int q = 0; q < na; ++q) {
+      const int j = act[q], Nj = s.N[j];
+      best = max(best, __ldg(&p.preBEF[Nj - t + 1]) - D[pos++]);
+      if (Nj > t) act[nn++] = (uint8_t)j;
+    }
+    na = nn;
+  }
+  return best;
+}
+
 // Backward dependency shift (R15) after the ordering; trial pipeline js
 // (-1: none) with trial chain end efb.
 __device__ int64_t tdep_bwd(const TPlan& p, const int64_t* D, int n, int js, int64_t efb, const TS& s) {
@@ -179,10 +302,9 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     s.cnt[s.N[j]] += 1;
   }
   for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
-  for (int i = 0; i < n; ++i) s.Qc[i] = 0;
   int sumc = n, itf = 0, atf = 0, itb = 0, atb = 0;
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
-  int64_t dep = tdep_fwd(p, G, n, sumc, kInf, s);
+  int64_t dep = tdep_fwd0(p, G, n, sumc, kInf, s);
   int64_t Delta;
   for (;;) {
     ++itf;
@@ -204,85 +326,23 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     ++atf;
     s.c[js] = (uint8_t)(cjs - 1);  // trial move
     s.cnt[cjs] -= 1;
-    const int64_t dep2 = tdep_fwd(p, G, n, sumc - 1, EF, s);
+    const int64_t dep2 = sumc == n ? tdep_fwd0(p, G, n, sumc - 1, EF, s) : tdep_fwd(p, G, n, sumc - 1, EF, s);
     if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
       s.c[js] = (uint8_t)cjs;
       s.cnt[cjs] += 1;
       break;
     }
+    if (sumc == n)
+      for (int i = 0; i < n; ++i) s.Qc[i] = 0;
     for (int i = 0; i < n; ++i) s.Qc[i] += EF <= G[i] ? 1 : 0;
     dep = dep2;
     --sumc;
   }
   const int64_t Df = Delta;
-  // ---------------- global ordering (R14): merge pre levels and moved EFs --
-  // pre entries (value PRE_EF(t) - Df, j, t-1), levels of equal value
-  // grouped; moved entries (INB_F[a_j][k], j, c_j + k) extracted in key
-  // order by repeated minimum search above the last key taken.
-  int maxc = 0;
-  for (int j = 0; j < m; ++j) {
-    maxc = max(maxc, (int)s.c[j]);
-    s.seen[j] = 0;
-  }
-  int slot = 0;
-  int64_t dep_b = kNegInf;
-  int64_t lastv = kNegInf;
-  int lastk = -1;
-  int64_t mv = kInf;
-  int mk = 0, mj = -1;
-  auto next_moved = [&]() {  // smallest moved key above (lastv, lastk)
-    mv = kInf;
-    mj = -1;
-    if (sumc == n) return;
-    for (int j = 0, a = 0, r = 0; j < m; ++j) {
-      const int cj = s.c[j], kfj = s.N[j] - cj;
-      for (int k = 0; k < kfj; ++k) {
-        const int64_t v = __ldg(&p.inbF[a * kmax + k]);
-        const int key = (j << 8) | (cj + k);
-        if ((v > lastv || (v == lastv && key > lastk)) && (v < mv || (v == mv && key < mk))) {
-          mv = v;
-          mk = key;
-          mj = j;
-        }
-      }
-      if (++r == rt) { r = 0; ++a; }
-    }
-  };
-  auto assign = [&](int j) {  // slot -> pipeline j (R14); rank of its deadline (R15)
-    const int r = s.N[j] - s.seen[j];
-    s.seen[j] += 1;
-    s.own[slot] = (uint8_t)j;
-    s.rk[slot] = (uint8_t)r;
-    dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);  // initial backward shift, no moves yet
-    ++slot;
-  };
-  next_moved();
-  for (int t1 = 1; t1 <= maxc;) {
-    int t2 = t1;
-    const int64_t pv = __ldg(&p.preEF[t1]);
-    while (t2 < maxc && __ldg(&p.preEF[t2 + 1]) == pv) ++t2;
-    const int64_t v = pv - Df;
-    for (int j = 0; j < m; ++j)
-      for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
-        const int key = (j << 8) | (t - 1);
-        while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
-          assign(mj);
-          lastv = mv;
-          lastk = mk;
-          next_moved();
-        }
-        assign(j);
-        lastv = v;
-        lastk = key;
-      }
-    t1 = t2 + 1;
-  }
-  while (mj >= 0) {
-    assign(mj);
-    lastv = mv;
-    lastk = mk;
-    next_moved();
-  }
+  // ---------------- global ordering (R14) -------------------------------
+  const bool moved = sumc < n;
+  bool have_order = moved || !p.strict;
+  int64_t dep_b = have_order ? order_general(p, D, n, m, Df, moved, s) : order_fast(p, D, m, s);
   // ---------------- backward OptimizeSchedule (R15) ------------------------
   int sumcb = n;
   bool init_b = false;
@@ -306,6 +366,10 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (kbj >= (int)__ldg(&p.lenB[rowoff])) break;
     const int64_t EFb = __ldg(&p.inbB[rowoff * kmax + kbj]);
     ++atb;
+    if (!have_order) {  // materialise owners and ranks (same order, same initial shift)
+      order_general(p, D, n, m, Df, false, s);
+      have_order = true;
+    }
     if (!init_b) {  // backward moves are rare: per-pipeline state on first use
       for (int j = 0; j < m; ++j) { s.cb[j] = s.N[j]; s.kb[j] = 0; }
       for (int i = 0; i < n; ++i) s.Qcb[i] = 0;
