@@ -5,48 +5,57 @@
 // R-FACT; readings R9-R18), restructured so that a warp instruction does
 // useful work for 32 candidates instead of spreading one candidate's n slots
 // over lanes: every per-slot / per-pipeline loop is a short sequential loop
-// in one thread, with the thread's small arrays (counts, owners, ranks) in
-// shared memory at an odd word stride (lanes touching the same index hit
-// distinct banks).  Each thread walks a run of consecutive candidate
-// indices, carrying the composition from one lexicographic successor to the
-// next.
+// in one thread, with the thread's small arrays in shared memory at an odd
+// word stride (lanes touching the same index hit distinct banks).  Each
+// thread walks a run of consecutive candidate indices, carrying the
+// composition from one lexicographic successor to the next.
+//
+// The dependency shift (R10) is evaluated per LEVEL of the sorted coarse
+// multiset, not per slot: G_i is ascending, so among the slots whose needed
+// position falls in one level the first one dominates, and the first slot
+// reaching position p is found by walking a slot pointer over the sorted
+// "thresholds" (the first slot each moved EF counts for).  Cost O(levels +
+// moves) instead of O(n).
 #include "optimus_dev.cuh"
 
 namespace optimus {
 namespace {
 
 constexpr int kTThreads = 128;
-constexpr int kTRun = 16;                 // consecutive candidates per thread
-constexpr int kTStrideW = 81;             // per-thread scratch: 81 words (odd)
-constexpr int kTStride = kTStrideW * 4;   // = 324 bytes
+constexpr int kTRun = 8;                  // consecutive candidates per thread
+constexpr int kTStrideW = 97;             // per-thread scratch: 97 words (odd)
+constexpr int kTStride = kTStrideW * 4;   // = 388 bytes
 
-// Per-thread scratch layout (bytes): N[32] c[32] cnt[34] Qc[32] own[32] rk[32]
-// cb[32] kb[32] Qcb[32] seen[32]  (= 322 <= 324)
+// Per-thread scratch (bytes): N c cnt[34] thr own rk cb kb Qcb seen mvj mvk
 struct TS {
   uint8_t* N;     // composition N_j
   uint8_t* c;     // coarse (not yet moved) forward microbatches c_j
   uint8_t* cnt;   // cnt[t] = #{j : c_j >= t}, t = 1..n (cnt[n+1] = 0)
-  uint8_t* Qc;    // Qc[i] = #{moved forward EF <= G_i}
+  uint8_t* thr;   // committed forward thresholds: first slot (1-based) each moved EF counts for, ascending
   uint8_t* own;   // owner pipeline of LLM microbatch slot i (global ordering)
   uint8_t* rk;    // rank of D_i within its owner's sorted deadlines
   uint8_t* cb;    // coarse backward microbatches per pipeline
-  uint8_t* kb;    // committed backward chains per pipeline
+  uint8_t* kb;    // committed backward chains per pipeline (ordering: slots given so far)
   uint8_t* Qcb;   // Qcb[i] = #{owner's moved backward EF <= D_i}
-  uint8_t* seen;  // ordering: slots already given to pipeline j
+  uint8_t* seen;  // ordering: active pipeline list / slots given
+  uint8_t* mvj;   // ordering: moved entries sorted by (value, key): pipeline
+  uint8_t* mvk;   //                                                  chain index
 };
 
-__device__ __forceinline__ TS ts_at(unsigned char* base) {
+__device__ __forceinline__ TS ts_at(unsigned char* b) {
   TS s;
-  s.N = base;
-  s.c = base + 32;
-  s.cnt = base + 64;
-  s.Qc = base + 98;
-  s.own = base + 130;
-  s.rk = base + 162;
-  s.cb = base + 194;
-  s.kb = base + 226;
-  s.Qcb = base + 258;
-  s.seen = base + 290;
+  s.N = b;
+  s.c = b + 32;
+  s.cnt = b + 64;
+  s.thr = b + 98;
+  s.own = b + 130;
+  s.rk = b + 162;
+  s.cb = b + 194;
+  s.kb = b + 226;
+  s.Qcb = b + 258;
+  s.seen = b + 290;
+  s.mvj = b + 322;
+  s.mvk = b + 354;
   return s;
 }
 
@@ -132,65 +141,133 @@ __device__ bool tnext(int m, TS& s) {
   return true;
 }
 
-// Forward dependency shift (R10) of the current state; pend = a trial EF
-// not yet counted in Qc (kInf: none).  need_i = i - #{moved EF <= G_i}; INF
-// if need_i > sum c; else max over need_i > 0 of PRE_EF(level of sorted
-// position need_i) - G_i.
-__device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, int n, int sumc, int64_t pend,
-                                            const TS& s) {
-  int t = 0, lend = 0;
-  int64_t best = kNegInf;
-  for (int i = 1; i <= n; ++i) {
-    const int64_t g = G[i - 1];
-    const int need = i - s.Qc[i - 1] - (pend <= g ? 1 : 0);
-    if (need > sumc) return kInf;
-    if (need <= 0) continue;
-    while (lend < need) lend += s.cnt[++t];
-    while (lend - s.cnt[t] >= need) lend -= s.cnt[t--];
-    best = max(best, __ldg(&p.preEF[t]) - g);
+// first slot (1-based) whose deadline G is >= v; n+1 if none
+__device__ __forceinline__ int first_ge(const int64_t* G, int n, int64_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (G[mid] >= v) hi = mid; else lo = mid + 1;
   }
-  return best;
+  return lo + 1;
 }
 
-// tdep_fwd while no forward chain has been committed (Qc = 0).  Position p
-// (1-based) of the sorted pre multiset is first reached by slot p, or p+1
-// once the trial EF counts (slots >= i0, G ascending); within a level the
-// term PRE_EF(t) - G_slot is largest at its first position, so one term per
-// level suffices.  INF when slot n still needs n pre entries (the trial EF
-// meets no deadline) but only n-1 remain.
-__device__ __forceinline__ int64_t tdep_fwd0(const TPlan& p, const int64_t* G, int n, int sumc, int64_t pend,
-                                             const TS& s) {
-  int i0 = n + 1;
-  if (pend != kInf) {
-    int lo = 0, hi = n;  // first slot index (0-based) with G >= pend
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (G[mid] >= pend) hi = mid; else lo = mid + 1;
+// Forward dependency shift (R10).  Slot i needs sorted pre position
+// need_i = i - q(i), q(i) = #{thresholds <= i} (the M committed ones plus
+// the trial one bp; n+1 = never); INF if some need_i > sum c; else the max
+// over levels t of PRE_EF(t) - G_{s(t)}, s(t) = first slot reaching the
+// level's first position (slots reaching later positions of the level have
+// larger G).
+__device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, int n, int sumc, int bp, const TS& s,
+                                            int M) {
+  // max_i need_i: need rises by one per slot and drops by one per threshold
+  int maxneed = 0;
+  {
+    int k = 0, q = 0;
+    bool used = false;
+    for (;;) {
+      const int a = k < M ? s.thr[k] : n + 1, b = used ? n + 1 : bp;
+      const int nb = min(a, b);
+      maxneed = max(maxneed, min(nb, n + 1) - 1 - q);
+      if (nb > n) break;
+      if (a <= b) ++k; else used = true;
+      ++q;
     }
-    i0 = lo + 1;
   }
-  if (n - (i0 <= n ? 1 : 0) > sumc) return kInf;  // slot n needs more pre entries than remain
+  if (maxneed > sumc) return kInf;
   int64_t best = kNegInf;
-  for (int t = 1, pos = 0; pos < sumc; ++t) {
+  int i = 0, q = 0, k = 0;
+  bool used = false;
+  for (int t = 1, pos = 0; pos < maxneed; ++t) {
     const int start = pos + 1;
-    const int slot = start < i0 ? start : start + 1;
-    best = max(best, __ldg(&p.preEF[t]) - G[slot - 1]);
+    i = max(i, start + q);
+    for (;;) {  // thresholds up to slot i lower its need: move right
+      const int a = k < M ? s.thr[k] : n + 1, b = used ? n + 1 : bp;
+      if (min(a, b) > i) break;
+      if (a <= b) ++k; else used = true;
+      ++q;
+      i = start + q;
+    }
+    best = max(best, __ldg(&p.preEF[t]) - G[i - 1]);
     pos += s.cnt[t];
   }
   return best;
 }
 
-// Global ordering (R14) in the general case: merge the pre levels (value
-// PRE_EF(t) - Df, key (j, t-1); levels of equal value grouped) with the
-// moved EFs (INB_F[a_j][k], key (j, c_j + k)) extracted in key order by
-// repeated minimum search above the last key taken.  Fills own[] / rk[]
-// and returns the initial backward shift max_i PREB_EF(rk_i) - D_i.
-__device__ int64_t order_general(const TPlan& p, const int64_t* D, int n, int m, int64_t Df, bool moved, TS& s) {
+__device__ __forceinline__ void assign_slot(const TPlan& p, const int64_t* D, TS& s, int j, int& slot, int64_t& dep_b) {
+  const int r = s.N[j] - s.kb[j];  // rank of this slot's deadline within pipeline j (R15)
+  s.kb[j] += 1;
+  s.own[slot] = (uint8_t)j;
+  s.rk[slot] = (uint8_t)r;
+  dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);  // initial backward shift
+  ++slot;
+}
+
+// Global ordering (R14), PRE_EF strict: pre entries (value PRE_EF(t) - Df,
+// key (j, t-1)) come level by level in pipeline order (active pipelines
+// compacted per level), merged with the moved EFs (INB_F[a_j][k], key
+// (j, c_j + k)) sorted by (value, key).  Fills own[] / rk[]; returns the
+// initial backward shift max_i PREB_EF(rk_i) - D_i.
+__device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t Df, TS& s) {
+  const int rt = p.rt, kmax = p.kmax;
+  auto mval = [&](int q) { return __ldg(&p.inbF[(s.mvj[q] / rt) * kmax + s.mvk[q]]); };
+  auto mkey = [&](int q) { return ((int)s.mvj[q] << 8) | (s.c[s.mvj[q]] + s.mvk[q]); };
+  int nm = 0;
+  for (int j = 0, a = 0, r = 0; j < m; ++j) {
+    const int cj = s.c[j], kfj = s.N[j] - cj;
+    s.kb[j] = 0;
+    for (int k = 0; k < kfj; ++k) {  // insertion sort of the moved entries
+      const int64_t v = __ldg(&p.inbF[a * kmax + k]);
+      const int key = (j << 8) | (cj + k);
+      int q = nm;
+      while (q > 0) {
+        const int64_t pv = mval(q - 1);
+        if (pv < v || (pv == v && mkey(q - 1) < key)) break;
+        s.mvj[q] = s.mvj[q - 1];
+        s.mvk[q] = s.mvk[q - 1];
+        --q;
+      }
+      s.mvj[q] = (uint8_t)j;
+      s.mvk[q] = (uint8_t)k;
+      ++nm;
+    }
+    if (++r == rt) { r = 0; ++a; }
+  }
+  uint8_t* act = s.seen;
+  int na = 0;
+  for (int j = 0; j < m; ++j)
+    if (s.c[j] > 0) act[na++] = (uint8_t)j;
+  int slot = 0, mi = 0;
+  int64_t dep_b = kNegInf;
+  for (int t = 1; na > 0; ++t) {
+    const int64_t v = __ldg(&p.preEF[t]) - Df;
+    int nn = 0;
+    for (int q = 0; q < na; ++q) {
+      const int j = act[q];
+      const int key = (j << 8) | (t - 1);
+      while (mi < nm) {
+        const int64_t mv = mval(mi);
+        if (!(mv < v || (mv == v && mkey(mi) < key))) break;
+        assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
+        ++mi;
+      }
+      assign_slot(p, D, s, j, slot, dep_b);
+      if (s.c[j] > t) act[nn++] = (uint8_t)j;
+    }
+    na = nn;
+  }
+  while (mi < nm) assign_slot(p, D, s, s.mvj[mi++], slot, dep_b);
+  return dep_b;
+}
+
+// Global ordering (R14) for any PRE_EF (levels of equal value grouped, so
+// ties order by (j, t-1)); moved entries extracted in key order by repeated
+// minimum search above the last key taken.
+__device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_t Df, bool moved, TS& s) {
   const int rt = p.rt, kmax = p.kmax;
   int maxc = 0;
   for (int j = 0; j < m; ++j) {
     maxc = max(maxc, (int)s.c[j]);
-    s.seen[j] = 0;
+    s.kb[j] = 0;
   }
   int slot = 0;
   int64_t dep_b = kNegInf, lastv = kNegInf, mv = kInf;
@@ -213,14 +290,6 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int n, int m,
       if (++r == rt) { r = 0; ++a; }
     }
   };
-  auto assign = [&](int j) {  // slot -> pipeline j; rank of its deadline (R15)
-    const int r = s.N[j] - s.seen[j];
-    s.seen[j] += 1;
-    s.own[slot] = (uint8_t)j;
-    s.rk[slot] = (uint8_t)r;
-    dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);
-    ++slot;
-  };
   next_moved();
   for (int t1 = 1; t1 <= maxc;) {
     int t2 = t1;
@@ -231,30 +300,29 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int n, int m,
       for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
         const int key = (j << 8) | (t - 1);
         while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
-          assign(mj);
+          assign_slot(p, D, s, mj, slot, dep_b);
           lastv = mv;
           lastk = mk;
           next_moved();
         }
-        assign(j);
+        assign_slot(p, D, s, j, slot, dep_b);
         lastv = v;
         lastk = key;
       }
     t1 = t2 + 1;
   }
   while (mj >= 0) {
-    assign(mj);
+    assign_slot(p, D, s, mj, slot, dep_b);
     lastv = mv;
     lastk = mk;
     next_moved();
   }
-  (void)n;
   return dep_b;
 }
 
 // Initial backward shift when no forward chain moved and PRE_EF is strict:
-// the order is (t, j), slot of (t, j) gets rank N_j - t + 1; active
-// pipelines compacted level by level (own/rk are not materialised).
+// the order is (t, j), slot of (t, j) gets rank N_j - t + 1; own/rk are not
+// materialised.
 __device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, int m, TS& s) {
   uint8_t* act = s.seen;
   for (int j = 0; j < m; ++j) act[j] = (uint8_t)j;
@@ -291,10 +359,27 @@ struct TStats {
   unsigned v[8];
 };
 
+// findCritical (R11): argmax over pipelines with count > 0 of DEV[row][count],
+// ties -> lowest j.  cnt8 = the per-pipeline counts.
+__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, const uint8_t* cnt8, int m, int& js) {
+  int64_t best = kNegInf;
+  js = -1;
+  const int rt = p.rt, np1 = p.np1;
+#pragma unroll 4
+  for (int j = 0; j < m; ++j) {
+    const int cj = cnt8[j];
+    if (cj > 0) {
+      const int64_t v = __ldg(&dev[(j / rt) * np1 + cj]);
+      if (v > best) { best = v; js = j; }
+    }
+  }
+  return best;
+}
+
 // One candidate, sequentially in this thread.
 __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
                          TStats& st) {
-  const int n = c.n, m = p.m, rt = p.rt, np1 = p.np1, kmax = p.kmax;
+  const int n = c.n, m = p.m, rt = p.rt, kmax = p.kmax;
   // ---------------- coarse init (R9) -------------------------------------
   for (int t = 0; t <= n + 1; ++t) s.cnt[t] = 0;
   for (int j = 0; j < m; ++j) {
@@ -302,62 +387,51 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     s.cnt[s.N[j]] += 1;
   }
   for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
-  int sumc = n, itf = 0, atf = 0, itb = 0, atb = 0;
+  int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
-  int64_t dep = tdep_fwd0(p, G, n, sumc, kInf, s);
+  int64_t dep = tdep_fwd(p, G, n, sumc, n + 1, s, 0);
   int64_t Delta;
   for (;;) {
     ++itf;
-    int64_t dev = kNegInf;
-    int js = -1;
-    for (int j = 0, a = 0, r = 0; j < m; ++j) {  // findCritical, ties -> lowest j (R11)
-      const int cj = s.c[j];
-      if (cj > 0) {
-        const int64_t v = __ldg(&p.devF[a * np1 + cj]);
-        if (v > dev) { dev = v; js = j; }
-      }
-      if (++r == rt) { r = 0; ++a; }
-    }
+    int js;
+    const int64_t dev = critical(p, p.devF, s.c, m, js);  // findCritical (R11)
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
     const int as = js / rt, cjs = s.c[js], kfj = s.N[js] - cjs;
     if (kfj >= (int)__ldg(&p.lenF[as])) break;  // ScheduleKernels fails (R12)
     const int64_t EF = __ldg(&p.inbF[as * kmax + kfj]);
     ++atf;
-    s.c[js] = (uint8_t)(cjs - 1);  // trial move
+    const int bp = first_ge(G, n, EF);  // EF_i + L <= F_i holds for slots >= bp
+    s.c[js] = (uint8_t)(cjs - 1);       // trial move
     s.cnt[cjs] -= 1;
-    const int64_t dep2 = sumc == n ? tdep_fwd0(p, G, n, sumc - 1, EF, s) : tdep_fwd(p, G, n, sumc - 1, EF, s);
+    const int64_t dep2 = tdep_fwd(p, G, n, sumc - 1, bp, s, M);
     if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
       s.c[js] = (uint8_t)cjs;
       s.cnt[cjs] += 1;
       break;
     }
-    if (sumc == n)
-      for (int i = 0; i < n; ++i) s.Qc[i] = 0;
-    for (int i = 0; i < n; ++i) s.Qc[i] += EF <= G[i] ? 1 : 0;
+    int q = M++;  // commit: insert the threshold
+    while (q > 0 && s.thr[q - 1] > bp) {
+      s.thr[q] = s.thr[q - 1];
+      --q;
+    }
+    s.thr[q] = (uint8_t)bp;
     dep = dep2;
     --sumc;
   }
   const int64_t Df = Delta;
   // ---------------- global ordering (R14) -------------------------------
-  const bool moved = sumc < n;
-  bool have_order = moved || !p.strict;
-  int64_t dep_b = have_order ? order_general(p, D, n, m, Df, moved, s) : order_fast(p, D, m, s);
+  bool have_order = M > 0 || !p.strict;
+  int64_t dep_b = !have_order ? order_fast(p, D, m, s)
+                  : p.strict  ? order_strict(p, D, m, Df, s)
+                              : order_general(p, D, m, Df, M > 0, s);
   // ---------------- backward OptimizeSchedule (R15) ------------------------
   int sumcb = n;
   bool init_b = false;
   for (;;) {
     ++itb;
-    int64_t dev = kNegInf;
-    int js = -1;
-    for (int j = 0, a = 0, r = 0; j < m; ++j) {
-      const int cbj = init_b ? s.cb[j] : s.N[j];
-      if (cbj > 0) {
-        const int64_t v = __ldg(&p.devB[a * np1 + cbj]);
-        if (v > dev) { dev = v; js = j; }
-      }
-      if (++r == rt) { r = 0; ++a; }
-    }
+    int js;
+    const int64_t dev = critical(p, p.devB, init_b ? s.cb : s.N, m, js);
     Delta = max((int64_t)0, max(dev, dep_b));
     if (Delta == 0 || sumcb == 0) break;
     const int as = js / rt, kfj = s.N[js] - s.c[js];
@@ -367,7 +441,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     const int64_t EFb = __ldg(&p.inbB[rowoff * kmax + kbj]);
     ++atb;
     if (!have_order) {  // materialise owners and ranks (same order, same initial shift)
-      order_general(p, D, n, m, Df, false, s);
+      order_strict(p, D, m, Df, s);
       have_order = true;
     }
     if (!init_b) {  // backward moves are rare: per-pipeline state on first use
