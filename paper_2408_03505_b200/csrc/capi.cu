@@ -56,10 +56,11 @@ struct Prep {
   int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0;
   int kmax_all = 0;
   int nk_max = 0;
+  int k0_trials = 0;
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_sim, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, o_stats, total_bytes;
+      o_comm_hi, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, o_stats, total_bytes;
   int grid;
 };
 
@@ -144,6 +145,11 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.ntp = pb->n_tp_opts;
   X.nops = 2 * X.n * X.v;
   const int64_t nv = (int64_t)X.n * X.v;
+  for (int s = 0; s < X.p; ++s) {  // K0 warm-up trials: every (stage, w <= Megatron default)
+    const int d = X.v == 1 ? std::min(X.n, X.p - 1 - s)
+                           : X.n == X.p ? X.n * X.v : std::min(X.n * X.v, 2 * (X.p - 1 - s) + (X.v - 1) * X.p);
+    X.k0_trials += d + 1;
+  }
   X.icapc = (int)(nv * X.lc * (runs_of(pb->llm_fwd_layer, 0) + runs_of(pb->llm_bwd_layer, 0)) + 1);
   X.icapm = (int)(nv * X.lc * (runs_of(pb->llm_fwd_layer, 1) + runs_of(pb->llm_bwd_layer, 1)) + 2);
 
@@ -170,7 +176,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
     if (nk > 8192) return fail(OPTIMUS_ERANGE, "encoder has %lld kernels per microbatch (> 8192 supported)", (long long)nk);
     X.nk_max = std::max<int>(X.nk_max, (int)nk);
   }
-  if ((size_t)X.p * 2 * X.v * X.n * 8 + (size_t)X.p * X.nops * 8 > 200 * 1024)
+  if ((size_t)X.p * 2 * X.v * X.n * 8 + (size_t)X.p * X.nops * 8 + 4 * (size_t)X.n * X.v + 16 > 200 * 1024 ||
+      (size_t)X.p * 2 * X.v * X.n > 65535)
     return fail(OPTIMUS_ERANGE, "PP*V*N_mb too large for the K0 shared-memory simulation");
   {
     const size_t ci = (size_t)(std::max(X.icapc, X.icapm) + 31) / 32;
@@ -255,6 +262,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_comm_lo = take((size_t)X.p * X.icapm * 8);
   X.o_comm_hi = take((size_t)X.p * X.icapm * 8);
   X.o_sim = take((size_t)X.p * 4);
+  X.o_k0res = take((size_t)(1 + X.k0_trials) * 8);
   X.o_tables = take((size_t)X.n_tables * 8);
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
@@ -316,6 +324,8 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.comm_lo = (int64_t*)(ws + X.o_comm_lo);
   c.comm_hi = (int64_t*)(ws + X.o_comm_hi);
   c.bestw = (int32_t*)(ws + X.o_sim);
+  c.k0res = (int64_t*)(ws + X.o_k0res);
+  c.k0_trials = X.k0_trials;
   c.tables = (int64_t*)(ws + X.o_tables);
   c.snap = (int64_t*)(ws + X.o_snap);
   c.bfill = (int64_t*)(ws + X.o_bfill);

@@ -31,6 +31,7 @@ struct Cfg {
   int32_t nops;          // 2*n*v ops per stage
   int32_t icapc, icapm;  // interval capacity per stage: compute-free, comm-free
   int32_t kmax_all;      // max kmax over plans
+  int32_t k0_trials;     // sum over stages of (Wdef_s + 1): K0 warm-up trials
   int32_t nk_max;        // max over TP options of the encoder's total kernel count (all layers, all branches)
   int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
   // packed inputs
@@ -54,6 +55,7 @@ struct Cfg {
   int64_t* comm_lo;       // [p][icapm]
   int64_t* comm_hi;       // [p][icapm]
   int32_t* bestw;         // [p] K0 warm-up search: smallest successful w per stage
+  int64_t* k0res;         // [1 + k0_trials] K0 wave: span of each simulation, -1 if it deadlocks
   // plans + tables (K1)
   const PlanDesc* plans;  // [E]
   int64_t* tables;

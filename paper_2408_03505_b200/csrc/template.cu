@@ -40,93 +40,136 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
   return v;
 }
 
-// K0 per-warp shared memory: [optab: p*nops int64][done: p*2*v*n int64].
-// optab[s][pos] packs the op at position pos of stage s for the warp's
-// current warm-up vector: bits 0-23 its own slot in done, 24-47 the slot of
-// its dependency (0xFFFFFF = none), 48 forward, 49 cross-stage dependency.
-constexpr uint64_t kNoDep = 0xFFFFFF;
-constexpr int kFinalWarps = 8;
+// K0 per-simulation shared memory: [vtab: n*v shorts x 2][optab: p*nops
+// uint64][endv: p*2*v*n int64].  vtab maps a virtual id k to its forward
+// chunk and microbatch (R2).  optab[s*nops + pos] packs the op at position
+// pos of stage s for the current warm-up vector: bits 0-15 its slot in
+// endv, 16-31 the slot of its cross-op dependency, 32-47 the slot of the
+// previous op of its stage (0xFFFF = none), 48 forward, 49 the dependency
+// is on another stage (adds pp_p2p).
+constexpr uint64_t kNone = 0xFFFF;
+constexpr int kSimThreads = 256;
+constexpr int kFinalThreads = 256;
 
-__host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int nops, int v, int n) {
-  return (size_t)p * nops * 8 + (size_t)p * 2 * v * n * 8;
+__host__ __device__ __forceinline__ size_t k0_vtab_bytes(int n, int v) { return ((size_t)4 * n * v + 15) & ~size_t(15); }
+__host__ __device__ __forceinline__ size_t k0_sim_bytes(int p, int nops, int v, int n) {
+  return k0_vtab_bytes(n, v) + (size_t)p * nops * 8 + (size_t)p * 2 * v * n * 8;
 }
 
-// Fill the warp's optab for the warm-up vector W (lane-parallel).
-__device__ void build_optab(const Cfg& c, const int* W, size_t base) {
-  uint64_t* tab = reinterpret_cast<uint64_t*>(k0_dsm + base);
-  const int p = c.p, v = c.v, n = c.n, nops = c.nops;
-  for (int i = threadIdx.x & 31; i < p * nops; i += 32) {
-    const int s = i / nops, pos = i % nops;
-    const OpRef op = op_at(p, v, n, W[s], pos);  // Megatron interleaved order (R2)
-    int ds = -1, df = 0, dc = 0;                 // dependency (R2)
-    if (op.fwd) {
-      if (s > 0) { ds = s - 1; df = 1; dc = op.chunk; }
-      else if (op.chunk > 0) { ds = p - 1; df = 1; dc = op.chunk - 1; }
-    } else {
-      if (s < p - 1) { ds = s + 1; df = 0; dc = op.chunk; }
-      else if (op.chunk < v - 1) { ds = 0; df = 0; dc = op.chunk + 1; }
-      else { ds = p - 1; df = 1; dc = v - 1; }
-    }
-    const uint64_t self = ((s * 2 + op.fwd) * v + op.chunk) * n + op.mb;
-    const uint64_t dep = ds < 0 ? kNoDep : (uint64_t)(((ds * 2 + df) * v + dc) * n + op.mb);
-    tab[i] = self | (dep << 24) | ((uint64_t)op.fwd << 48) | ((uint64_t)(ds >= 0 && ds != s) << 49);
+// op at position pos of stage s under warm-up count Ws (R2): its endv slot,
+// dependency slot and whether the dependency is on another stage
+__device__ __forceinline__ void op_slots(int p, int v, int n, int s, int pos, int Ws, const short* vch,
+                                         const short* vmb, int& self, int& dep, int& fwd, int& cross) {
+  const int nv = n * v, r = pos - Ws;
+  int k;
+  if (r < 0) { k = pos; fwd = 1; }
+  else if (r < 2 * (nv - Ws)) { fwd = (r & 1) ? 0 : 1; k = fwd ? Ws + r / 2 : r / 2; }
+  else { fwd = 0; k = (nv - Ws) + (r - 2 * (nv - Ws)); }
+  const int chf = vch[k], mb = vmb[k], ch = fwd ? chf : v - 1 - chf;
+  int ds = -1, df = 0, dc = 0;
+  if (fwd) {
+    if (s > 0) { ds = s - 1; df = 1; dc = ch; }
+    else if (ch > 0) { ds = p - 1; df = 1; dc = ch - 1; }
+  } else {
+    if (s < p - 1) { ds = s + 1; df = 0; dc = ch; }
+    else if (ch < v - 1) { ds = 0; df = 0; dc = ch + 1; }
+    else { ds = p - 1; df = 1; dc = v - 1; }
   }
-  __syncwarp();
+  self = ((s * 2 + fwd) * v + ch) * n + mb;
+  dep = ds < 0 ? (int)kNone : ((ds * 2 + df) * v + dc) * n + mb;
+  cross = ds >= 0 && ds != s;
+}
+
+// Fill vtab and optab for the warm-up vector W (whole block).
+__device__ void build_optab(const Cfg& c, const int* W) {
+  const int p = c.p, v = c.v, n = c.n, nops = c.nops, nv = n * v;
+  short* vch = reinterpret_cast<short*>(k0_dsm);
+  short* vmb = vch + nv;
+  uint64_t* tab = reinterpret_cast<uint64_t*>(k0_dsm + k0_vtab_bytes(n, v));
+  for (int k = threadIdx.x; k < nv; k += blockDim.x) {
+    vch[k] = (short)((k % (p * v)) / p);
+    vmb[k] = (short)((k / (p * v)) * p + (k % p));
+  }
+  __syncthreads();
+  for (int s = 0; s < p; ++s) {
+    const int Ws = W[s];
+    for (int pos = threadIdx.x; pos < nops; pos += blockDim.x) {
+      int self, dep, fwd, cross, pself = (int)kNone, pd, pf, pc;
+      op_slots(p, v, n, s, pos, Ws, vch, vmb, self, dep, fwd, cross);
+      if (pos > 0) op_slots(p, v, n, s, pos - 1, Ws, vch, vmb, pself, pd, pf, pc);
+      tab[s * nops + pos] = (uint64_t)self | ((uint64_t)dep << 16) | ((uint64_t)pself << 32) |
+                            ((uint64_t)fwd << 48) | ((uint64_t)cross << 49);
+    }
+  }
+  __syncthreads();
 }
 
 // ASAP list schedule of the pipeline in optab's fixed per-stage order (R2,
-// R3), one warp, lane = stage.  A trial stops as soon as an op ends after
-// span_limit.  record: also write op starts, F, B.  Returns ok
-// (deadlock-free and within the limit) and the span (max last-op end).
-__device__ void warp_simulate(const Cfg& c, size_t base, bool record, int64_t dur_f, int64_t dur_b,
-                              int64_t span_limit, int64_t* span, int* ok) {
-  const uint64_t* tab = reinterpret_cast<const uint64_t*>(k0_dsm + base);
-  volatile int64_t* done = reinterpret_cast<volatile int64_t*>(k0_dsm + base + (size_t)c.p * c.nops * 8);
-  const int lane = threadIdx.x & 31;
-  const int p = c.p, v = c.v, n = c.n, nops = c.nops;
+// R3), computed by the whole block as a relaxation: every round, each op
+// whose stage predecessor and dependency have ended gets start = max(their
+// ends (+ pp_p2p across stages), T_ag).  A round without progress before
+// every op is placed means the order deadlocks.  record: also write op
+// starts, F, B.  Returns ok and the span (max last-op end).
+__device__ void block_simulate(const Cfg& c, bool record, int64_t dur_f, int64_t dur_b, int64_t* span, int* ok) {
+  __shared__ long long red[kSimThreads / 32];
+  const int p = c.p, v = c.v, n = c.n, nops = c.nops, total = p * nops;
+  const uint64_t* tab = reinterpret_cast<const uint64_t*>(k0_dsm + k0_vtab_bytes(n, v));
+  volatile int64_t* endv = reinterpret_cast<volatile int64_t*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)total * 8);
   const int sz = p * 2 * v * n;
-  for (int i = lane; i < sz; i += 32) done[i] = -1;
-  __syncwarp();
-  int pos = 0;
-  int64_t fr = max((int64_t)0, c.T_ag);  // every op starts after the DP all-gather (R3)
-  const int64_t pp2p = c.pp_p2p;
-  bool over = false;
-  const uint64_t* row = tab + (size_t)min(lane, p - 1) * nops;
-  for (;;) {
-    bool prog = false;
-    if (lane < p) {
-      while (pos < nops) {
-        const uint64_t e = row[pos];
-        const int dep = (int)((e >> 24) & kNoDep);
-        int64_t t = fr;
-        if (dep != (int)kNoDep) {
-          const int64_t de = done[dep];
-          if (de < 0) break;
-          t = max(t, de + ((e >> 49) & 1 ? pp2p : 0));
+  const int64_t T_ag = max((int64_t)0, c.T_ag), pp2p = c.pp_p2p;
+  for (int i = threadIdx.x; i < sz; i += blockDim.x) endv[i] = -1;
+  __syncthreads();
+  int left = 1;
+  while (left) {
+    int prog = 0;
+    left = 0;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const uint64_t e = tab[i];
+      const int self = (int)(e & kNone);
+      if (endv[self] >= 0) continue;
+      int64_t t = T_ag;  // every op starts after the DP all-gather (R3)
+      const int prev = (int)((e >> 32) & kNone), dep = (int)((e >> 16) & kNone);
+      if (prev != (int)kNone) {
+        const int64_t pe = endv[prev];
+        if (pe < 0) { left = 1; continue; }
+        t = max(t, pe);
+      }
+      if (dep != (int)kNone) {
+        const int64_t de = endv[dep];
+        if (de < 0) { left = 1; continue; }
+        t = max(t, de + ((e >> 49) & 1 ? pp2p : 0));
+      }
+      const bool fwd = (e >> 48) & 1;
+      endv[self] = t + (fwd ? dur_f : dur_b);
+      prog = 1;
+      if (record) {
+        c.opstart[i] = t;  // optab is stage-major, like opstart
+        const int mb = self % n, ch = (self / n) % v;
+        if (i < nops && ch == 0) {
+          if (fwd) c.F[mb] = t;               // F_i: start of F(stage 0, chunk 0, i) (R4)
+          else c.B[mb] = t + dur_b;           // B_i: end of B(stage 0, chunk 0, i)
         }
-        const bool fwd = (e >> 48) & 1;
-        const int64_t fin = t + (fwd ? dur_f : dur_b);
-        if (fin > span_limit) { over = true; break; }
-        const int self = (int)(e & kNoDep);
-        done[self] = fin;
-        if (record) {
-          c.opstart[(int64_t)lane * nops + pos] = t;
-          const int mb = self % n, ch = (self / n) % v;
-          if (lane == 0 && ch == 0) {
-            if (fwd) c.F[mb] = t;    // F_i: start of F(stage 0, chunk 0, i) (R4)
-            else c.B[mb] = fin;      // B_i: end of B(stage 0, chunk 0, i)
-          }
-        }
-        fr = fin;
-        ++pos;
-        prog = true;
       }
     }
-    __syncwarp();
-    if (__any_sync(0xffffffffu, over) || !__any_sync(0xffffffffu, prog)) break;
+    prog = __syncthreads_or(prog);
+    left = __syncthreads_or(left);
+    if (left && !prog) break;  // deadlock
   }
-  *ok = __all_sync(0xffffffffu, lane >= p || pos == nops) && !__any_sync(0xffffffffu, over);
-  *span = warp_max64(lane < p ? fr : 0);
+  *ok = !left;
+  // span: max over stages of the last op's end
+  int64_t mx = 0;
+  for (int s = threadIdx.x; s < p; s += blockDim.x) mx = max(mx, (int64_t)endv[tab[s * nops + nops - 1] & kNone]);
+  mx = warp_max64(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+    x = warp_max64(x);
+    if (threadIdx.x == 0) red[0] = x;
+  }
+  __syncthreads();
+  *span = red[0];
+  __syncthreads();
 }
 
 __device__ __forceinline__ int default_w(int p, int v, int n, int s) {  // Megatron default warm-up (R2)
@@ -146,111 +189,119 @@ __device__ __forceinline__ void dur_fb(const Cfg& c, int64_t& f, int64_t& b) {
   b = (int64_t)c.lc * list_sum(c, 1);
 }
 
-// K0a: default warm-up, default schedule (span to preserve), reset of the search.
-__global__ void __launch_bounds__(32) k0_default(Cfg c) {
+// K0a, one block per simulation: block 0 the default warm-up (its span must
+// be preserved; it is the final schedule under policy 0), block 1 + t trial
+// t = (s, w) of GetEncLLMDep's warm-up adjustment (R5: for s = p-1
+// .. 0 the smallest w in [0, Wdef_s] keeping the schedule deadlock-free with
+// the default span).  All stage phases run at once, each assuming the later
+// stages take their guessed value; the trial with every stage at its guess
+// records its schedule (it is the final one when K0b verifies every guess).
+// res[b] = span, or -1 if the schedule deadlocks.
+__global__ void __launch_bounds__(kSimThreads) k0_wave(Cfg c) {
   __shared__ int Wsm[kMaxP];
-  const int lane = threadIdx.x;
+  const int p = c.p, v = c.v, n = c.n;
+  int s = -1, w = 0;
+  if (blockIdx.x > 0) {
+    if (c.policy != 1) return;
+    s = 0;
+    w = blockIdx.x - 1;
+    while (s < p && w > default_w(p, v, n, s)) { w -= default_w(p, v, n, s) + 1; ++s; }
+    if (s >= p) return;
+  }
   int64_t df, db;
   dur_fb(c, df, db);
-  if (lane < c.p) {
-    const int w = default_w(c.p, c.v, c.n, lane);
-    c.Wdef[lane] = w;
-    c.W[lane] = w;
-    c.bestw[lane] = INT32_MAX;
-    Wsm[lane] = w;
+  if (threadIdx.x < p) {
+    const int t = threadIdx.x, d = default_w(p, v, n, t);
+    Wsm[t] = s < 0 || t < s ? d : t == s ? w : guess_w(p, v, n, t);
+    if (blockIdx.x == 0) c.Wdef[t] = d;
   }
-  __syncwarp();
-  build_optab(c, Wsm, 0);
+  __syncthreads();
+  build_optab(c, Wsm);
+  const bool all_guess = s == 0 && w == guess_w(p, v, n, 0);
+  const bool record = c.policy == 1 ? all_guess : blockIdx.x == 0;
   int64_t sp;
   int ok;
-  warp_simulate(c, 0, false, df, db, INT64_MAX, &sp, &ok);
-  if (lane == 0) { c.scal[0] = sp; c.scal[2] = ok; }
+  block_simulate(c, record, df, db, &sp, &ok);
+  if (threadIdx.x == 0) c.k0res[blockIdx.x] = ok ? sp : -1;
 }
 
-// K0b: GetEncLLMDep's warm-up adjustment (R5) is, for s = p-1 .. 0,
-// the smallest w in [0, Wdef_s] keeping the schedule deadlock-free with the
-// default span.  All stage phases run here at once, one trial (s, w) per
-// block, each assuming the later stages take their guessed value; K0c
-// verifies (a stage's result is exact when every later guess was right).
-__global__ void __launch_bounds__(32) k0_wave(Cfg c) {
-  __shared__ int Wsm[kMaxP];
-  const int lane = threadIdx.x, p = c.p, v = c.v, n = c.n;
-  if (c.policy != 1 || c.scal[2] == 0) return;
-  int s = 0, w = blockIdx.x;
-  while (s < p && w > default_w(p, v, n, s)) { w -= default_w(p, v, n, s) + 1; ++s; }
-  if (s >= p) return;
-  int64_t df, db;
-  dur_fb(c, df, db);
-  if (lane < p) Wsm[lane] = lane < s ? default_w(p, v, n, lane) : lane == s ? w : guess_w(p, v, n, lane);
-  __syncwarp();
-  build_optab(c, Wsm, 0);
-  int64_t sp;
-  int ok;
-  warp_simulate(c, 0, false, df, db, c.scal[0], &sp, &ok);
-  if (lane == 0 && ok && sp == c.scal[0]) atomicMin(&c.bestw[s], w);
-}
-
-// K0c: verify the wave from the last stage down, redo the phases below the
-// first wrong guess exactly (kFinalWarps trials at a time), then the final
-// schedule with its op starts, F_i, B_i and T_end.
-__global__ void __launch_bounds__(kFinalWarps * 32) k0_final(Cfg c) {
-  __shared__ int Wcur[kMaxP];
-  __shared__ int Wsm[kFinalWarps][kMaxP];
-  __shared__ int best_sm;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, p = c.p, v = c.v, n = c.n;
-  const int nwarps = blockDim.x >> 5;
-  if (c.scal[2] == 0) return;  // default schedule deadlocks: template fails
-  const size_t base = (size_t)warp * k0_warp_bytes(p, c.nops, v, n);
-  int64_t df, db;
-  dur_fb(c, df, db);
-  const int64_t span_def = c.scal[0];
-  int s0 = -1;
-  if (c.policy == 1) {
-    int s = p - 1;
-    while (s >= 0 && c.bestw[s] == guess_w(p, v, n, s)) --s;
-    s0 = s;  // stages > s0 verified; stage s0 exact (its later stages were right)
+// K0b: verify the wave from the last stage down; in the common case the
+// recorded all-guess schedule is the final one.  Otherwise redo the phases
+// below the first wrong guess exactly, one trial at a time, and record the
+// final schedule.  Writes W, T_end and the ok flag.
+__global__ void __launch_bounds__(kFinalThreads) k0_final(Cfg c) {
+  __shared__ int Wcur[kMaxP], firstb[kMaxP + 1];
+  __shared__ int s0_sm;
+  const int p = c.p, v = c.v, n = c.n;
+  const int64_t span_def = c.k0res[0];
+  if (threadIdx.x == 0) c.scal[0] = span_def;
+  if (span_def < 0) {  // default schedule deadlocks: template fails
+    if (threadIdx.x == 0) c.scal[2] = 0;
+    return;
   }
+  int64_t df, db;
+  dur_fb(c, df, db);
+  if (threadIdx.x == 0) {
+    int base = 1;
+    for (int s = 0; s < p; ++s) { firstb[s] = base; base += default_w(p, v, n, s) + 1; }
+  }
+  __syncthreads();
+  if (c.policy == 1 && threadIdx.x < p) {  // smallest successful w per stage (speculative)
+    const int s = threadIdx.x;
+    int best = INT32_MAX;
+    for (int x = 0; x <= default_w(p, v, n, s); ++x)
+      if (c.k0res[firstb[s] + x] == span_def) { best = x; break; }
+    c.bestw[s] = best;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = -1;
+    if (c.policy == 1) {
+      s = p - 1;
+      while (s >= 0 && c.bestw[s] == guess_w(p, v, n, s)) --s;
+    }
+    s0_sm = s;  // stages > s0 verified; stage s0 exact (its later stages were right)
+  }
+  __syncthreads();
+  const int s0 = s0_sm;
   if (threadIdx.x < p) {
     const int t = threadIdx.x;
     Wcur[t] = c.policy != 1 ? default_w(p, v, n, t)
                             : t > s0 ? guess_w(p, v, n, t) : t == s0 ? c.bestw[t] : default_w(p, v, n, t);
   }
   __syncthreads();
-  for (int s = s0 - 1; s >= 0; --s) {  // exact sequential phases (rarely needed)
-    const int wd = default_w(p, v, n, s);
-    for (int b = 0; b <= wd; b += nwarps) {
-      if (threadIdx.x == 0) best_sm = INT32_MAX;
+  if (c.policy != 1 || s0 < 0) {  // the recorded schedule (default, or all guesses verified) is final
+    if (threadIdx.x < p) c.W[threadIdx.x] = Wcur[threadIdx.x];
+    if (threadIdx.x == 0) {
+      c.scal[1] = span_def + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3); span kept by R5
+      c.scal[2] = 1;
+    }
+    return;
+  }
+  __shared__ int Wt[kMaxP];
+  for (int s = s0 - 1; s >= 0; --s) {  // exact sequential phases
+    for (int w = 0; w <= default_w(p, v, n, s); ++w) {
+      if (threadIdx.x < p) Wt[threadIdx.x] = threadIdx.x == s ? w : Wcur[threadIdx.x];
       __syncthreads();
-      const int w = b + warp;
-      if (w <= wd) {
-        if (lane < p) Wsm[warp][lane] = lane == s ? w : Wcur[lane];
-        __syncwarp();
-        build_optab(c, Wsm[warp], base);
-        int64_t sp;
-        int ok;
-        warp_simulate(c, base, false, df, db, span_def, &sp, &ok);
-        if (lane == 0 && ok && sp == span_def) atomicMin(&best_sm, w);
-      }
-      __syncthreads();
-      const int bw = best_sm;
-      __syncthreads();
-      if (bw != INT32_MAX) {
-        if (threadIdx.x == 0) Wcur[s] = bw;
+      build_optab(c, Wt);
+      int64_t sp;
+      int ok;
+      block_simulate(c, false, df, db, &sp, &ok);
+      if (ok && sp == span_def) {  // uniform over the block
+        if (threadIdx.x == 0) Wcur[s] = w;
         __syncthreads();
         break;
       }
     }
   }
-  if (warp == 0) {
-    build_optab(c, Wcur, 0);
-    int64_t sp;
-    int ok;
-    warp_simulate(c, 0, true, df, db, INT64_MAX, &sp, &ok);
-    if (lane < p) c.W[lane] = Wcur[lane];
-    if (lane == 0) {
-      c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
-      c.scal[2] = ok;
-    }
+  build_optab(c, Wcur);
+  int64_t sp;
+  int ok;
+  block_simulate(c, true, df, db, &sp, &ok);
+  if (threadIdx.x < p) c.W[threadIdx.x] = Wcur[threadIdx.x];
+  if (threadIdx.x == 0) {
+    c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
+    c.scal[2] = ok;
   }
 }
 
@@ -389,22 +440,14 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
 }  // namespace
 
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
-  const size_t per = k0_warp_bytes(c.p, c.nops, c.v, c.n);
-  if (per > 200 * 1024) return cudaErrorInvalidConfiguration;
-  const int fw = (int)std::max<size_t>(1, std::min<size_t>(kFinalWarps, (200 * 1024) / per));
-  cudaFuncSetAttribute(k0_default, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
-  cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
-  cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(per * fw));
-  int trials = 0;
-  for (int s = 0; s < c.p; ++s) {
-    const int p = c.p, v = c.v, n = c.n;
-    trials += (v == 1 ? std::min(n, p - 1 - s) : n == p ? n * v : std::min(n * v, 2 * (p - 1 - s) + (v - 1) * p)) + 1;
-  }
-  k0_default<<<1, 32, per, st>>>(c);
-  k0_wave<<<std::max(1, trials), 32, per, st>>>(c);
-  k0_final<<<1, 32 * fw, per * fw, st>>>(c);
+  const size_t smem = k0_sim_bytes(c.p, c.nops, c.v, c.n);
+  if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
+  cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k0_wave<<<1 + c.k0_trials, kSimThreads, smem, st>>>(c);
+  k0_final<<<1, kFinalThreads, smem, st>>>(c);
   k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int), st>>>(c);
-  if (launches) *launches += 4;
+  if (launches) *launches += 3;
   return cudaGetLastError();
 }
 
