@@ -210,6 +210,8 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the single JSON line
     dist = None
     if world > 1:
         import torch.distributed as dist

@@ -373,13 +373,21 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
     return fail(OPTIMUS_ENOSPACE, "workspace has %zu bytes, needs %zu", bytes, X.total_bytes);
   }
   int dev = 0;
-  cudaDeviceProp prop;
+  int sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaGetDeviceProperties(&prop, dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
-  c->sms = prop.multiProcessorCount;
-  c->grid = std::min(4096, eval_grid(c->sms));
-  c->grid_thread = std::min(4096, eval_thread_grid(c->sms));
+  c->sms = sms;
+  {  // occupancy-derived persistent grids, computed once per process and SM count
+    static int cached_sms = -1, cached_grid = 0, cached_grid_thread = 0;
+    if (cached_sms != sms) {
+      cached_grid = std::min(4096, eval_grid(sms));
+      cached_grid_thread = std::min(4096, eval_thread_grid(sms));
+      cached_sms = sms;
+    }
+    c->grid = cached_grid;
+    c->grid_thread = cached_grid_thread;
+  }
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
   cudaStream_t st = (cudaStream_t)cuda_stream;

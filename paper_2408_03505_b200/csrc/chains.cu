@@ -107,11 +107,15 @@ struct VR {
 };
 
 // A window of 32 consecutive intervals in registers (lane l = interval
-// base+l) plus the prefetched next window.
+// base+l) plus the prefetched next window, and the "current" interval of
+// the chain-stage as warp-uniform scalars (cur = -1: none): the interval
+// the last kernel of this resource went into; every earlier interval ends
+// at or before `ready` from then on, so first fit can start there.
 struct Win {
-  int base;
+  int base, cur;
   bool dirty;
   int64_t lo, hi, nlo, nhi;
+  int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative)
 };
 
 template <bool M>
@@ -129,13 +133,20 @@ __device__ __forceinline__ void win_fetch(const VR<M>& V, int b, int64_t& lo, in
 template <bool M>
 __device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
   w.base = b;
+  w.cur = -1;
   w.dirty = false;
   win_fetch(V, b, w.lo, w.hi);
   win_fetch(V, b + 32, w.nlo, w.nhi);
 }
 
+__device__ __forceinline__ void win_sync_cur(Win& w) {
+  if (w.cur >= 0 && (threadIdx.x & 31) == w.cur - w.base) w.lo = w.clo;
+  w.cur = -1;
+}
+
 template <bool M>
 __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
+  win_sync_cur(w);
   if (!w.dirty) return;
   const int lane = threadIdx.x & 31;
   for (int i = V.hw + lane; i < w.base; i += 32) V.fill[i] = V.start_at(i);  // gap fill
@@ -148,16 +159,28 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
 
 // Place one kernel of duration d at or after `ready` (R12): the first
 // interval (time order) with end > ready and max(ready, lo) + d <= end.
+// Fast path: the current interval (uniform scalars); else a ballot over the
+// 32-interval window, then the following windows.
 template <bool M>
 __device__ __forceinline__ bool place(VR<M>& V, Win& w, int64_t d, int64_t& ready) {
-  const int lane = threadIdx.x & 31;
+  if (w.cur >= 0) {
+    const int64_t x = max(ready, w.clo);
+    if (x + d <= w.chi) {
+      w.clo = x + d;
+      ready = x + d;
+      return true;
+    }
+    win_sync_cur(w);
+  }
   for (;;) {
     const int64_t x = max(ready, w.lo);
     const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
     if (b) {
       const int f = __ffs(b) - 1;
       const int64_t xf = __shfl_sync(FULL, x, f);
-      if (lane == f) w.lo = xf + d;
+      w.chi = __shfl_sync(FULL, w.hi, f);
+      w.cur = w.base + f;
+      w.clo = xf + d;
       w.dirty = true;
       ready = xf + d;
       return true;
@@ -441,8 +464,12 @@ cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_uni
   L.KM = std::max(1, c.kmax_all);
   const size_t smem = k1_smem_bytes(L);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-  cudaFuncSetAttribute(k1_chains<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k1_chains<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attrs = false;  // opt in to large dynamic shared memory once per process
+  if (!attrs) {
+    cudaFuncSetAttribute(k1_chains<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k1_chains<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attrs = true;
+  }
   // one block per unit, one warp per stage of the widest plan
   if (fwd_units > 0) k1_chains<false><<<(unsigned)fwd_units, 32 * c.p, smem, st>>>(c, fwd_units, L);
   if (bwd_units > 0) k1_chains<true><<<(unsigned)bwd_units, 32 * c.p, smem, st>>>(c, bwd_units, L);

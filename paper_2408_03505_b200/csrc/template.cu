@@ -442,8 +442,12 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
   const size_t smem = k0_sim_bytes(c.p, c.nops, c.v, c.n);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-  cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attrs = false;  // opt in to large dynamic shared memory once per process
+  if (!attrs) {
+    cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attrs = true;
+  }
   k0_wave<<<1 + c.k0_trials, kSimThreads, smem, st>>>(c);
   k0_final<<<1, kFinalThreads, smem, st>>>(c);
   k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int), st>>>(c);
