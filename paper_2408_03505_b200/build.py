@@ -18,7 +18,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in SRC + HDR)
     if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= newest:
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *SRC]
+    extra = os.environ.get("OPTIMUS_NVCC_EXTRA", "").split()  # tuning sweeps only, e.g. -DK2T_MINB=5
+    cmd = [NVCC, *FLAGS, *extra, "-o", OUT + ".tmp", *SRC]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)

@@ -23,10 +23,18 @@ namespace {
 
 constexpr int kTThreads = 128;
 constexpr int kTRun = 8;                  // consecutive candidates per thread
-constexpr int kTStrideW = 97;             // per-thread scratch: 97 words (odd)
-constexpr int kTStride = kTStrideW * 4;   // = 388 bytes
+#ifndef K2T_MINB
+#define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
+#endif
+constexpr int kTStrideW = 65;             // per-thread scratch: 65 words (odd)
+constexpr int kTStride = kTStrideW * 4;   // = 260 bytes
 
-// Per-thread scratch (bytes): N c cnt[34] thr own rk cb kb Qcb seen mvj mvk
+// Per-thread scratch (bytes 0..255).  The three phases of one candidate use
+// disjoint live sets, so bytes 64..255 are shared between them:
+//   all      N[0..31] c[32..63]
+//   forward  cnt[64..97] thr[98..129]
+//   ordering seen[64..95] kb[96..127] mvj[128..159] mvk[160..191] own[192..223] rk[224..255]
+//   backward cb[64..95] Qcb[96..127] own rk   (kb_j = N_j - cb_j is implied)
 struct TS {
   uint8_t* N;     // composition N_j
   uint8_t* c;     // coarse (not yet moved) forward microbatches c_j
@@ -35,9 +43,9 @@ struct TS {
   uint8_t* own;   // owner pipeline of LLM microbatch slot i (global ordering)
   uint8_t* rk;    // rank of D_i within its owner's sorted deadlines
   uint8_t* cb;    // coarse backward microbatches per pipeline
-  uint8_t* kb;    // committed backward chains per pipeline (ordering: slots given so far)
+  uint8_t* kb;    // ordering: slots given to each pipeline so far
   uint8_t* Qcb;   // Qcb[i] = #{owner's moved backward EF <= D_i}
-  uint8_t* seen;  // ordering: active pipeline list / slots given
+  uint8_t* seen;  // ordering: active pipeline list
   uint8_t* mvj;   // ordering: moved entries sorted by (value, key): pipeline
   uint8_t* mvk;   //                                                  chain index
 };
@@ -48,14 +56,14 @@ __device__ __forceinline__ TS ts_at(unsigned char* b) {
   s.c = b + 32;
   s.cnt = b + 64;
   s.thr = b + 98;
-  s.own = b + 130;
-  s.rk = b + 162;
-  s.cb = b + 194;
-  s.kb = b + 226;
-  s.Qcb = b + 258;
-  s.seen = b + 290;
-  s.mvj = b + 322;
-  s.mvk = b + 354;
+  s.seen = b + 64;
+  s.kb = b + 96;
+  s.mvj = b + 128;
+  s.mvk = b + 160;
+  s.own = b + 192;
+  s.rk = b + 224;
+  s.cb = b + 64;
+  s.Qcb = b + 96;
   return s;
 }
 
@@ -435,7 +443,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     Delta = max((int64_t)0, max(dev, dep_b));
     if (Delta == 0 || sumcb == 0) break;
     const int as = js / rt, kfj = s.N[js] - s.c[js];
-    const int kbj = init_b ? s.kb[js] : 0;
+    const int kbj = init_b ? s.N[js] - s.cb[js] : 0;
     const int64_t rowoff = (int64_t)as * (kmax + 1) + kfj;
     if (kbj >= (int)__ldg(&p.lenB[rowoff])) break;
     const int64_t EFb = __ldg(&p.inbB[rowoff * kmax + kbj]);
@@ -445,7 +453,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
       have_order = true;
     }
     if (!init_b) {  // backward moves are rare: per-pipeline state on first use
-      for (int j = 0; j < m; ++j) { s.cb[j] = s.N[j]; s.kb[j] = 0; }
+      for (int j = 0; j < m; ++j) s.cb[j] = s.N[j];
       for (int i = 0; i < n; ++i) s.Qcb[i] = 0;
       init_b = true;
     }
@@ -453,7 +461,6 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (dep2 > Delta) break;
     for (int i = 0; i < n; ++i) s.Qcb[i] += (s.own[i] == js && EFb <= D[i]) ? 1 : 0;
     s.cb[js] -= 1;
-    s.kb[js] += 1;
     dep_b = dep2;
     --sumcb;
   }
@@ -473,7 +480,7 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
 }
 
 template <bool EXPLICIT>
-__global__ void __launch_bounds__(kTThreads) k2_eval_thread(Cfg c, EvalArgs A) {
+__global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[kMaxN], D[kMaxN];
   __shared__ long long bl_sm[kTThreads / 32];
