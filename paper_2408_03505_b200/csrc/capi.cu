@@ -220,6 +220,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
         d.preB = toff; toff += (int64_t)P * np1;
         d.devF = toff; toff += (int64_t)d.rp * np1;
         d.devB = toff; toff += (int64_t)d.rp * np1;
+        d.devK = toff; toff += (int64_t)d.rp * np1;
         d.inbF = toff; toff += (int64_t)d.rp * d.kmax;
         d.lenF = toff; toff += d.rp;
         d.inbB = toff; toff += (int64_t)d.rp * (d.kmax + 1) * d.kmax;

@@ -81,6 +81,20 @@ __global__ void k_plan_tables(Cfg c) {
     c.tables[pd.devF + i] = df;
     c.tables[pd.devB + i] = db;
   }
+  __syncthreads();
+  // order ranks of the DEV entries (K2's findCritical compares 32-bit keys
+  // rank << 5 | 31 - j): rank = #{entries < v}, >= rp for cnt > 0, 0 at cnt 0
+  const int V = pd.rp * (n + 1);
+  uint32_t* key = reinterpret_cast<uint32_t*>(c.tables + pd.devK);
+  for (int i = threadIdx.x; i < 2 * V; i += blockDim.x) {
+    const int64_t* dv = c.tables + (i < V ? pd.devF : pd.devB);
+    const int ii = i < V ? i : i - V;
+    const int64_t v = dv[ii];
+    uint32_t r = 0;
+    if (ii % (n + 1) != 0)
+      for (int q = 0; q < V; ++q) r += dv[q] < v ? 1u : 0u;
+    key[i] = r;
+  }
 }
 
 // ------------------------------------------------------ first-fit machinery

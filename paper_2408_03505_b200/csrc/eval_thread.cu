@@ -75,6 +75,8 @@ struct TPlan {
   const int64_t* preBEF;  // PREB_EF(t)
   const int64_t* devF;
   const int64_t* devB;
+  const uint32_t* keyF;   // order ranks of devF / devB (0 at count 0)
+  const uint32_t* keyB;
   const int64_t* inbF;
   const int64_t* lenF;
   const int64_t* inbB;
@@ -95,6 +97,8 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.preBEF = c.tables + d.preB + (int64_t)(d.P - 1) * (c.n + 1);
   p.devF = c.tables + d.devF;
   p.devB = c.tables + d.devB;
+  p.keyF = reinterpret_cast<const uint32_t*>(c.tables + d.devK);
+  p.keyB = p.keyF + (int64_t)d.rp * (c.n + 1);
   p.inbF = c.tables + d.inbF;
   p.lenF = c.tables + d.lenF;
   p.inbB = c.tables + d.inbB;
@@ -368,20 +372,22 @@ struct TStats {
 };
 
 // findCritical (R11): argmax over pipelines with count > 0 of DEV[row][count],
-// ties -> lowest j.  cnt8 = the per-pipeline counts.
-__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, const uint8_t* cnt8, int m, int& js) {
-  int64_t best = kNegInf;
-  js = -1;
+// ties -> lowest j.  cnt8 = the per-pipeline counts.  Compares the 32-bit
+// keys rank(DEV[row][count]) << 5 | (31 - j) (m <= 32): the max key is the
+// max DEV at the lowest j; rank 0 (count 0) never wins over a count > 0.
+__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, const uint32_t* key, const uint8_t* cnt8,
+                                            int m, int& js) {
   const int rt = p.rt, np1 = p.np1;
+  uint32_t best = 0;
+  int base = 0, r = 0;
 #pragma unroll 4
   for (int j = 0; j < m; ++j) {
-    const int cj = cnt8[j];
-    if (cj > 0) {
-      const int64_t v = __ldg(&dev[(j / rt) * np1 + cj]);
-      if (v > best) { best = v; js = j; }
-    }
+    best = max(best, (__ldg(&key[base + cnt8[j]]) << 5) | (uint32_t)(31 - j));
+    if (++r == rt) { r = 0; base += np1; }
   }
-  return best;
+  if (best < 32u) { js = -1; return kNegInf; }
+  js = 31 - (int)(best & 31u);
+  return __ldg(&dev[(js / rt) * np1 + cnt8[js]]);
 }
 
 // One candidate, sequentially in this thread.
@@ -402,7 +408,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (;;) {
     ++itf;
     int js;
-    const int64_t dev = critical(p, p.devF, s.c, m, js);  // findCritical (R11)
+    const int64_t dev = critical(p, p.devF, p.keyF, s.c, m, js);  // findCritical (R11)
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
     const int as = js / rt, cjs = s.c[js], kfj = s.N[js] - cjs;
@@ -439,7 +445,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (;;) {
     ++itb;
     int js;
-    const int64_t dev = critical(p, p.devB, init_b ? s.cb : s.N, m, js);
+    const int64_t dev = critical(p, p.devB, p.keyB, init_b ? s.cb : s.N, m, js);
     Delta = max((int64_t)0, max(dev, dep_b));
     if (Delta == 0 || sumcb == 0) break;
     const int as = js / rt, kfj = s.N[js] - s.c[js];

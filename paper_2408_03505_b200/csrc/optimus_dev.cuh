@@ -22,6 +22,7 @@ struct PlanDesc {
   uint64_t first, count;
   // offsets, in int64 elements, of this plan's tables from Cfg::tables
   int64_t preF, preB, devF, devB, inbF, lenF, inbB, lenB;
+  int64_t devK;       // rp*(n+1) words: uint32 order ranks of DEV_F then DEV_B (0 at cnt 0)
   int64_t slot_base;  // first K1 scratch slot of this plan
 };
 
