@@ -69,6 +69,7 @@ __device__ __forceinline__ TS ts_at(unsigned char* b) {
 
 struct TPlan {
   int e, P, rt, m, kmax, np1;
+  unsigned rtm;            // row of pipeline j = (j * rtm) >> 16 (exact for j < 32, rt <= 32)
   bool strict;            // PRE_EF strictly increasing: pre entries order by (t, j)
   uint64_t first, count;
   const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
@@ -83,11 +84,14 @@ struct TPlan {
   const int64_t* lenB;
 };
 
+__device__ __forceinline__ int row_of(const TPlan& p, int j) { return (int)(((unsigned)j * p.rtm) >> 16); }
+
 __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   const PlanDesc& d = c.plans[e];
   p.e = e;
   p.P = d.P;
   p.rt = d.rt;
+  p.rtm = 65536u / (unsigned)d.rt + 1u;
   p.m = d.m;
   p.kmax = d.kmax;
   p.np1 = c.n + 1;
@@ -221,7 +225,7 @@ __device__ __forceinline__ void assign_slot(const TPlan& p, const int64_t* D, TS
 // initial backward shift max_i PREB_EF(rk_i) - D_i.
 __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t Df, TS& s) {
   const int rt = p.rt, kmax = p.kmax;
-  auto mval = [&](int q) { return __ldg(&p.inbF[(s.mvj[q] / rt) * kmax + s.mvk[q]]); };
+  auto mval = [&](int q) { return __ldg(&p.inbF[row_of(p, s.mvj[q]) * kmax + s.mvk[q]]); };
   auto mkey = [&](int q) { return ((int)s.mvj[q] << 8) | (s.c[s.mvj[q]] + s.mvk[q]); };
   int nm = 0;
   for (int j = 0, a = 0, r = 0; j < m; ++j) {
@@ -371,6 +375,14 @@ struct TStats {
   unsigned v[8];
 };
 
+// decode a findCritical key: pipeline js and its DEV value (-inf, js = -1 if none)
+__device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev, const uint8_t* cnt8, uint32_t best,
+                                              int& js) {
+  if (best < 32u) { js = -1; return kNegInf; }
+  js = 31 - (int)(best & 31u);
+  return __ldg(&dev[row_of(p, js) * p.np1 + cnt8[js]]);
+}
+
 // findCritical (R11): argmax over pipelines with count > 0 of DEV[row][count],
 // ties -> lowest j.  cnt8 = the per-pipeline counts.  Compares the 32-bit
 // keys rank(DEV[row][count]) << 5 | (31 - j) (m <= 32): the max key is the
@@ -385,9 +397,7 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, 
     best = max(best, (__ldg(&key[base + cnt8[j]]) << 5) | (uint32_t)(31 - j));
     if (++r == rt) { r = 0; base += np1; }
   }
-  if (best < 32u) { js = -1; return kNegInf; }
-  js = 31 - (int)(best & 31u);
-  return __ldg(&dev[(js / rt) * np1 + cnt8[js]]);
+  return crit_value(p, dev, cnt8, best, js);
 }
 
 // One candidate, sequentially in this thread.
@@ -396,9 +406,19 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   const int n = c.n, m = p.m, rt = p.rt, kmax = p.kmax;
   // ---------------- coarse init (R9) -------------------------------------
   for (int t = 0; t <= n + 1; ++t) s.cnt[t] = 0;
-  for (int j = 0; j < m; ++j) {
-    s.c[j] = s.N[j];
-    s.cnt[s.N[j]] += 1;
+  // the first findCritical of both phases runs on N: one pass for both keys
+  uint32_t kf0 = 0, kb0 = 0;
+  {
+    int base = 0, r = 0;
+    for (int j = 0; j < m; ++j) {
+      const int Nj = s.N[j];
+      s.c[j] = (uint8_t)Nj;
+      s.cnt[Nj] += 1;
+      const uint32_t lo = (uint32_t)(31 - j);
+      kf0 = max(kf0, (__ldg(&p.keyF[base + Nj]) << 5) | lo);
+      kb0 = max(kb0, (__ldg(&p.keyB[base + Nj]) << 5) | lo);
+      if (++r == rt) { r = 0; base += p.np1; }
+    }
   }
   for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
   int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
@@ -408,10 +428,11 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (;;) {
     ++itf;
     int js;
-    const int64_t dev = critical(p, p.devF, p.keyF, s.c, m, js);  // findCritical (R11)
+    const int64_t dev = itf == 1 ? crit_value(p, p.devF, s.c, kf0, js)  // findCritical (R11)
+                                 : critical(p, p.devF, p.keyF, s.c, m, js);
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
-    const int as = js / rt, cjs = s.c[js], kfj = s.N[js] - cjs;
+    const int as = row_of(p, js), cjs = s.c[js], kfj = s.N[js] - cjs;
     if (kfj >= (int)__ldg(&p.lenF[as])) break;  // ScheduleKernels fails (R12)
     const int64_t EF = __ldg(&p.inbF[as * kmax + kfj]);
     ++atf;
@@ -445,10 +466,10 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (;;) {
     ++itb;
     int js;
-    const int64_t dev = critical(p, p.devB, p.keyB, init_b ? s.cb : s.N, m, js);
+    const int64_t dev = !init_b ? crit_value(p, p.devB, s.N, kb0, js) : critical(p, p.devB, p.keyB, s.cb, m, js);
     Delta = max((int64_t)0, max(dev, dep_b));
     if (Delta == 0 || sumcb == 0) break;
-    const int as = js / rt, kfj = s.N[js] - s.c[js];
+    const int as = row_of(p, js), kfj = s.N[js] - s.c[js];
     const int kbj = init_b ? s.N[js] - s.cb[js] : 0;
     const int64_t rowoff = (int64_t)as * (kmax + 1) + kfj;
     if (kbj >= (int)__ldg(&p.lenB[rowoff])) break;
