@@ -60,7 +60,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_hw, o_partials, o_counter, o_stats, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_partials, o_counter, o_stats, total_bytes;
   int grid;
 };
 
@@ -262,12 +262,13 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_comp_hi = take((size_t)X.p * X.icapc * 8);
   X.o_comm_lo = take((size_t)X.p * X.icapm * 8);
   X.o_comm_hi = take((size_t)X.p * X.icapm * 8);
+  X.o_bmax = take((size_t)X.p * 4 * ((std::max(X.icapc, X.icapm) + 31) / 32) * 8);
   X.o_sim = take((size_t)X.p * 4);
   X.o_k0res = take((size_t)(1 + X.k0_trials) * 8);
   X.o_tables = take((size_t)X.n_tables * 8);
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
-  X.o_snap_hw = take((size_t)X.n_slots * 2 * 4);
+  X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
@@ -324,13 +325,15 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.comp_hi = (int64_t*)(ws + X.o_comp_hi);
   c.comm_lo = (int64_t*)(ws + X.o_comm_lo);
   c.comm_hi = (int64_t*)(ws + X.o_comm_hi);
+  c.bmax = (int64_t*)(ws + X.o_bmax);
+  c.ci_n = (std::max(X.icapc, X.icapm) + 31) / 32;
   c.bestw = (int32_t*)(ws + X.o_sim);
   c.k0res = (int64_t*)(ws + X.o_k0res);
   c.k0_trials = X.k0_trials;
   c.tables = (int64_t*)(ws + X.o_tables);
   c.snap = (int64_t*)(ws + X.o_snap);
   c.bfill = (int64_t*)(ws + X.o_bfill);
-  c.snap_hw = (int32_t*)(ws + X.o_snap_hw);
+  c.snap_own = (int8_t*)(ws + X.o_snap_own);
   return c;
 }
 

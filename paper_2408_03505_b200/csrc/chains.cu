@@ -29,6 +29,13 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifdef K1_STATS  // development instrumentation (OPTIMUS_NVCC_EXTRA=-DK1_STATS): per-warp event counts
+__shared__ unsigned long long k1st[32][8];  // placements, fast hits, ballots, window advances, place cyc, wait cyc
+#define K1ST(i, v) do { if ((threadIdx.x & 31) == 0) k1st[threadIdx.x >> 5][i] += (v); } while (0)
+#else
+#define K1ST(i, v) do { } while (0)
+#endif
+
 // ------------------------------------------------------------ plan tables
 __global__ void k_plan_tables(Cfg c) {
   const int e = blockIdx.x;
@@ -97,27 +104,43 @@ __global__ void k_plan_tables(Cfg c) {
   }
 }
 
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, (int64_t)__shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
 // ------------------------------------------------------ first-fit machinery
 // Register view of one (LLM stage, resource) interval list of one unit.
 // Forward (M = false): intervals as in the template; fill = this unit's fill
-// pointers, valid below hw.  Mirrored (M = true, R15): interval i' is real
-// interval count-1-i' in time t -> T_end - t; its end is T_end minus the
-// forward fill pointer of forward snapshot kf (valid below hwf).
+// pointers, valid in the 32-blocks marked in wm; blocks written back during the
+// current chain are marked in dmask.  Mirrored (M = true, R15): interval i'
+// is real interval count-1-i' in time t -> T_end - t; its end is T_end minus
+// the forward fill pointer of forward snapshot kf.  Snapshots are
+// copy-on-write per 32-block: own[b] = the forward version (chain count)
+// whose buffer holds block b of snapshot kf, -1 = untouched (fill = start).
 template <bool M>
 struct VR {
-  int count, hw, hwf;
+  int count;
+  uint32_t* wm;          // 32-blocks of fill written so far by this unit (smem); others: fill = start
   const int64_t* S;
   const int64_t* H;
   int64_t* fill;
-  const int64_t* snapf;
+  uint32_t* dmask;       // forward: dirty 32-blocks of the running chain (smem)
+  int64_t* bm;           // largest capacity hi - lo of each 32-block (smem; lowered as blocks fill)
+  const int8_t* own;     // mirror: owner version of each 32-block of snapshot kf (smem)
+  const int64_t* snap0;  // mirror: this list in snapshot version 0; version o at + o * vstride
+  int64_t vstride;
   int64_t T_end;
   __device__ __forceinline__ int64_t hi_at(int i) const {
     if (!M) return H[i];
     const int r = count - 1 - i;
-    return T_end - (r < hwf ? snapf[r] : S[r]);
+    const int o = own[r >> 5];
+    return T_end - (o < 0 ? S[r] : snap0[o * vstride + r]);
   }
   __device__ __forceinline__ int64_t start_at(int i) const { return M ? T_end - H[count - 1 - i] : S[i]; }
-  __device__ __forceinline__ int64_t lo_at(int i) const { return i < hw ? fill[i] : start_at(i); }
+  __device__ __forceinline__ int64_t lo_at(int i) const {
+    return ((wm[i >> 10] >> ((i >> 5) & 31)) & 1u) ? fill[i] : start_at(i);
+  }
 };
 
 // A window of 32 consecutive intervals in registers (lane l = interval
@@ -129,7 +152,7 @@ struct Win {
   int base, cur;
   bool dirty;
   int64_t lo, hi, nlo, nhi;
-  int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative)
+  int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative); chi = -inf when cur < 0
 };
 
 template <bool M>
@@ -148,6 +171,7 @@ template <bool M>
 __device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
   w.base = b;
   w.cur = -1;
+  w.chi = kNegInf;
   w.dirty = false;
   win_fetch(V, b, w.lo, w.hi);
   win_fetch(V, b + 32, w.nlo, w.nhi);
@@ -156,6 +180,7 @@ __device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
 __device__ __forceinline__ void win_sync_cur(Win& w) {
   if (w.cur >= 0 && (threadIdx.x & 31) == w.cur - w.base) w.lo = w.clo;
   w.cur = -1;
+  w.chi = kNegInf;
 }
 
 template <bool M>
@@ -163,121 +188,156 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   win_sync_cur(w);
   if (!w.dirty) return;
   const int lane = threadIdx.x & 31;
-  for (int i = V.hw + lane; i < w.base; i += 32) V.fill[i] = V.start_at(i);  // gap fill
   const int i = w.base + lane;
   if (i < V.count) V.fill[i] = w.lo;
-  V.hw = max(V.hw, min(V.count, w.base + 32));
+  const int64_t cap = warp_max64(i < V.count ? w.hi - w.lo : kNegInf);
+  if (lane == 0) {
+    V.bm[w.base >> 5] = cap;
+    V.wm[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
+    if (!M) V.dmask[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
+  }
   w.dirty = false;
   __syncwarp();
 }
 
 // Place one kernel of duration d at or after `ready` (R12): the first
 // interval (time order) with end > ready and max(ready, lo) + d <= end.
-// Fast path: the current interval (uniform scalars); else a ballot over the
-// 32-interval window, then the following windows.
-template <bool M>
-__device__ __forceinline__ bool place(VR<M>& V, Win& w, int64_t d, int64_t& ready) {
-  if (w.cur >= 0) {
-    const int64_t x = max(ready, w.clo);
-    if (x + d <= w.chi) {
-      w.clo = x + d;
-      ready = x + d;
-      return true;
-    }
-    win_sync_cur(w);
+// Slow path, after the kernel did not fit the current interval (the fast
+// path in place_stage): a ballot over the 32-interval window, then the
+// following windows.
+// first 32-block >= b that ends after `ready` and whose largest capacity
+// can hold d (CI if none): ci = block ends, bm = block capacities
+__device__ __forceinline__ int next_block(const int64_t* ci, const int64_t* bm, int CI, int b, int64_t ready,
+                                          int64_t d) {
+  const int lane = threadIdx.x & 31;
+  for (; b < CI; b += 32) {
+    const int k = b + lane;
+    const unsigned m = __ballot_sync(FULL, k < CI && ci[k] > ready && bm[k] >= d);
+    if (m) return b + __ffs(m) - 1;
   }
+  return CI;
+}
+
+template <bool M>
+__device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t& ready, const int64_t* ci,
+                                           const int64_t* bm, int CI) {
+  win_sync_cur(w);
   for (;;) {
-    const int64_t x = max(ready, w.lo);
-    const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
-    if (b) {
-      const int f = __ffs(b) - 1;
-      const int64_t xf = __shfl_sync(FULL, x, f);
-      w.chi = __shfl_sync(FULL, w.hi, f);
-      w.cur = w.base + f;
-      w.clo = xf + d;
-      w.dirty = true;
-      ready = xf + d;
-      return true;
+    const int blk = w.base >> 5;
+    if (ci[blk] > ready && bm[blk] >= d) {  // else no interval of the window can take it
+      K1ST(0, 1);
+      const int64_t x = max(ready, w.lo);
+      const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
+      if (b) {
+        const int f = __ffs(b) - 1;
+        const int64_t xf = __shfl_sync(FULL, x, f);
+        w.chi = __shfl_sync(FULL, w.hi, f);
+        w.cur = w.base + f;
+        w.clo = xf + d;
+        w.dirty = true;
+        ready = xf + d;
+        return true;
+      }
     }
     win_flush(V, w);
-    if (w.base + 32 >= V.count) return false;
-    w.base += 32;
-    w.lo = w.nlo;
-    w.hi = w.nhi;
+    K1ST(3, 1);
+    const int nb = next_block(ci, bm, CI, blk + 1, ready, d);
+    if (32 * nb >= V.count) return false;
+    if (32 * nb == w.base + 32) {
+      w.lo = w.nlo;
+      w.hi = w.nhi;
+    } else {
+      win_fetch(V, 32 * nb, w.lo, w.hi);
+    }
+    w.base = 32 * nb;
     win_fetch(V, w.base + 32, w.nlo, w.nhi);
   }
 }
 
 // Per-warp shared memory of a K1 unit.
 struct UnitSm {
-  int64_t* seq_d;     // [NK] flattened kernel durations of the whole encoder, stage-major
-  uint8_t* seq_k;     // [NK] kinds
+  int64_t* seq;       // [NK] flattened kernels of the whole encoder, stage-major: duration | comm << 63
   int* soff;          // [P+1] stage offsets into seq
-  int* hw;            // [2P] valid fill prefix per (stage, resource)
+  uint32_t* wm;       // [P][2][MW] blocks of the fill arrays written so far
   int64_t* ci;        // [P][2][CI] coarse index: end of the last interval of each 32-block
-  int CI;
+  int64_t* bm;        // [P][2][CI] largest base capacity of each 32-block (this orientation)
+  int8_t* own;        // [P][2][CI] snapshot block owners (forward: current, mirror: snapshot kf)
+  uint32_t* dmask;    // [P][2][MW] forward: blocks written during the running chain
+  int CI, MW;
 };
 
 __host__ __device__ inline size_t unit_smem_bytes(int NK, int P, int CI) {
-  return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)NK + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
-         ((size_t)2 * P * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8;
+  const int MW = (CI + 31) / 32;
+  return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
+         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI + 15) / 16 * 16 +
+         (size_t)P * 2 * MW * 4;
 }
 
 __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
   UnitSm u;
-  u.seq_d = (int64_t*)p;
+  u.seq = (int64_t*)p;
   p += ((size_t)NK * 8 + 15) / 16 * 16;
-  u.seq_k = p;
-  p += ((size_t)NK + 15) / 16 * 16;
   u.soff = (int*)p;
   p += ((size_t)(P + 1) * 4 + 15) / 16 * 16;
-  u.hw = (int*)p;
-  p += ((size_t)2 * P * 4 + 15) / 16 * 16;
+  u.wm = (uint32_t*)p;
+  p += ((size_t)P * 2 * ((CI + 31) / 32) * 4 + 15) / 16 * 16;
   u.ci = (int64_t*)p;
+  u.bm = u.ci + (size_t)P * 2 * CI;
+  p += (size_t)P * 2 * CI * 8 * 2;
+  u.own = (int8_t*)p;
+  p += ((size_t)P * 2 * CI + 15) / 16 * 16;
+  u.dmask = (uint32_t*)p;
   u.CI = CI;
+  u.MW = (CI + 31) / 32;
   return u;
 }
 
-// Flatten the encoder's stage kernel lists (R8; §4.4 branches in order,
-// P:478) for plan pd: stage s = for each branch its layers
+// Flatten stage s of the encoder's kernel lists (R8; §4.4 branches in order,
+// P:478) for plan pd (one warp per stage): stage s = for each branch its layers
 // [floor(sL/P), floor((s+1)L/P)); mirrored time runs each layer's backward
 // list in reverse (R15).
-__device__ void build_seq(const Cfg& c, const PlanDesc& pd, bool mirror, UnitSm& U) {
+__device__ void build_seq(const Cfg& c, const PlanDesc& pd, bool mirror, UnitSm& U, int s) {
   const int lane = threadIdx.x & 31, P = pd.P;
-  int pos = 0;
-  for (int s = 0; s < P; ++s) {
-    if (lane == 0) U.soff[s] = pos;
+  int pos = 0;  // kernels of the stages before s
+  for (int t = 0; t < s; ++t)
     for (int b = 0; b < c.nb; ++b) {
-      const int L = c.blayers[b];
-      const int l0 = s * L / P, l1 = (s + 1) * L / P;
-      const int id = enc_list_id(b, pd.ti, c.ntp, mirror ? 1 : 0);
-      const int off = c.loff[id], len = c.loff[id + 1] - off;
-      const int cnt = (l1 - l0) * len;
-      for (int x = lane; x < cnt; x += 32) {
-        const int k = x % len;
-        const int kk = mirror ? off + len - 1 - k : off + k;
-        U.seq_d[pos + x] = c.lns[kk];
-        U.seq_k[pos + x] = (uint8_t)c.lkind[kk];
-      }
-      pos += cnt;
+      const int L = c.blayers[b], id = enc_list_id(b, pd.ti, c.ntp, mirror ? 1 : 0);
+      pos += ((t + 1) * L / P - t * L / P) * (c.loff[id + 1] - c.loff[id]);
     }
+  if (lane == 0) U.soff[s] = pos;
+  for (int b = 0; b < c.nb; ++b) {
+    const int L = c.blayers[b];
+    const int l0 = s * L / P, l1 = (s + 1) * L / P;
+    const int id = enc_list_id(b, pd.ti, c.ntp, mirror ? 1 : 0);
+    const int off = c.loff[id], len = c.loff[id + 1] - off;
+    const int cnt = (l1 - l0) * len;
+    for (int x = lane; x < cnt; x += 32) {
+      const int k = x % len;
+      const int kk = mirror ? off + len - 1 - k : off + k;
+      U.seq[pos + x] = c.lns[kk] | (c.lkind[kk] != 0 ? INT64_MIN : 0);
+    }
+    pos += cnt;
   }
-  if (lane == 0) U.soff[P] = pos;
-  __syncwarp();
+  if (lane == 0 && s == P - 1) U.soff[P] = pos;
 }
 
+// view of list r of stage s of row a; fill = this unit's fill array of the
+// stage, snap0 = the stage's snapshot version-0 array (both [icapc + icapm])
 template <bool M>
-__device__ VR<M> make_view(const Cfg& c, const PlanDesc& pd, int a, int s, int r, int64_t* fill,
-                           const int64_t* snapf, int hwf, int hw) {
+__device__ VR<M> make_view(const Cfg& c, const PlanDesc& pd, int a, int s, int r, int64_t* fill, const UnitSm& U,
+                           const int64_t* snap0) {
   const int q = a * pd.P + s;
   VR<M> V;
   V.count = r == 0 ? c.ncomp[q] : c.ncomm[q];
   V.S = r == 0 ? c.comp_lo + (int64_t)q * c.icapc : c.comm_lo + (int64_t)q * c.icapm;
   V.H = r == 0 ? c.comp_hi + (int64_t)q * c.icapc : c.comm_hi + (int64_t)q * c.icapm;
-  V.fill = fill;
-  V.snapf = snapf;
-  V.hwf = hwf;
-  V.hw = hw;
+  V.fill = fill ? fill + (r ? c.icapc : 0) : nullptr;
+  V.dmask = U.dmask + (2 * s + r) * U.MW;
+  V.bm = U.bm + (2 * s + r) * U.CI;
+  V.own = U.own + (2 * s + r) * U.CI;
+  V.snap0 = snap0 + (r ? c.icapc : 0);
+  V.vstride = (int64_t)pd.rp * pd.P * (c.icapc + c.icapm);
+  V.wm = U.wm + (2 * s + r) * U.MW;
   V.T_end = c.scal[1];
   return V;
 }
@@ -304,9 +364,8 @@ __device__ __forceinline__ int ci_search(const int64_t* ci, int CI, int64_t read
 
 struct UnitCtx {
   int P, a;
-  int64_t* fill;        // this unit's fill state, slot-major: [P][icapc + icapm]
-  const int64_t* snap;  // mirror: forward snapshot kf, same layout
-  const int* snap_hw;   // mirror: [P][2] (nullptr -> all 0)
+  int64_t* fill;         // this unit's fill state, slot-major: [P][icapc + icapm]
+  const int64_t* snap0;  // snapshot version 0 of this row, same layout (version o at + o * rp * P * icap)
 };
 
 // Place stage s of one chain starting at `ready` (R12; mirrored lists and
@@ -318,28 +377,84 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
                             int64_t* end) {
   const int icap = c.icapc + c.icapm;
   int64_t* f0 = X.fill + (int64_t)s * icap;
-  const int64_t* s0 = M ? X.snap + (int64_t)s * icap : nullptr;
-  VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, s0, X.snap_hw ? X.snap_hw[2 * s] : 0, U.hw[2 * s]);
-  VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0 + c.icapc, M ? s0 + c.icapc : nullptr,
-                          X.snap_hw ? X.snap_hw[2 * s + 1] : 0, U.hw[2 * s + 1]);
+  const int64_t* s0 = X.snap0 + (int64_t)s * icap;
+  VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, U, s0);
+  VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0, U, s0);
   Win w0, w1;  // compute-free / comm-free windows of this stage
   win_open(V0, w0, ci_search(U.ci + (2 * s) * U.CI, U.CI, ready));
   win_open(V1, w1, ci_search(U.ci + (2 * s + 1) * U.CI, U.CI, ready));
-  const int i0 = U.soff[s], i1 = U.soff[s + 1];
-  bool ok = true;
-  int64_t d = i0 < i1 ? U.seq_d[i0] : 0;
-  int kind = i0 < i1 ? U.seq_k[i0] : 0;
-  for (int i = i0; i < i1 && ok; ++i) {
-    const int64_t dn = U.seq_d[min(i + 1, i1 - 1)];  // prefetch the next kernel
-    const int kn = U.seq_k[min(i + 1, i1 - 1)];
-    ok = kind == 0 ? place(V0, w0, d, ready) : place(V1, w1, d, ready);
-    d = dn;
-    kind = kn;
+  const int i1 = U.soff[s + 1];
+  const int64_t* seq = U.seq;
+  const int i0 = U.soff[s];
+  int i = i0;
+#ifdef K1_STATS
+  const long long t0 = clock64();
+#endif
+  for (;;) {
+    // fast path, 32 kernels at a time (lane l = kernel i+l): while every
+    // kernel fits the current interval of its resource (chi = -inf when
+    // there is none), a kernel starts at the previous end unless it is the
+    // first of its resource in the batch (then at max(prev end, clo)), so
+    // e_l = D_l + max(ready, clo_r - Dex_{f_r} for each resource r whose
+    // first lane f_r <= l), D = inclusive prefix sum of the durations.
+    // The first kernel that does not fit goes to the slow path.
+    while (i < i1) {
+      const int lane = threadIdx.x & 31;
+      const bool valid = i + lane < i1;
+      const int64_t v = valid ? seq[i + lane] : 0;
+      const bool comm = v < 0;
+      const int64_t d = v & INT64_MAX;
+      int64_t D = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(FULL, D, o);
+        if (lane >= o) D += t;
+      }
+      const unsigned mc = __ballot_sync(FULL, valid && comm), mp = __ballot_sync(FULL, valid && !comm);
+      const int fc = mc ? __ffs(mc) - 1 : 32, fp = mp ? __ffs(mp) - 1 : 32;
+      const int64_t Dex = D - d;
+      const int64_t Ac = w1.clo - __shfl_sync(FULL, Dex, fc & 31);
+      const int64_t Ap = w0.clo - __shfl_sync(FULL, Dex, fp & 31);
+      int64_t st = ready;
+      if (lane >= fc) st = max(st, Ac);
+      if (lane >= fp) st = max(st, Ap);
+      const int64_t e = D + st;
+      const unsigned bad = __ballot_sync(FULL, valid && e > (comm ? w1.chi : w0.chi));
+      const int nv = min(32, i1 - i);
+      const int f = bad ? __ffs(bad) - 1 : nv;  // kernels placed by this batch
+      if (f > 0) {
+        ready = __shfl_sync(FULL, e, f - 1);
+        const unsigned below = f == 32 ? FULL : ((1u << f) - 1u);
+        const unsigned lc = mc & below, lp = mp & below;
+        const int64_t ec = __shfl_sync(FULL, e, lc ? 31 - __clz(lc) : 0);
+        const int64_t ep = __shfl_sync(FULL, e, lp ? 31 - __clz(lp) : 0);
+        if (lc) w1.clo = ec;
+        if (lp) w0.clo = ep;
+        i += f;
+      }
+      if (f < nv) break;
+    }
+    if (i >= i1) break;
+    const int64_t v = seq[i];
+    K1ST(2, 1);
+#ifdef K1_STATS
+    const long long ts0 = clock64();
+#endif
+    const bool ok = v < 0 ? place_slow(V1, w1, v & INT64_MAX, ready, U.ci + (2 * s + 1) * U.CI,
+                                       U.bm + (2 * s + 1) * U.CI, U.CI)
+                          : place_slow(V0, w0, v & INT64_MAX, ready, U.ci + (2 * s) * U.CI, U.bm + (2 * s) * U.CI,
+                                       U.CI);
+#ifdef K1_STATS
+    K1ST(7, clock64() - ts0);
+#endif
+    if (!ok) return false;
+    ++i;
   }
-  if (!ok) return false;
+#ifdef K1_STATS
+  K1ST(4, clock64() - t0);
+#endif
   win_flush(V0, w0);
   win_flush(V1, w1);
-  if ((threadIdx.x & 31) == 0) { U.hw[2 * s] = V0.hw; U.hw[2 * s + 1] = V1.hw; }
   __syncwarp();
   *end = ready;
   return true;
@@ -391,22 +506,35 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
   volatile int64_t* endv = (volatile int64_t*)(dsm + ub + (((size_t)L.Pmax * L.KM * 4 + 15) & ~size_t(15)));
   volatile int* stop = &stop_at;
   auto slot = [&](int k, int st) { return pd.slot_base + ((int64_t)k * pd.rp + a) * P + st; };
-  if (s == 0) build_seq(c, pd, M, U);
+#ifdef K1_STATS
+  const long long tk0 = clock64();
+  if (threadIdx.x < 32 * 8) k1st[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+  __syncthreads();
+#endif
+  if (active) build_seq(c, pd, M, U, s);
   for (int i = threadIdx.x; i < P * L.KM; i += blockDim.x) status[i] = 0;
   if (threadIdx.x == 0) stop_at = pd.kmax;
-  const int64_t* snap = M ? c.snap + slot(kf, 0) * icap : nullptr;
-  const int* snap_hw = (M && kf > 0) ? c.snap_hw + slot(kf, 0) * 2 : nullptr;
+  const int64_t* snap0 = c.snap + slot(0, 0) * icap;
   if (active) {
-    if (lane < 2) U.hw[2 * s + lane] = 0;
     for (int r = 0; r < 2; ++r) {
-      VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, M ? snap + (int64_t)s * icap + (r ? c.icapc : 0) : nullptr,
-                             snap_hw ? snap_hw[2 * s + r] : 0, 0);
+      // block owners: forward starts untouched; mirror loads snapshot kf's map
+      int8_t* own = U.own + (2 * s + r) * U.CI;
+      const int8_t* gown = c.snap_own + (slot(kf, s) * 2 + r) * c.ci_n;
+      for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? gown[b] : (int8_t)-1;
+      for (int b = lane; b < U.MW; b += 32) U.dmask[(2 * s + r) * U.MW + b] = U.wm[(2 * s + r) * U.MW + b] = 0u;
+      __syncwarp();
+      VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, U, snap0 + (int64_t)s * icap);
       build_ci(V, U.ci + (2 * s + r) * U.CI, U.CI);
+      const int64_t* bsrc = c.bmax + (((int64_t)(a * P + s) * 2 + r) * 2 + (M ? 1 : 0)) * c.ci_n;
+      for (int k = lane; k < U.CI; k += 32) U.bm[(2 * s + r) * U.CI + k] = bsrc[k];
     }
   }
   __syncthreads();
   if (active) {
-    const UnitCtx X{P, a, (M ? c.bfill : c.snap) + slot(M ? kf : 0, 0) * icap, snap, snap_hw};
+    const UnitCtx X{P, a, (M ? c.bfill : c.snap) + slot(M ? kf : 0, 0) * icap, snap0};
+#ifdef K1_STATS
+    K1ST(1, clock64() - tk0);
+#endif
     const int64_t T_end = c.scal[1];
     const int q = a * P + s;
     const int64_t ws = M ? T_end - c.z[q] : c.w[q];
@@ -416,10 +544,16 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
       if (s > 0) {  // wait for chain k of the upstream stage
         int st;
         bool quit = false;
+#ifdef K1_STATS
+        const long long tw0 = clock64();
+#endif
         while ((st = status[(s - 1) * L.KM + k]) == 0) {
           if (k >= *stop) { quit = true; break; }
           __nanosleep(20);
         }
+#ifdef K1_STATS
+        K1ST(5, clock64() - tw0);
+#endif
         if (quit || st == 2) break;
         ready = max(endv[(s - 1) * L.KM + k] + c.enc_p2p, ws);
       }
@@ -431,13 +565,42 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
         }
         break;
       }
-      if (!M) {  // snapshot this stage after k+1 chains
+      if (!M) {  // snapshot version k+1 of this stage: copy the blocks written by chain k
         for (int r = 0; r < 2; ++r) {
-          const int h = U.hw[2 * s + r];
           const int64_t* src = X.fill + (int64_t)s * icap + (r ? c.icapc : 0);
           int64_t* dst = c.snap + slot(k + 1, s) * icap + (r ? c.icapc : 0);
-          for (int i = lane; i < h; i += 32) dst[i] = src[i];
-          if (lane == 0) c.snap_hw[slot(k + 1, s) * 2 + r] = h;
+          const int cap = r ? c.icapm : c.icapc;
+          uint32_t* dm = U.dmask + (2 * s + r) * U.MW;
+          int8_t* own = U.own + (2 * s + r) * U.CI;
+          for (int wi = 0; wi < U.MW; ++wi) {
+            unsigned m = dm[wi];
+            while (m) {  // up to 8 blocks per round, loads in flight together
+              int bl[8];
+              int64_t val[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                bl[j] = m ? wi * 32 + __ffs(m) - 1 : -1;
+                m &= m - 1;
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int idx = bl[j] * 32 + lane;
+                if (bl[j] >= 0 && idx < cap) val[j] = src[idx];
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int idx = bl[j] * 32 + lane;
+                if (bl[j] >= 0 && idx < cap) dst[idx] = val[j];
+                if (bl[j] >= 0 && lane == 0) own[bl[j]] = (int8_t)(k + 1);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) dm[wi] = 0u;
+          }
+          __syncwarp();
+          int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
+          for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
+          __syncwarp();
         }
       }
       if (lane == 0) {
@@ -452,6 +615,12 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
       __syncwarp();
     }
   }
+#ifdef K1_STATS
+  K1ST(6, clock64() - tk0);
+  if (active && lane == 0 && k1st[s][6] > 300000)
+    printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d ballot=%llu setup=%llu slow=%llu adv=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
+           (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
+#endif
   __syncthreads();
   if (threadIdx.x == 0) {  // chains completed by every stage
     int k = 0;

@@ -34,6 +34,7 @@ struct Cfg {
   int32_t kmax_all;      // max kmax over plans
   int32_t k0_trials;     // sum over stages of (Wdef_s + 1): K0 warm-up trials
   int32_t nk_max;        // max over TP options of the encoder's total kernel count (all layers, all branches)
+  int32_t ci_n;          // 32-interval blocks per interval list: ceil(max(icapc, icapm) / 32)
   int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
   // packed inputs
   const int32_t* lkind;   // kernel kinds, all lists concatenated
@@ -55,6 +56,7 @@ struct Cfg {
   int64_t* comp_hi;       // [p][icapc] compute-free interval ends
   int64_t* comm_lo;       // [p][icapm]
   int64_t* comm_hi;       // [p][icapm]
+  int64_t* bmax;          // [p][2 resources][2 orientations][ci_n]: max base capacity (hi - lo) per 32-interval block
   int32_t* bestw;         // [p] K0 warm-up search: smallest successful w per stage
   int64_t* k0res;         // [1 + k0_trials] K0 wave: span of each simulation, -1 if it deadlocks
   // plans + tables (K1)
@@ -62,7 +64,7 @@ struct Cfg {
   int64_t* tables;
   int64_t* snap;          // [slots][icapc+icapm] forward fill snapshots (slot k=0 is the working copy)
   int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
-  int32_t* snap_hw;       // [slots][2] valid prefix of each snapshot slot
+  int8_t* snap_own;       // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
   const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
 };
 

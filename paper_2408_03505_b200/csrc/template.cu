@@ -435,6 +435,25 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
     __syncthreads();
   }
   if (threadIdx.x == 0) { c.ncomp[s] = run_c; c.ncomm[s] = run_m; }
+  __syncthreads();
+  // per 32-interval block, the largest base capacity hi - lo, in time order
+  // (orientation 0) and in mirrored order (1, interval i' = count-1-i): no
+  // kernel longer than it fits anywhere in the block (K1 skips such blocks)
+  const int CI = c.ci_n, lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < 4 * CI; t += kIvThreads / 32) {
+    const int r = t / (2 * CI), o = (t / CI) & 1, b = t % CI;
+    const int cnt = r == 0 ? run_c : run_m;
+    const int64_t* L = r == 0 ? clo : mlo;
+    const int64_t* H = r == 0 ? chi : mhi;
+    const int i = 32 * b + lane;
+    int64_t cap = kNegInf;
+    if (i < cnt) {
+      const int ri = o == 0 ? i : cnt - 1 - i;
+      cap = H[ri] - L[ri];
+    }
+    cap = warp_max64(cap);
+    if (lane == 0) c.bmax[(((int64_t)s * 2 + r) * 2 + o) * CI + b] = cap;
+  }
 }
 
 }  // namespace
