@@ -111,24 +111,25 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
 
 // ------------------------------------------------------ first-fit machinery
 // Register view of one (LLM stage, resource) interval list of one unit.
-// Forward (M = false): intervals as in the template; fill = this unit's fill
-// pointers, valid in the 32-blocks marked in wm; blocks written back during the
-// current chain are marked in dmask.  Mirrored (M = true, R15): interval i'
-// is real interval count-1-i' in time t -> T_end - t; its end is T_end minus
-// the forward fill pointer of forward snapshot kf.  Snapshots are
-// copy-on-write per 32-block: own[b] = the forward version (chain count)
-// whose buffer holds block b of snapshot kf, -1 = untouched (fill = start).
+// Snapshots of the forward fill state are versioned per 32-interval block:
+// version v = the state after v forward chains, own[b] = the version whose
+// buffer holds block b (-1: never written, fill = start).
+// Forward (M = false): intervals as in the template; chain k writes every
+// block it touches into version k+1's buffer and points own[b] there, so
+// version k+1 = own map after chain k, no copies.  Mirrored (M = true,
+// R15): interval i' is real interval count-1-i' in time t -> T_end - t; its
+// end is T_end minus the fill pointer of forward version kf (own = kf's map);
+// the unit's own fill state lives in `fill`, valid in the blocks marked in wm.
 template <bool M>
 struct VR {
-  int count;
-  uint32_t* wm;          // 32-blocks of fill written so far by this unit (smem); others: fill = start
+  int count, ver;        // forward: version this chain writes
+  uint32_t* wm;          // mirror: 32-blocks of fill written so far (smem)
   const int64_t* S;
   const int64_t* H;
-  int64_t* fill;
-  uint32_t* dmask;       // forward: dirty 32-blocks of the running chain (smem)
+  int64_t* fill;         // mirror: this unit's fill array
   int64_t* bm;           // largest capacity hi - lo of each 32-block (smem; lowered as blocks fill)
-  const int8_t* own;     // mirror: owner version of each 32-block of snapshot kf (smem)
-  const int64_t* snap0;  // mirror: this list in snapshot version 0; version o at + o * vstride
+  int8_t* own;           // owner version per 32-block (smem): forward current, mirror kf's
+  int64_t* snap0;        // this list in version 0's buffer; version o at + o * vstride
   int64_t vstride;
   int64_t T_end;
   __device__ __forceinline__ int64_t hi_at(int i) const {
@@ -139,7 +140,9 @@ struct VR {
   }
   __device__ __forceinline__ int64_t start_at(int i) const { return M ? T_end - H[count - 1 - i] : S[i]; }
   __device__ __forceinline__ int64_t lo_at(int i) const {
-    return ((wm[i >> 10] >> ((i >> 5) & 31)) & 1u) ? fill[i] : start_at(i);
+    if (M) return ((wm[i >> 10] >> ((i >> 5) & 31)) & 1u) ? fill[i] : start_at(i);
+    const int o = own[i >> 5];
+    return o < 0 ? S[i] : snap0[o * vstride + i];
   }
 };
 
@@ -189,12 +192,12 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   if (!w.dirty) return;
   const int lane = threadIdx.x & 31;
   const int i = w.base + lane;
-  if (i < V.count) V.fill[i] = w.lo;
+  if (i < V.count) (M ? V.fill : V.snap0 + V.ver * V.vstride)[i] = w.lo;  // forward: the whole block
   const int64_t cap = warp_max64(i < V.count ? w.hi - w.lo : kNegInf);
   if (lane == 0) {
     V.bm[w.base >> 5] = cap;
-    V.wm[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
-    if (!M) V.dmask[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
+    if (M) V.wm[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
+    else V.own[w.base >> 5] = (int8_t)V.ver;
   }
   w.dirty = false;
   __syncwarp();
@@ -225,7 +228,6 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
   for (;;) {
     const int blk = w.base >> 5;
     if (ci[blk] > ready && bm[blk] >= d) {  // else no interval of the window can take it
-      K1ST(0, 1);
       const int64_t x = max(ready, w.lo);
       const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
       if (b) {
@@ -240,7 +242,6 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
       }
     }
     win_flush(V, w);
-    K1ST(3, 1);
     const int nb = next_block(ci, bm, CI, blk + 1, ready, d);
     if (32 * nb >= V.count) return false;
     if (32 * nb == w.base + 32) {
@@ -262,15 +263,13 @@ struct UnitSm {
   int64_t* ci;        // [P][2][CI] coarse index: end of the last interval of each 32-block
   int64_t* bm;        // [P][2][CI] largest base capacity of each 32-block (this orientation)
   int8_t* own;        // [P][2][CI] snapshot block owners (forward: current, mirror: snapshot kf)
-  uint32_t* dmask;    // [P][2][MW] forward: blocks written during the running chain
   int CI, MW;
 };
 
 __host__ __device__ inline size_t unit_smem_bytes(int NK, int P, int CI) {
   const int MW = (CI + 31) / 32;
   return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
-         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI + 15) / 16 * 16 +
-         (size_t)P * 2 * MW * 4;
+         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI + 15) / 16 * 16;
 }
 
 __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
@@ -285,8 +284,6 @@ __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
   u.bm = u.ci + (size_t)P * 2 * CI;
   p += (size_t)P * 2 * CI * 8 * 2;
   u.own = (int8_t*)p;
-  p += ((size_t)P * 2 * CI + 15) / 16 * 16;
-  u.dmask = (uint32_t*)p;
   u.CI = CI;
   u.MW = (CI + 31) / 32;
   return u;
@@ -325,14 +322,14 @@ __device__ void build_seq(const Cfg& c, const PlanDesc& pd, bool mirror, UnitSm&
 // stage, snap0 = the stage's snapshot version-0 array (both [icapc + icapm])
 template <bool M>
 __device__ VR<M> make_view(const Cfg& c, const PlanDesc& pd, int a, int s, int r, int64_t* fill, const UnitSm& U,
-                           const int64_t* snap0) {
+                           int64_t* snap0, int ver) {
   const int q = a * pd.P + s;
   VR<M> V;
   V.count = r == 0 ? c.ncomp[q] : c.ncomm[q];
   V.S = r == 0 ? c.comp_lo + (int64_t)q * c.icapc : c.comm_lo + (int64_t)q * c.icapm;
   V.H = r == 0 ? c.comp_hi + (int64_t)q * c.icapc : c.comm_hi + (int64_t)q * c.icapm;
   V.fill = fill ? fill + (r ? c.icapc : 0) : nullptr;
-  V.dmask = U.dmask + (2 * s + r) * U.MW;
+  V.ver = ver;
   V.bm = U.bm + (2 * s + r) * U.CI;
   V.own = U.own + (2 * s + r) * U.CI;
   V.snap0 = snap0 + (r ? c.icapc : 0);
@@ -364,8 +361,8 @@ __device__ __forceinline__ int ci_search(const int64_t* ci, int CI, int64_t read
 
 struct UnitCtx {
   int P, a;
-  int64_t* fill;         // this unit's fill state, slot-major: [P][icapc + icapm]
-  const int64_t* snap0;  // snapshot version 0 of this row, same layout (version o at + o * rp * P * icap)
+  int64_t* fill;   // mirror: this unit's fill state, slot-major: [P][icapc + icapm]
+  int64_t* snap0;  // version 0 of this row's forward snapshots, same layout (version o at + o * rp * P * icap)
 };
 
 // Place stage s of one chain starting at `ready` (R12; mirrored lists and
@@ -373,13 +370,16 @@ struct UnitCtx {
 // kernel end.  On failure the stage's fill state may be partly modified
 // (the unit stops).
 template <bool M>
-__device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, UnitSm& U, int s, int64_t ready,
-                            int64_t* end) {
+__device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, UnitSm& U, int s, int k,
+                            int64_t ready, int64_t* end) {
+#ifdef K1_STATS
+  const long long tp0 = clock64();
+#endif
   const int icap = c.icapc + c.icapm;
-  int64_t* f0 = X.fill + (int64_t)s * icap;
-  const int64_t* s0 = X.snap0 + (int64_t)s * icap;
-  VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, U, s0);
-  VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0, U, s0);
+  int64_t* f0 = M ? X.fill + (int64_t)s * icap : nullptr;
+  int64_t* s0 = X.snap0 + (int64_t)s * icap;
+  VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, U, s0, k + 1);
+  VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0, U, s0, k + 1);
   Win w0, w1;  // compute-free / comm-free windows of this stage
   win_open(V0, w0, ci_search(U.ci + (2 * s) * U.CI, U.CI, ready));
   win_open(V1, w1, ci_search(U.ci + (2 * s + 1) * U.CI, U.CI, ready));
@@ -389,6 +389,7 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
   int i = i0;
 #ifdef K1_STATS
   const long long t0 = clock64();
+  K1ST(0, t0 - tp0);
 #endif
   for (;;) {
     // fast path, 32 kernels at a time (lane l = kernel i+l): while every
@@ -514,16 +515,16 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
   if (active) build_seq(c, pd, M, U, s);
   for (int i = threadIdx.x; i < P * L.KM; i += blockDim.x) status[i] = 0;
   if (threadIdx.x == 0) stop_at = pd.kmax;
-  const int64_t* snap0 = c.snap + slot(0, 0) * icap;
+  int64_t* snap0 = c.snap + slot(0, 0) * icap;
   if (active) {
     for (int r = 0; r < 2; ++r) {
       // block owners: forward starts untouched; mirror loads snapshot kf's map
       int8_t* own = U.own + (2 * s + r) * U.CI;
       const int8_t* gown = c.snap_own + (slot(kf, s) * 2 + r) * c.ci_n;
       for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? gown[b] : (int8_t)-1;
-      for (int b = lane; b < U.MW; b += 32) U.dmask[(2 * s + r) * U.MW + b] = U.wm[(2 * s + r) * U.MW + b] = 0u;
+      for (int b = lane; b < U.MW; b += 32) U.wm[(2 * s + r) * U.MW + b] = 0u;
       __syncwarp();
-      VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, U, snap0 + (int64_t)s * icap);
+      VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, U, snap0 + (int64_t)s * icap, 0);
       build_ci(V, U.ci + (2 * s + r) * U.CI, U.CI);
       const int64_t* bsrc = c.bmax + (((int64_t)(a * P + s) * 2 + r) * 2 + (M ? 1 : 0)) * c.ci_n;
       for (int k = lane; k < U.CI; k += 32) U.bm[(2 * s + r) * U.CI + k] = bsrc[k];
@@ -531,7 +532,7 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
   }
   __syncthreads();
   if (active) {
-    const UnitCtx X{P, a, (M ? c.bfill : c.snap) + slot(M ? kf : 0, 0) * icap, snap0};
+    const UnitCtx X{P, a, M ? c.bfill + slot(kf, 0) * icap : nullptr, snap0};
 #ifdef K1_STATS
     K1ST(1, clock64() - tk0);
 #endif
@@ -558,50 +559,12 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
         ready = max(endv[(s - 1) * L.KM + k] + c.enc_p2p, ws);
       }
       int64_t end;
-      if (!place_stage<M>(c, pd, X, U, s, ready, &end)) {
+      if (!place_stage<M>(c, pd, X, U, s, k, ready, &end)) {
         if (lane == 0) {
           atomicMin(&stop_at, k);
           status[s * L.KM + k] = 2;
         }
         break;
-      }
-      if (!M) {  // snapshot version k+1 of this stage: copy the blocks written by chain k
-        for (int r = 0; r < 2; ++r) {
-          const int64_t* src = X.fill + (int64_t)s * icap + (r ? c.icapc : 0);
-          int64_t* dst = c.snap + slot(k + 1, s) * icap + (r ? c.icapc : 0);
-          const int cap = r ? c.icapm : c.icapc;
-          uint32_t* dm = U.dmask + (2 * s + r) * U.MW;
-          int8_t* own = U.own + (2 * s + r) * U.CI;
-          for (int wi = 0; wi < U.MW; ++wi) {
-            unsigned m = dm[wi];
-            while (m) {  // up to 8 blocks per round, loads in flight together
-              int bl[8];
-              int64_t val[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                bl[j] = m ? wi * 32 + __ffs(m) - 1 : -1;
-                m &= m - 1;
-              }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int idx = bl[j] * 32 + lane;
-                if (bl[j] >= 0 && idx < cap) val[j] = src[idx];
-              }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int idx = bl[j] * 32 + lane;
-                if (bl[j] >= 0 && idx < cap) dst[idx] = val[j];
-                if (bl[j] >= 0 && lane == 0) own[bl[j]] = (int8_t)(k + 1);
-              }
-            }
-            __syncwarp();
-            if (lane == 0) dm[wi] = 0u;
-          }
-          __syncwarp();
-          int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
-          for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
-          __syncwarp();
-        }
       }
       if (lane == 0) {
         endv[s * L.KM + k] = end;
@@ -613,12 +576,18 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
         }
       }
       __syncwarp();
+      if (!M)  // publish version k+1 of this stage: the block owner maps after chain k
+        for (int r = 0; r < 2; ++r) {
+          const int8_t* own = U.own + (2 * s + r) * U.CI;
+          int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
+          for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
+        }
     }
   }
 #ifdef K1_STATS
   K1ST(6, clock64() - tk0);
   if (active && lane == 0 && k1st[s][6] > 300000)
-    printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d ballot=%llu setup=%llu slow=%llu adv=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
+    printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d prolog=%llu setup=%llu slow=%llu x=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
            (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
 #endif
   __syncthreads();
