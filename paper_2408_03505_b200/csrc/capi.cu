@@ -53,14 +53,15 @@ struct Prep {
   std::vector<uint64_t> binom;
   std::vector<HostPlan> plans;
   uint64_t total = 0;
-  int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0;
+  int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0, n_flags = 0;
+  std::vector<int32_t> units;
   int kmax_all = 0;
   int nk_max = 0;
   int k0_trials = 0;
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_partials, o_counter, o_stats, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_partials, o_counter, o_stats, total_bytes;
   int grid;
 };
 
@@ -227,6 +228,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
         d.lenB = toff; toff += (int64_t)d.rp * (d.kmax + 1);
         d.slot_base = slot;
         slot += (int64_t)X.p * (d.kmax + 1);
+        d.flag_base = X.n_flags;
+        X.n_flags += (int64_t)d.rp * (d.kmax + 1);
         X.fwd_units += d.rp;
         X.bwd_units += (int64_t)d.rp * (d.kmax + 1);
         X.kmax_all = std::max(X.kmax_all, d.kmax);
@@ -235,6 +238,18 @@ int prepare(const optimus_problem* pb, Prep& X) {
     }
   }
   X.total = first;
+  // K1 unit list: forward units, then backward units ordered by kf (the
+  // ones that can start at once first)
+  for (size_t e = 0; e < X.plans.size(); ++e)
+    if (X.plans[e].d.count)
+      for (int a = 0; a < X.plans[e].d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8));
+  for (int kf = 0; kf <= X.kmax_all; ++kf)
+    for (size_t e = 0; e < X.plans.size(); ++e) {
+      const PlanDesc& d = X.plans[e].d;
+      if (d.count && kf <= d.kmax)
+        for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8 | kf));
+    }
+  X.n_flags = std::max<int64_t>(X.n_flags, 1);
   X.n_tables = std::max<int64_t>(toff, 1);
   X.n_slots = std::max<int64_t>(slot, 1);
 
@@ -247,6 +262,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_blayers = take(X.blayers.size() * 4);
   X.o_binom = take(X.binom.size() * 8);
   X.o_plans = take(X.plans.size() * sizeof(PlanDesc));
+  X.o_units = take(std::max<size_t>(X.units.size(), 1) * 4);
   X.inputs_bytes = o;
   X.o_W = take(X.p * 4);
   X.o_Wdef = take(X.p * 4);
@@ -268,6 +284,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_tables = take((size_t)X.n_tables * 8);
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
+  X.o_k1flags = take((size_t)X.n_flags * 4);
   X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
@@ -334,6 +351,8 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.snap = (int64_t*)(ws + X.o_snap);
   c.bfill = (int64_t*)(ws + X.o_bfill);
   c.snap_own = (int8_t*)(ws + X.o_snap_own);
+  c.k1flags = (int32_t*)(ws + X.o_k1flags);
+  c.k1units = (const int32_t*)(ws + X.o_units);
   return c;
 }
 
@@ -403,6 +422,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   memcpy(h.data() + X.o_blayers, X.blayers.data(), X.blayers.size() * 4);
   memcpy(h.data() + X.o_binom, X.binom.data(), X.binom.size() * 8);
   for (size_t i = 0; i < X.plans.size(); ++i) memcpy(h.data() + X.o_plans + i * sizeof(PlanDesc), &X.plans[i].d, sizeof(PlanDesc));
+  memcpy(h.data() + X.o_units, X.units.data(), X.units.size() * 4);
   e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);

@@ -43,6 +43,7 @@ __global__ void k_plan_tables(Cfg c) {
   if (pd.count == 0) return;
   const int P = pd.P, n = c.n;
   __shared__ int64_t tau_f[kMaxP], tau_b[kMaxP];
+  for (int i = threadIdx.x; i < pd.rp * (pd.kmax + 1); i += blockDim.x) c.k1flags[pd.flag_base + i] = 0;
   // stage sums tau[s] over the stage's layers of every branch (R8)
   for (int s = threadIdx.x; s < P; s += blockDim.x) {
     int64_t tf = 0, tb = 0;
@@ -136,7 +137,7 @@ struct VR {
     if (!M) return H[i];
     const int r = count - 1 - i;
     const int o = own[r >> 5];
-    return T_end - (o < 0 ? S[r] : snap0[o * vstride + r]);
+    return T_end - (o < 0 ? S[r] : __ldcg(&snap0[o * vstride + r]));  // published by another block: L2
   }
   __device__ __forceinline__ int64_t start_at(int i) const { return M ? T_end - H[count - 1 - i] : S[i]; }
   __device__ __forceinline__ int64_t lo_at(int i) const {
@@ -461,20 +462,6 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
   return true;
 }
 
-__device__ bool decode_row_unit(const Cfg& c, int64_t u, bool with_kf, int& e, int& a, int& kf) {
-  for (e = 0; e < c.E; ++e) {
-    const PlanDesc& pd = c.plans[e];
-    if (pd.count == 0) continue;
-    const int64_t nu = (int64_t)pd.rp * (with_kf ? pd.kmax + 1 : 1);
-    if (u < nu) {
-      if (with_kf) { a = (int)(u / (pd.kmax + 1)); kf = (int)(u % (pd.kmax + 1)); }
-      else { a = (int)u; kf = 0; }
-      return true;
-    }
-    u -= nu;
-  }
-  return false;
-}
 
 struct K1Launch {
   int NK, Pmax, CI, KM;  // KM = max kmax
@@ -484,22 +471,43 @@ __host__ __device__ inline size_t k1_smem_bytes(const K1Launch& L) {
   return unit_smem_bytes(L.NK, L.Pmax, L.CI) + (size_t)L.Pmax * L.KM * (8 + 4) + 16;
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // One K1 unit per block, one warp per encoder stage s (a wavefront over
 // chains): chain k of stage s starts when chain k of stage s-1 has ended
 // (shared-memory flags) and chain k-1 of stage s is done (program order).
-// Forward (M = false): successive chains on fresh instances, fill state of
-// every stage snapshotted after every chain.  Backward (M = true): mirrored
-// chains on top of forward snapshot kf.  Both stop at the first failure.
+// Forward (M = false): successive chains on fresh instances; after chain k
+// each stage publishes version k+1 of its fill state (flags[k+1] counts the
+// stages), and the unit ends with flags[0] = 1.  Backward (M = true):
+// mirrored chains on top of forward version kf, started once it is
+// published (or skipped when the forward unit ended with fewer chains).
+// Both stop at the first failure.
 template <bool M>
-__global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
+__device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, int a, int kf) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int stop_at;  // first chain index known to fail (chains >= it are void)
+  __shared__ int go;
   const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int e, a, kf;
-  if (!decode_row_unit(c, blockIdx.x, M, e, a, kf)) return;  // uniform over the block
   const PlanDesc pd = c.plans[e];
   const int P = pd.P, icap = c.icapc + c.icapm;
-  if (M && kf > (int)c.tables[pd.lenF + a]) return;  // uniform: no pipeline of this row has kf forward chains
+  int* flags = c.k1flags + pd.flag_base + (int64_t)a * (pd.kmax + 1);
+  if (M && kf > 0) {  // wait for forward version kf of this row
+    if (threadIdx.x == 0) {
+      int ok;
+      for (;;) {
+        if (ld_acquire(&flags[kf]) >= P) { ok = 1; break; }
+        if (ld_acquire(&flags[0]) != 0) { ok = ld_acquire(&flags[kf]) >= P; break; }
+        __nanosleep(256);
+      }
+      go = ok;
+    }
+    __syncthreads();
+    if (!go) return;  // uniform: no pipeline of this row has kf forward chains
+  }
   const bool active = s < P;  // warps beyond this plan's P only join the barriers
   UnitSm U = carve(dsm, L.NK, L.Pmax, L.CI);
   const size_t ub = unit_smem_bytes(L.NK, L.Pmax, L.CI);
@@ -521,7 +529,7 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
       // block owners: forward starts untouched; mirror loads snapshot kf's map
       int8_t* own = U.own + (2 * s + r) * U.CI;
       const int8_t* gown = c.snap_own + (slot(kf, s) * 2 + r) * c.ci_n;
-      for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? gown[b] : (int8_t)-1;
+      for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? (int8_t)__ldcg((const signed char*)&gown[b]) : (int8_t)-1;
       for (int b = lane; b < U.MW; b += 32) U.wm[(2 * s + r) * U.MW + b] = 0u;
       __syncwarp();
       VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, U, snap0 + (int64_t)s * icap, 0);
@@ -576,12 +584,16 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
         }
       }
       __syncwarp();
-      if (!M)  // publish version k+1 of this stage: the block owner maps after chain k
+      if (!M) {  // publish version k+1 of this stage: the block owner maps after chain k
         for (int r = 0; r < 2; ++r) {
           const int8_t* own = U.own + (2 * s + r) * U.CI;
           int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
           for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
         }
+        __threadfence();  // this lane's block and map stores before the count
+        __syncwarp();
+        if (lane == 0) atomicAdd(&flags[k + 1], 1);
+      }
     }
   }
 #ifdef K1_STATS
@@ -594,9 +606,22 @@ __global__ void k1_chains(Cfg c, int64_t units, K1Launch L) {
   if (threadIdx.x == 0) {  // chains completed by every stage
     int k = 0;
     while (k < pd.kmax && status[(P - 1) * L.KM + k] == 1) ++k;
-    if (M) c.tables[pd.lenB + (int64_t)a * (pd.kmax + 1) + kf] = k;
-    else c.tables[pd.lenF + a] = k;
+    if (M) {
+      c.tables[pd.lenB + (int64_t)a * (pd.kmax + 1) + kf] = k;
+    } else {
+      c.tables[pd.lenF + a] = k;
+      __threadfence();
+      atomicExch(&flags[0], 1);  // forward unit done: versions > lenF never come
+    }
   }
+}
+
+// block size 32 * p: register budgets per p range (MAXT threads, MINB blocks per SM)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, int64_t fwd_units, K1Launch L) {
+  const int32_t u = c.k1units[blockIdx.x];
+  if ((int64_t)blockIdx.x < fwd_units) k1_unit<false>(c, L, u >> 16, (u >> 8) & 255, 0);
+  else k1_unit<true>(c, L, u >> 16, (u >> 8) & 255, u & 255);
 }
 
 }  // namespace
@@ -618,14 +643,21 @@ cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_uni
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   static bool attrs = false;  // opt in to large dynamic shared memory once per process
   if (!attrs) {
-    cudaFuncSetAttribute(k1_chains<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k1_chains<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k1_chains<384, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k1_chains<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k1_chains<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attrs = true;
   }
-  // one block per unit, one warp per stage of the widest plan
-  if (fwd_units > 0) k1_chains<false><<<(unsigned)fwd_units, 32 * c.p, smem, st>>>(c, fwd_units, L);
-  if (bwd_units > 0) k1_chains<true><<<(unsigned)bwd_units, 32 * c.p, smem, st>>>(c, bwd_units, L);
-  if (launches) *launches += (fwd_units > 0) + (bwd_units > 0);
+  // one block per unit (forward units first: their blocks are dispatched
+  // before any backward block that waits on them), one warp per stage of
+  // the widest plan
+  const unsigned nb = (unsigned)(fwd_units + bwd_units), nt = 32 * c.p;
+  if (nb > 0) {
+    if (c.p <= 12) k1_chains<384, 2><<<nb, nt, smem, st>>>(c, fwd_units, L);
+    else if (c.p <= 16) k1_chains<512, 1><<<nb, nt, smem, st>>>(c, fwd_units, L);
+    else k1_chains<1024, 1><<<nb, nt, smem, st>>>(c, fwd_units, L);
+  }
+  if (launches) *launches += (fwd_units + bwd_units > 0);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,7 @@ struct PlanDesc {
   int64_t preF, preB, devF, devB, inbF, lenF, inbB, lenB;
   int64_t devK;       // rp*(n+1) words: uint32 order ranks of DEV_F then DEV_B (0 at cnt 0)
   int64_t slot_base;  // first K1 scratch slot of this plan
+  int64_t flag_base;  // first K1 flag of this plan: per row [kmax + 1] (0: forward done, v: stages that published version v)
 };
 
 // Everything a kernel needs: scalars + device pointers into the workspace.
@@ -65,6 +66,8 @@ struct Cfg {
   int64_t* snap;          // [slots][icapc+icapm] forward fill snapshots (slot k=0 is the working copy)
   int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
   int8_t* snap_own;       // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
+  int32_t* k1flags;       // K1 forward -> backward progress flags (PlanDesc::flag_base); zeroed by k_plan_tables
+  const int32_t* k1units; // K1 units: forward (plan, row) first, then backward (plan, row, kf) by kf; e<<16|a<<8|kf
   const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
 };
 
