@@ -10,7 +10,6 @@ constexpr int64_t kInf = INT64_MAX / 4;   // "no finite shift" / +infinity
 constexpr int64_t kNegInf = -(INT64_MAX / 4);
 constexpr int kMaxP = 32;                 // LLM pipeline stages handled (one lane per stage in K0)
 constexpr int kMaxN = 32;                 // microbatches per LLM pipeline in K2 (one lane per slot)
-constexpr int kSimWarps = 32;             // warps of the K0 warm-up search block
 
 // List ids in the packed input: 0 = LLM layer fwd, 1 = LLM layer bwd,
 // 2 + 2*(branch*ntp + ti) = encoder layer fwd at TP option ti, +1 = bwd.

@@ -7,10 +7,12 @@
 // goes into compute-free time, encoder comm into comm-free time.
 // Readings R2-R6.
 //
-// k0_template: one block of 32 warps.  A warp simulates the whole LLM
-//   pipeline (lane = stage) as an ASAP list schedule in the fixed per-stage
-//   Megatron order; the reverse-stage warm-up search (R5) tests up to 32
-//   warm-up values of one stage at once, one warp each.
+// k0_wave: one warp per simulation (lane = stage): the ASAP list schedule
+//   of the LLM pipeline in the fixed per-stage Megatron order, in lockstep
+//   rounds; the default warm-up vector and every (stage, w) trial of the
+//   reverse-stage warm-up search (R5) run at once, speculatively.
+// k0_final: verifies the speculation (exact fallback on all warps of one
+//   block), fixes W and T_end.
 // k0_intervals: one block per LLM stage.  Threads expand the stage's ops
 //   into kernels (lane-parallel over the kernel index), emit the gap after
 //   each compute kernel (compute-free interval) and after each comm kernel
@@ -40,20 +42,20 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
   return v;
 }
 
-// K0 per-simulation shared memory: [vtab: n*v shorts x 2][optab: p*nops
-// uint64][endv: p*2*v*n int64].  vtab maps a virtual id k to its forward
-// chunk and microbatch (R2).  optab[s*nops + pos] packs the op at position
-// pos of stage s for the current warm-up vector: bits 0-15 its slot in
-// endv, 16-31 the slot of its cross-op dependency, 32-47 the slot of the
-// previous op of its stage (0xFFFF = none), 48 forward, 49 the dependency
-// is on another stage (adds pp_p2p).
-constexpr uint64_t kNone = 0xFFFF;
-constexpr int kSimThreads = 256;
-constexpr int kFinalThreads = 256;
+// K0 shared memory: [vtab: n*v shorts x 2] then, per simulating warp,
+// [W: kMaxP ints][endv: p*2*v*n int64].  vtab maps a virtual id k to its
+// forward chunk and microbatch (R2); endv[slot] = end of the op in that
+// slot (-1: not placed yet).
+constexpr int kNone = 0xFFFF;
+constexpr int kSimWarps = 8;  // simulations per block
 
 __host__ __device__ __forceinline__ size_t k0_vtab_bytes(int n, int v) { return ((size_t)4 * n * v + 15) & ~size_t(15); }
-__host__ __device__ __forceinline__ size_t k0_sim_bytes(int p, int nops, int v, int n) {
-  return k0_vtab_bytes(n, v) + (size_t)p * nops * 8 + (size_t)p * 2 * v * n * 8;
+__host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int v, int n) {
+  return (size_t)kMaxP * 4 + (size_t)p * 2 * v * n * 8;
+}
+__host__ __device__ __forceinline__ int k0_sim_warps(int p, int v, int n) {
+  const size_t room = 200 * 1024 - k0_vtab_bytes(n, v);
+  return (int)max((size_t)1, min((size_t)kSimWarps, room / k0_warp_bytes(p, v, n)));
 }
 
 // op at position pos of stage s under warm-up count Ws (R2): its endv slot,
@@ -80,96 +82,65 @@ __device__ __forceinline__ void op_slots(int p, int v, int n, int s, int pos, in
   cross = ds >= 0 && ds != s;
 }
 
-// Fill vtab and optab for the warm-up vector W (whole block).
-__device__ void build_optab(const Cfg& c, const int* W) {
-  const int p = c.p, v = c.v, n = c.n, nops = c.nops, nv = n * v;
+__device__ void build_vtab(const Cfg& c) {
+  const int p = c.p, v = c.v, n = c.n, nv = n * v;
   short* vch = reinterpret_cast<short*>(k0_dsm);
   short* vmb = vch + nv;
-  uint64_t* tab = reinterpret_cast<uint64_t*>(k0_dsm + k0_vtab_bytes(n, v));
   for (int k = threadIdx.x; k < nv; k += blockDim.x) {
     vch[k] = (short)((k % (p * v)) / p);
     vmb[k] = (short)((k / (p * v)) * p + (k % p));
   }
   __syncthreads();
-  for (int s = 0; s < p; ++s) {
-    const int Ws = W[s];
-    for (int pos = threadIdx.x; pos < nops; pos += blockDim.x) {
-      int self, dep, fwd, cross, pself = (int)kNone, pd, pf, pc;
-      op_slots(p, v, n, s, pos, Ws, vch, vmb, self, dep, fwd, cross);
-      if (pos > 0) op_slots(p, v, n, s, pos - 1, Ws, vch, vmb, pself, pd, pf, pc);
-      tab[s * nops + pos] = (uint64_t)self | ((uint64_t)dep << 16) | ((uint64_t)pself << 32) |
-                            ((uint64_t)fwd << 48) | ((uint64_t)cross << 49);
-    }
-  }
-  __syncthreads();
 }
 
-// ASAP list schedule of the pipeline in optab's fixed per-stage order (R2,
-// R3), computed by the whole block as a relaxation: every round, each op
-// whose stage predecessor and dependency have ended gets start = max(their
-// ends (+ pp_p2p across stages), T_ag).  A round without progress before
-// every op is placed means the order deadlocks.  record: also write op
-// starts, F, B.  Returns ok and the span (max last-op end).
-__device__ void block_simulate(const Cfg& c, bool record, int64_t dur_f, int64_t dur_b, int64_t* span, int* ok) {
-  __shared__ long long red[kSimThreads / 32];
-  const int p = c.p, v = c.v, n = c.n, nops = c.nops, total = p * nops;
-  const uint64_t* tab = reinterpret_cast<const uint64_t*>(k0_dsm + k0_vtab_bytes(n, v));
-  volatile int64_t* endv = reinterpret_cast<volatile int64_t*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)total * 8);
-  const int sz = p * 2 * v * n;
+// One simulation per warp, lane = stage: the ASAP list schedule of the
+// pipeline in the fixed per-stage order for warm-up vector W (R2, R3).
+// Every round each stage places its next op if that op's dependency has
+// ended: start = max(previous op's end, dependency end (+ pp_p2p across
+// stages), T_ag).  A round without progress before every op is placed
+// means the order deadlocks.  record: also write op starts, F, B.
+// Returns the span (max last-op end), or -1 on deadlock.
+__device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, bool record, int64_t dur_f,
+                                 int64_t dur_b) {
+  const int lane = threadIdx.x & 31, p = c.p, v = c.v, n = c.n, nops = c.nops, nv = n * v;
+  const short* vch = reinterpret_cast<const short*>(k0_dsm);
+  const short* vmb = vch + nv;
+  volatile int64_t* endv = endv_;
+  for (int i = lane; i < p * 2 * v * n; i += 32) endv[i] = -1;
+  __syncwarp();
   const int64_t T_ag = max((int64_t)0, c.T_ag), pp2p = c.pp_p2p;
-  for (int i = threadIdx.x; i < sz; i += blockDim.x) endv[i] = -1;
-  __syncthreads();
-  int left = 1;
-  while (left) {
-    int prog = 0;
-    left = 0;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const uint64_t e = tab[i];
-      const int self = (int)(e & kNone);
-      if (endv[self] >= 0) continue;
-      int64_t t = T_ag;  // every op starts after the DP all-gather (R3)
-      const int prev = (int)((e >> 32) & kNone), dep = (int)((e >> 16) & kNone);
-      if (prev != (int)kNone) {
-        const int64_t pe = endv[prev];
-        if (pe < 0) { left = 1; continue; }
-        t = max(t, pe);
-      }
-      if (dep != (int)kNone) {
-        const int64_t de = endv[dep];
-        if (de < 0) { left = 1; continue; }
-        t = max(t, de + ((e >> 49) & 1 ? pp2p : 0));
-      }
-      const bool fwd = (e >> 48) & 1;
-      endv[self] = t + (fwd ? dur_f : dur_b);
-      prog = 1;
-      if (record) {
-        c.opstart[i] = t;  // optab is stage-major, like opstart
-        const int mb = self % n, ch = (self / n) % v;
-        if (i < nops && ch == 0) {
-          if (fwd) c.F[mb] = t;               // F_i: start of F(stage 0, chunk 0, i) (R4)
-          else c.B[mb] = t + dur_b;           // B_i: end of B(stage 0, chunk 0, i)
+  const int s = lane, Ws = s < p ? W[s] : 0;
+  int pos = s < p ? 0 : nops;
+  int64_t tprev = T_ag;  // every op starts after the DP all-gather (R3)
+  for (;;) {
+    bool prog = false;
+    if (pos < nops) {
+      int self, dep, fwd, cross;
+      op_slots(p, v, n, s, pos, Ws, vch, vmb, self, dep, fwd, cross);
+      const int64_t de = dep == kNone ? 0 : endv[dep];
+      if (de >= 0) {
+        const int64_t t = dep == kNone ? tprev : max(tprev, de + (cross ? pp2p : 0));
+        const int64_t e = t + (fwd ? dur_f : dur_b);
+        endv[self] = e;
+        if (record) {
+          c.opstart[(int64_t)s * nops + pos] = t;
+          const int mb = self % n, ch = (self / n) % v;
+          if (s == 0 && ch == 0) {
+            if (fwd) c.F[mb] = t;      // F_i: start of F(stage 0, chunk 0, i) (R4)
+            else c.B[mb] = e;          // B_i: end of B(stage 0, chunk 0, i)
+          }
         }
+        tprev = e;
+        ++pos;
+        prog = true;
       }
     }
-    prog = __syncthreads_or(prog);
-    left = __syncthreads_or(left);
-    if (left && !prog) break;  // deadlock
+    __syncwarp();
+    const unsigned left = __ballot_sync(0xffffffffu, pos < nops), any = __ballot_sync(0xffffffffu, prog);
+    if (!left) break;
+    if (!any) return -1;  // deadlock
   }
-  *ok = !left;
-  // span: max over stages of the last op's end
-  int64_t mx = 0;
-  for (int s = threadIdx.x; s < p; s += blockDim.x) mx = max(mx, (int64_t)endv[tab[s * nops + nops - 1] & kNone]);
-  mx = warp_max64(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    int64_t x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
-    x = warp_max64(x);
-    if (threadIdx.x == 0) red[0] = x;
-  }
-  __syncthreads();
-  *span = red[0];
-  __syncthreads();
+  return warp_max64(tprev);  // lanes >= p hold T_ag <= every end
 }
 
 __device__ __forceinline__ int default_w(int p, int v, int n, int s) {  // Megatron default warm-up (R2)
@@ -189,50 +160,52 @@ __device__ __forceinline__ void dur_fb(const Cfg& c, int64_t& f, int64_t& b) {
   b = (int64_t)c.lc * list_sum(c, 1);
 }
 
-// K0a, one block per simulation: block 0 the default warm-up (its span must
-// be preserved; it is the final schedule under policy 0), block 1 + t trial
-// t = (s, w) of GetEncLLMDep's warm-up adjustment (R5: for s = p-1
-// .. 0 the smallest w in [0, Wdef_s] keeping the schedule deadlock-free with
-// the default span).  All stage phases run at once, each assuming the later
-// stages take their guessed value; the trial with every stage at its guess
-// records its schedule (it is the final one when K0b verifies every guess).
-// res[b] = span, or -1 if the schedule deadlocks.
-__global__ void __launch_bounds__(kSimThreads) k0_wave(Cfg c) {
-  __shared__ int Wsm[kMaxP];
-  const int p = c.p, v = c.v, n = c.n;
+// K0a, one warp per simulation: simulation 0 the default warm-up (its span
+// must be preserved; it is the final schedule under policy 0), simulation
+// 1 + t trial t = (s, w) of GetEncLLMDep's warm-up adjustment (R5, P:444:
+// for s = p-1 .. 0 the smallest w in [0, Wdef_s] keeping the schedule
+// deadlock-free with the default span).  All stage phases run at once, each
+// assuming the later stages take their guessed value; the trial with every
+// stage at its guess records its schedule (it is the final one when K0b
+// verifies every guess).  res[b] = span, or -1 if the schedule deadlocks.
+__global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int wpb) {
+  const int p = c.p, v = c.v, n = c.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  build_vtab(c);
+  const int b = blockIdx.x * wpb + warp;
+  if (warp >= wpb || b >= nsim) return;
+  int* Wsm = reinterpret_cast<int*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)warp * k0_warp_bytes(p, v, n));
+  int64_t* endv = reinterpret_cast<int64_t*>(Wsm + kMaxP);
   int s = -1, w = 0;
-  if (blockIdx.x > 0) {
+  if (b > 0) {
     if (c.policy != 1) return;
     s = 0;
-    w = blockIdx.x - 1;
+    w = b - 1;
     while (s < p && w > default_w(p, v, n, s)) { w -= default_w(p, v, n, s) + 1; ++s; }
     if (s >= p) return;
   }
   int64_t df, db;
   dur_fb(c, df, db);
-  if (threadIdx.x < p) {
-    const int t = threadIdx.x, d = default_w(p, v, n, t);
-    Wsm[t] = s < 0 || t < s ? d : t == s ? w : guess_w(p, v, n, t);
-    if (blockIdx.x == 0) c.Wdef[t] = d;
+  if (lane < p) {
+    const int d = default_w(p, v, n, lane);
+    Wsm[lane] = s < 0 || lane < s ? d : lane == s ? w : guess_w(p, v, n, lane);
+    if (b == 0) c.Wdef[lane] = d;
   }
-  __syncthreads();
-  build_optab(c, Wsm);
+  __syncwarp();
   const bool all_guess = s == 0 && w == guess_w(p, v, n, 0);
-  const bool record = c.policy == 1 ? all_guess : blockIdx.x == 0;
-  int64_t sp;
-  int ok;
-  block_simulate(c, record, df, db, &sp, &ok);
-  if (threadIdx.x == 0) c.k0res[blockIdx.x] = ok ? sp : -1;
+  const bool record = c.policy == 1 ? all_guess : b == 0;
+  const int64_t sp = warp_simulate(c, Wsm, endv, record, df, db);
+  if (lane == 0) c.k0res[b] = sp;
 }
 
 // K0b: verify the wave from the last stage down; in the common case the
 // recorded all-guess schedule is the final one.  Otherwise redo the phases
-// below the first wrong guess exactly, one trial at a time, and record the
-// final schedule.  Writes W, T_end and the ok flag.
-__global__ void __launch_bounds__(kFinalThreads) k0_final(Cfg c) {
+// below the first wrong guess exactly (the trials of one phase run on all
+// warps at once; the smallest successful w wins) and record the final
+// schedule.  Writes W, T_end and the ok flag.
+__global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   __shared__ int Wcur[kMaxP], firstb[kMaxP + 1];
-  __shared__ int s0_sm;
-  const int p = c.p, v = c.v, n = c.n;
+  __shared__ int s0_sm, wbest;
+  const int p = c.p, v = c.v, n = c.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t span_def = c.k0res[0];
   if (threadIdx.x == 0) c.scal[0] = span_def;
   if (span_def < 0) {  // default schedule deadlocks: template fails
@@ -278,30 +251,34 @@ __global__ void __launch_bounds__(kFinalThreads) k0_final(Cfg c) {
     }
     return;
   }
-  __shared__ int Wt[kMaxP];
+  build_vtab(c);
+  int* Wt = reinterpret_cast<int*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)warp * k0_warp_bytes(p, v, n));
+  int64_t* endv = reinterpret_cast<int64_t*>(Wt + kMaxP);
   for (int s = s0 - 1; s >= 0; --s) {  // exact sequential phases
-    for (int w = 0; w <= default_w(p, v, n, s); ++w) {
-      if (threadIdx.x < p) Wt[threadIdx.x] = threadIdx.x == s ? w : Wcur[threadIdx.x];
-      __syncthreads();
-      build_optab(c, Wt);
-      int64_t sp;
-      int ok;
-      block_simulate(c, false, df, db, &sp, &ok);
-      if (ok && sp == span_def) {  // uniform over the block
-        if (threadIdx.x == 0) Wcur[s] = w;
-        __syncthreads();
-        break;
+    const int nw = default_w(p, v, n, s) + 1;
+    if (threadIdx.x == 0) wbest = INT32_MAX;
+    __syncthreads();
+    for (int w0 = 0; w0 < nw; w0 += wpb) {
+      const int w = w0 + warp;
+      if (warp < wpb && w < nw) {
+        if (lane < p) Wt[lane] = lane == s ? w : Wcur[lane];
+        __syncwarp();
+        const int64_t sp = warp_simulate(c, Wt, endv, false, df, db);
+        if (lane == 0 && sp == span_def) atomicMin(&wbest, w);
       }
+      __syncthreads();
+      if (wbest != INT32_MAX) break;  // uniform
     }
+    if (threadIdx.x == 0) Wcur[s] = wbest;  // w = Wdef_s always succeeds (default schedule)
+    __syncthreads();
   }
-  build_optab(c, Wcur);
-  int64_t sp;
-  int ok;
-  block_simulate(c, true, df, db, &sp, &ok);
-  if (threadIdx.x < p) c.W[threadIdx.x] = Wcur[threadIdx.x];
-  if (threadIdx.x == 0) {
-    c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
-    c.scal[2] = ok;
+  if (warp == 0) {
+    const int64_t sp = warp_simulate(c, Wcur, endv, true, df, db);
+    if (lane < p) c.W[lane] = Wcur[lane];
+    if (lane == 0) {
+      c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
+      c.scal[2] = sp >= 0;
+    }
   }
 }
 
@@ -459,7 +436,8 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
 }  // namespace
 
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
-  const size_t smem = k0_sim_bytes(c.p, c.nops, c.v, c.n);
+  const int wpb = k0_sim_warps(c.p, c.v, c.n);
+  const size_t smem = k0_vtab_bytes(c.n, c.v) + (size_t)wpb * k0_warp_bytes(c.p, c.v, c.n);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
   static bool attrs = false;  // opt in to large dynamic shared memory once per process
   if (!attrs) {
@@ -467,8 +445,9 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
     cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attrs = true;
   }
-  k0_wave<<<1 + c.k0_trials, kSimThreads, smem, st>>>(c);
-  k0_final<<<1, kFinalThreads, smem, st>>>(c);
+  const int nsim = 1 + c.k0_trials;
+  k0_wave<<<(nsim + wpb - 1) / wpb, 32 * kSimWarps, smem, st>>>(c, nsim, wpb);
+  k0_final<<<1, 32 * kSimWarps, smem, st>>>(c, wpb);
   k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int), st>>>(c);
   if (launches) *launches += 3;
   return cudaGetLastError();
