@@ -178,7 +178,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
     X.nk_max = std::max<int>(X.nk_max, (int)nk);
   }
   if ((size_t)X.p * 2 * X.v * X.n * 8 + (size_t)X.p * X.nops * 8 + 4 * (size_t)X.n * X.v + 16 > 200 * 1024 ||
-      (size_t)X.p * 2 * X.v * X.n > 65535)
+      (size_t)X.p * 2 * X.v * X.n > 32767)
     return fail(OPTIMUS_ERANGE, "PP*V*N_mb too large for the K0 shared-memory simulation");
   {
     const size_t ci = (size_t)(std::max(X.icapc, X.icapm) + 31) / 32;
@@ -344,6 +344,7 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.comm_hi = (int64_t*)(ws + X.o_comm_hi);
   c.bmax = (int64_t*)(ws + X.o_bmax);
   c.ci_n = (std::max(X.icapc, X.icapm) + 31) / 32;
+  c.nflags = (int32_t)X.n_flags;
   c.bestw = (int32_t*)(ws + X.o_sim);
   c.k0res = (int64_t*)(ws + X.o_k0res);
   c.k0_trials = X.k0_trials;
@@ -360,7 +361,6 @@ int build(optimus_ctx* c, cudaStream_t st) {
   c->build_launches = 0;
   if (c->timing) CK(cudaEventRecord(c->ev[0], st));
   CK(launch_template(c->cfg, st, &c->build_launches));
-  CK(launch_plan_tables(c->cfg, st, &c->build_launches));
   CK(launch_chain_tables(c->cfg, c->X.fwd_units, c->X.bwd_units, st, &c->build_launches));
   if (c->timing) CK(cudaEventRecord(c->ev[1], st));
   return OPTIMUS_OK;
@@ -426,6 +426,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);

@@ -12,14 +12,19 @@
 // k-th forward chain of ANY pipeline of PP-row a ends at INB_F[a][k], and
 // the k-th backward chain after kf forward chains at INB_B[a][kf][k].
 //
-// k_plan_tables: one block per plan — stage sums, coarse GPipe fill tables
-//   PRE_F / PRE_B (R9) and the critical-path tables DEV_F / DEV_B (R11).
-// k1_forward:  one warp per (plan, row): successive forward chains until the
-//   first failure; snapshots the fill state after each chain.
-// k1_backward: one warp per (plan, row, kf): mirrored backward chains on top
-//   of forward snapshot kf.
-// First fit is warp-cooperative: a window of 32 consecutive intervals lives
-// in registers (lane i = interval base+i), one ballot tests all 32.
+// K1 (k1_chains), one launch, one block per unit, one warp per encoder stage:
+//   forward units (plan, row): successive forward chains until the first
+//   failure, publishing a versioned snapshot of the fill state after each;
+//   backward units (plan, row, kf): mirrored backward chains on top of
+//   forward version kf, started as soon as it is published.  The last E
+//   blocks build the per-plan tables K2 reads: coarse GPipe fill tables
+//   PRE_F / PRE_B (R9), the critical-path tables DEV_F / DEV_B (R11) and
+//   their order ranks.
+// First fit: while kernels fit the current interval of their resource, 32
+// kernels are placed at once by a max-plus scan over the warp; otherwise a
+// window of 32 consecutive intervals lives in registers (lane i = interval
+// base+i) and one ballot tests all 32, skipping blocks that end before the
+// ready time or cannot hold the kernel.
 #include <algorithm>
 
 #include "optimus_dev.cuh"
@@ -37,13 +42,11 @@ __shared__ unsigned long long k1st[32][8];  // placements, fast hits, ballots, w
 #endif
 
 // ------------------------------------------------------------ plan tables
-__global__ void k_plan_tables(Cfg c) {
-  const int e = blockIdx.x;
+__device__ void plan_tables(const Cfg& c, int e) {
   const PlanDesc pd = c.plans[e];
   if (pd.count == 0) return;
   const int P = pd.P, n = c.n;
   __shared__ int64_t tau_f[kMaxP], tau_b[kMaxP];
-  for (int i = threadIdx.x; i < pd.rp * (pd.kmax + 1); i += blockDim.x) c.k1flags[pd.flag_base + i] = 0;
   // stage sums tau[s] over the stage's layers of every branch (R8)
   for (int s = threadIdx.x; s < P; s += blockDim.x) {
     int64_t tf = 0, tb = 0;
@@ -618,7 +621,11 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
 
 // block size 32 * p: register budgets per p range (MAXT threads, MINB blocks per SM)
 template <int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, int64_t fwd_units, K1Launch L) {
+__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, int64_t fwd_units, int64_t units, K1Launch L) {
+  if ((int64_t)blockIdx.x >= units) {  // the per-plan tables ride along (only K2 reads them)
+    plan_tables(c, (int)(blockIdx.x - units));
+    return;
+  }
   const int32_t u = c.k1units[blockIdx.x];
   if ((int64_t)blockIdx.x < fwd_units) k1_unit<false>(c, L, u >> 16, (u >> 8) & 255, 0);
   else k1_unit<true>(c, L, u >> 16, (u >> 8) & 255, u & 255);
@@ -626,11 +633,6 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, int64_t fwd_units
 
 }  // namespace
 
-cudaError_t launch_plan_tables(const Cfg& c, cudaStream_t st, int* launches) {
-  k_plan_tables<<<c.E, 128, 0, st>>>(c);
-  if (launches) *launches += 1;
-  return cudaGetLastError();
-}
 
 cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st,
                                 int* launches) {
@@ -651,13 +653,12 @@ cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_uni
   // one block per unit (forward units first: their blocks are dispatched
   // before any backward block that waits on them), one warp per stage of
   // the widest plan
-  const unsigned nb = (unsigned)(fwd_units + bwd_units), nt = 32 * c.p;
-  if (nb > 0) {
-    if (c.p <= 12) k1_chains<384, 2><<<nb, nt, smem, st>>>(c, fwd_units, L);
-    else if (c.p <= 16) k1_chains<512, 1><<<nb, nt, smem, st>>>(c, fwd_units, L);
-    else k1_chains<1024, 1><<<nb, nt, smem, st>>>(c, fwd_units, L);
-  }
-  if (launches) *launches += (fwd_units + bwd_units > 0);
+  const int64_t units = fwd_units + bwd_units;
+  const unsigned nb = (unsigned)(units + c.E), nt = 32 * c.p;
+  if (c.p <= 12) k1_chains<384, 2><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
+  else if (c.p <= 16) k1_chains<512, 1><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
+  else k1_chains<1024, 1><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
+  if (launches) *launches += 1;
   return cudaGetLastError();
 }
 

@@ -35,6 +35,7 @@ struct Cfg {
   int32_t k0_trials;     // sum over stages of (Wdef_s + 1): K0 warm-up trials
   int32_t nk_max;        // max over TP options of the encoder's total kernel count (all layers, all branches)
   int32_t ci_n;          // 32-interval blocks per interval list: ceil(max(icapc, icapm) / 32)
+  int32_t nflags;        // K1 flags (zeroed by k0_final)
   int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
   // packed inputs
   const int32_t* lkind;   // kernel kinds, all lists concatenated
@@ -44,7 +45,7 @@ struct Cfg {
   // template (K0)
   int32_t* W;             // [p] adjusted warm-up counts (policy 1) or defaults
   int32_t* Wdef;          // [p]
-  int64_t* scal;          // [0] span_def, [1] T_end, [2] ok flag
+  int64_t* scal;          // [0] span_def, [1] T_end, [2] ok flag, [3] K0 wave: span_def + 1 once known (0 before)
   int64_t* F;             // [n]
   int64_t* B;             // [n]
   int64_t* w;             // [p] first LLM compute instant
@@ -65,7 +66,7 @@ struct Cfg {
   int64_t* snap;          // [slots][icapc+icapm] forward fill snapshots (slot k=0 is the working copy)
   int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
   int8_t* snap_own;       // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
-  int32_t* k1flags;       // K1 forward -> backward progress flags (PlanDesc::flag_base); zeroed by k_plan_tables
+  int32_t* k1flags;       // K1 forward -> backward progress flags (PlanDesc::flag_base); zeroed by k0_final
   const int32_t* k1units; // K1 units: forward (plan, row) first, then backward (plan, row, kf) by kf; e<<16|a<<8|kf
   const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
 };
@@ -100,7 +101,6 @@ __host__ __device__ inline OpRef op_at(int p, int v, int n, int W, int pos) {
 // Host launchers (defined in the .cu files).
 namespace optimus {
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
-cudaError_t launch_plan_tables(const Cfg& c, cudaStream_t st, int* launches);
 cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st, int* launches);
 struct EvalArgs {
   uint64_t begin, end;       // global index range (eval_candidates)

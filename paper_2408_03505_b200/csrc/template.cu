@@ -43,15 +43,16 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
 }
 
 // K0 shared memory: [vtab: n*v shorts x 2] then, per simulating warp,
-// [W: kMaxP ints][endv: p*2*v*n int64].  vtab maps a virtual id k to its
-// forward chunk and microbatch (R2); endv[slot] = end of the op in that
-// slot (-1: not placed yet).
+// [W: kMaxP ints][endv: p*(2vn+1) int64][optab: p*(nops+1) uint32].  vtab
+// maps a virtual id k to its forward chunk and microbatch (R2); endv[slot]
+// = end of the op in that slot (-1: not placed yet).  Per-stage strides are
+// odd (2vn+1, nops+1) so that the 32 lanes (stages) hit distinct banks.
 constexpr int kNone = 0xFFFF;
 constexpr int kSimWarps = 8;  // simulations per block
 
 __host__ __device__ __forceinline__ size_t k0_vtab_bytes(int n, int v) { return ((size_t)4 * n * v + 15) & ~size_t(15); }
 __host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int v, int n) {
-  return (size_t)kMaxP * 4 + (size_t)p * 2 * v * n * 8;
+  return (size_t)kMaxP * 4 + (size_t)p * (2 * v * n + 1) * (8 + 4);  // W, endv, optab (odd per-stage strides)
 }
 __host__ __device__ __forceinline__ int k0_sim_warps(int p, int v, int n) {
   const size_t room = 200 * 1024 - k0_vtab_bytes(n, v);
@@ -95,50 +96,82 @@ __device__ void build_vtab(const Cfg& c) {
 
 // One simulation per warp, lane = stage: the ASAP list schedule of the
 // pipeline in the fixed per-stage order for warm-up vector W (R2, R3).
-// Every round each stage places its next op if that op's dependency has
-// ended: start = max(previous op's end, dependency end (+ pp_p2p across
-// stages), T_ag).  A round without progress before every op is placed
-// means the order deadlocks.  record: also write op starts, F, B.
-// Returns the span (max last-op end), or -1 on deadlock.
-__device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, bool record, int64_t dur_f,
-                                 int64_t dur_b) {
+// Each stage places its ops in order; an op starts at max(previous op's
+// end, dependency end (+ pp_p2p across stages), T_ag) once its dependency
+// has ended, one op per stage per round between warp barriers.  No
+// progress in a whole check period (8 rounds) before every op is placed means the
+// order deadlocks.  record: also write op starts, F, B.  Returns the span
+// (max last-op end), or -1 on deadlock.  A trial of R5 that must keep the
+// default span returns -3 as soon as an op ends after `bound` (the default
+// span when known; poll: read it from scal[3] once the default simulation
+// has published it).
+__device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uint32_t* optab, bool record,
+                                 int64_t dur_f, int64_t dur_b, int64_t bound = INT64_MAX, bool poll = false) {
   const int lane = threadIdx.x & 31, p = c.p, v = c.v, n = c.n, nops = c.nops, nv = n * v;
   const short* vch = reinterpret_cast<const short*>(k0_dsm);
   const short* vmb = vch + nv;
   volatile int64_t* endv = endv_;
-  for (int i = lane; i < p * 2 * v * n; i += 32) endv[i] = -1;
+  const int S = 2 * v * n;  // slots per stage; padded stride S + 1
+  for (int i = lane; i < p * (S + 1); i += 32) endv[i] = -1;
+  const int s = lane;
+  // op tables, built by the whole warp: self slot | dep slot << 15 (0x7FFF
+  // none) | fwd << 30 | cross << 31 (padded slots)
+  for (int st = 0, pos = lane; st < p;) {
+    int self, dep, fwd, cross;
+    op_slots(p, v, n, st, pos, W[st], vch, vmb, self, dep, fwd, cross);
+    const int ps = self + self / S, pd = dep == kNone ? 0x7FFF : dep + dep / S;
+    optab[(size_t)st * (nops + 1) + pos] = (uint32_t)ps | (uint32_t)pd << 15 | (uint32_t)fwd << 30 | (uint32_t)cross << 31;
+    pos += 32;
+    while (st < p && pos >= nops) { pos -= nops; ++st; }
+  }
+  const uint32_t* tab = optab + (size_t)s * (nops + 1);
   __syncwarp();
   const int64_t T_ag = max((int64_t)0, c.T_ag), pp2p = c.pp_p2p;
-  const int s = lane, Ws = s < p ? W[s] : 0;
   int pos = s < p ? 0 : nops;
   int64_t tprev = T_ag;  // every op starts after the DP all-gather (R3)
-  for (;;) {
-    bool prog = false;
-    if (pos < nops) {
-      int self, dep, fwd, cross;
-      op_slots(p, v, n, s, pos, Ws, vch, vmb, self, dep, fwd, cross);
-      const int64_t de = dep == kNone ? 0 : endv[dep];
-      if (de >= 0) {
-        const int64_t t = dep == kNone ? tprev : max(tprev, de + (cross ? pp2p : 0));
-        const int64_t e = t + (fwd ? dur_f : dur_b);
-        endv[self] = e;
-        if (record) {
-          c.opstart[(int64_t)s * nops + pos] = t;
-          const int mb = self % n, ch = (self / n) % v;
-          if (s == 0 && ch == 0) {
-            if (fwd) c.F[mb] = t;      // F_i: start of F(stage 0, chunk 0, i) (R4)
-            else c.B[mb] = e;          // B_i: end of B(stage 0, chunk 0, i)
-          }
+  bool prog = false;
+  uint32_t op = pos < nops ? tab[pos] : 0;
+  int64_t polled = 0;
+  for (int round = 0;; ++round) {
+    if (poll && (round & 7) == 0 && lane == 0) polled = *(volatile int64_t*)&c.scal[3];  // used 8 rounds later
+    const int dep = (op >> 15) & 0x7FFF;
+    const int64_t de = pos >= nops ? -1 : dep == 0x7FFF ? 0 : endv[dep];
+    if (de >= 0) {  // one op per stage per round (running ahead serialises the warp)
+      const uint32_t nxt = tab[min(pos + 1, nops - 1)];
+      const int self = op & 0x7FFF;
+      const bool fwd = (op >> 30) & 1;
+      const int64_t t = dep == 0x7FFF ? tprev : max(tprev, de + ((op >> 31) ? pp2p : 0));
+      const int64_t e = t + (fwd ? dur_f : dur_b);
+      endv[self] = e;
+      if (record) {
+        c.opstart[(int64_t)s * nops + pos] = t;
+        const int us = self - self / (S + 1);  // unpadded slot
+        const int mb = us % n, ch = (us / n) % v;
+        if (s == 0 && ch == 0) {
+          if (fwd) c.F[mb] = t;      // F_i: start of F(stage 0, chunk 0, i) (R4)
+          else c.B[mb] = e;          // B_i: end of B(stage 0, chunk 0, i)
         }
-        tprev = e;
-        ++pos;
-        prog = true;
       }
+      tprev = e;
+      ++pos;
+      op = nxt;
+      prog = true;
     }
     __syncwarp();
-    const unsigned left = __ballot_sync(0xffffffffu, pos < nops), any = __ballot_sync(0xffffffffu, prog);
-    if (!left) break;
-    if (!any) return -1;  // deadlock
+    if ((round & 7) == 7) {  // periodic checks: done, deadlock, default span exceeded
+      const unsigned left = __ballot_sync(0xffffffffu, pos < nops), any = __ballot_sync(0xffffffffu, prog);
+#ifdef K0_STATS
+      if (!left && lane == 0 && record) printf("K0ROUNDS %d\n", round);
+#endif
+      if (!left) break;
+      if (!any) return -1;  // no progress in 8 rounds: deadlock
+      prog = false;
+      if (poll && bound == INT64_MAX) {
+        const int64_t b = __shfl_sync(0xffffffffu, polled, 0);
+        if (b > 0) bound = b - 1;
+      }
+      if (__any_sync(0xffffffffu, tprev > bound)) return -3;
+    }
   }
   return warp_max64(tprev);  // lanes >= p hold T_ag <= every end
 }
@@ -175,6 +208,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int w
   if (warp >= wpb || b >= nsim) return;
   int* Wsm = reinterpret_cast<int*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)warp * k0_warp_bytes(p, v, n));
   int64_t* endv = reinterpret_cast<int64_t*>(Wsm + kMaxP);
+  uint32_t* optab = reinterpret_cast<uint32_t*>(endv + (size_t)p * (2 * v * n + 1));
   int s = -1, w = 0;
   if (b > 0) {
     if (c.policy != 1) return;
@@ -193,8 +227,17 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int w
   __syncwarp();
   const bool all_guess = s == 0 && w == guess_w(p, v, n, 0);
   const bool record = c.policy == 1 ? all_guess : b == 0;
-  const int64_t sp = warp_simulate(c, Wsm, endv, record, df, db);
-  if (lane == 0) c.k0res[b] = sp;
+#ifdef K0_STATS
+  const long long t0 = clock64();
+#endif
+  const int64_t sp = warp_simulate(c, Wsm, endv, optab, record, df, db, INT64_MAX, b > 0 && !record);
+#ifdef K0_STATS
+  if (lane == 0) printf("K0ST b=%d s=%d w=%d sp=%lld cyc=%lld blk=%d\n", b, s, w, (long long)sp, clock64() - t0, blockIdx.x);
+#endif
+  if (lane == 0) {
+    c.k0res[b] = sp;
+    if (b == 0) atomicExch((unsigned long long*)&c.scal[3], (unsigned long long)(sp + 1));  // trials may stop early
+  }
 }
 
 // K0b: verify the wave from the last stage down; in the common case the
@@ -207,7 +250,11 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   __shared__ int s0_sm, wbest;
   const int p = c.p, v = c.v, n = c.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t span_def = c.k0res[0];
-  if (threadIdx.x == 0) c.scal[0] = span_def;
+  if (threadIdx.x == 0) {
+    c.scal[0] = span_def;
+    c.scal[3] = 0;  // reset for the next build's wave
+  }
+  for (int i = threadIdx.x; i < c.nflags; i += blockDim.x) c.k1flags[i] = 0;  // K1 progress flags
   if (span_def < 0) {  // default schedule deadlocks: template fails
     if (threadIdx.x == 0) c.scal[2] = 0;
     return;
@@ -254,6 +301,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   build_vtab(c);
   int* Wt = reinterpret_cast<int*>(k0_dsm + k0_vtab_bytes(n, v) + (size_t)warp * k0_warp_bytes(p, v, n));
   int64_t* endv = reinterpret_cast<int64_t*>(Wt + kMaxP);
+  uint32_t* optab = reinterpret_cast<uint32_t*>(endv + (size_t)p * (2 * v * n + 1));
   for (int s = s0 - 1; s >= 0; --s) {  // exact sequential phases
     const int nw = default_w(p, v, n, s) + 1;
     if (threadIdx.x == 0) wbest = INT32_MAX;
@@ -263,7 +311,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
       if (warp < wpb && w < nw) {
         if (lane < p) Wt[lane] = lane == s ? w : Wcur[lane];
         __syncwarp();
-        const int64_t sp = warp_simulate(c, Wt, endv, false, df, db);
+        const int64_t sp = warp_simulate(c, Wt, endv, optab, false, df, db, span_def);
         if (lane == 0 && sp == span_def) atomicMin(&wbest, w);
       }
       __syncthreads();
@@ -273,7 +321,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
     __syncthreads();
   }
   if (warp == 0) {
-    const int64_t sp = warp_simulate(c, Wcur, endv, true, df, db);
+    const int64_t sp = warp_simulate(c, Wcur, endv, optab, true, df, db);
     if (lane < p) c.W[lane] = Wcur[lane];
     if (lane == 0) {
       c.scal[1] = sp + c.T_rs;  // T_end = max_p(last op end_p + T_rs) (R3)
