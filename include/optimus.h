@@ -73,8 +73,8 @@ typedef struct {
   int32_t llm_layers;         /* multiple of PP * V                                      */
   int32_t n_mb;               /* N_mb, microbatches per LLM pipeline             */
   int32_t warmup_policy;      /* 0 = Megatron default warm-up, 1 = adjusted (§4.3) */
-  optimus_seq llm_fwd_layer;  /* one LLM layer forward, >= 1 compute kernel              */
-  optimus_seq llm_bwd_layer;  /* one LLM layer backward, >= 1 compute kernel             */
+  optimus_seq llm_fwd_layer;  /* one LLM layer forward, >= 1 compute, <= 256 kernels     */
+  optimus_seq llm_bwd_layer;  /* one LLM layer backward, >= 1 compute, <= 256 kernels    */
   int64_t dp_allgather_ns;    /* DP all-gather bubble before any LLM op          */
   int64_t dp_reducescatter_ns;/* DP reduce-scatter bubble after the last op      */
   int64_t pp_p2p_ns;          /* LLM stage-to-stage activation/gradient latency          */

@@ -117,6 +117,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
   int rc;
   if ((rc = check_seq(pb->llm_fwd_layer, "llm_fwd_layer", true, false))) return rc;
   if ((rc = check_seq(pb->llm_bwd_layer, "llm_bwd_layer", true, false))) return rc;
+  if (pb->llm_fwd_layer.len > 256 || pb->llm_bwd_layer.len > 256)
+    return fail(OPTIMUS_ERANGE, "LLM layer kernel lists longer than 256 kernels are not supported");
   if ((runs_of(pb->llm_fwd_layer, 1) > 0) != (runs_of(pb->llm_bwd_layer, 1) > 0))
     return fail(OPTIMUS_EINVAL, "llm_fwd_layer and llm_bwd_layer must both have TP comm kernels or neither");
   if (pb->n_branches < 1 || !pb->branch_layers || !pb->branch_params)

@@ -31,10 +31,13 @@ namespace {
 // compiles to LDS/STS, not to generic strong loads/stores)
 extern __shared__ __align__(16) unsigned char k0_dsm[];
 
+// sum of list `id`'s durations (called by a whole warp)
 __device__ int64_t list_sum(const Cfg& c, int id) {
-  int64_t s = 0;
-  for (int i = c.loff[id]; i < c.loff[id + 1]; ++i) s += c.lns[i];
-  return s;
+  const int lane = threadIdx.x & 31, off = c.loff[id], len = c.loff[id + 1] - off;
+  int64_t a = 0;
+  for (int i = lane; i < len; i += 32) a += c.lns[off + i];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
 }
 
 __device__ __forceinline__ int64_t warp_max64(int64_t v) {
@@ -52,7 +55,7 @@ constexpr int kSimWarps = 8;  // simulations per block
 
 __host__ __device__ __forceinline__ size_t k0_vtab_bytes(int n, int v) { return ((size_t)4 * n * v + 15) & ~size_t(15); }
 __host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int v, int n) {
-  return (size_t)kMaxP * 4 + (size_t)p * (2 * v * n + 1) * (8 + 4);  // W, endv, optab (odd per-stage strides)
+  return ((size_t)kMaxP * 4 + (size_t)p * (2 * v * n + 1) * (8 + 4) + 15) & ~size_t(15);  // W, endv, optab
 }
 __host__ __device__ __forceinline__ int k0_sim_warps(int p, int v, int n) {
   const size_t room = 200 * 1024 - k0_vtab_bytes(n, v);
@@ -116,13 +119,12 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
   const int s = lane;
   // op tables, built by the whole warp: self slot | dep slot << 15 (0x7FFF
   // none) | fwd << 30 | cross << 31 (padded slots)
-  for (int st = 0, pos = lane; st < p;) {
+  for (int idx = lane; idx < p * nops; idx += 32) {
+    const int st = idx / nops, pos = idx - st * nops;
     int self, dep, fwd, cross;
     op_slots(p, v, n, st, pos, W[st], vch, vmb, self, dep, fwd, cross);
     const int ps = self + self / S, pd = dep == kNone ? 0x7FFF : dep + dep / S;
     optab[(size_t)st * (nops + 1) + pos] = (uint32_t)ps | (uint32_t)pd << 15 | (uint32_t)fwd << 30 | (uint32_t)cross << 31;
-    pos += 32;
-    while (st < p && pos >= nops) { pos -= nops; ++st; }
   }
   const uint32_t* tab = optab + (size_t)s * (nops + 1);
   __syncwarp();
@@ -333,56 +335,118 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
 // ------------------------------------------------------------ intervals
 constexpr int kIvThreads = 512;
 
-struct ListInfo {
-  int off, len;
+constexpr int kLmax = 256;  // LLM layer kernel list capacity (validated at load)
+
+// One LLM layer kernel list in shared memory: per kernel its duration,
+// kind, start offset within a layer pass and the next kernel of the same
+// kind in the pass (-1 none).
+struct LTab {
+  int len, firstc, lastc, firstm;  // first compute, last compute, first comm index (-1 if none)
   int64_t sum;
-  int firstc, lastc, firstm;  // first compute, last compute, first comm index (-1 if none)
+  int64_t dur[kLmax], koff[kLmax];
+  int16_t nsame[kLmax];
+  uint8_t kind[kLmax];
 };
 
-__device__ ListInfo list_info(const Cfg& c, int id) {
-  ListInfo L;
-  L.off = c.loff[id];
-  L.len = c.loff[id + 1] - L.off;
-  L.sum = 0;
-  L.firstc = L.lastc = L.firstm = -1;
-  for (int i = 0; i < L.len; ++i) {
-    L.sum += c.lns[L.off + i];
-    if (c.lkind[L.off + i] == 0) {
-      if (L.firstc < 0) L.firstc = i;
-      L.lastc = i;
-    } else if (L.firstm < 0) {
-      L.firstm = i;
-    }
+// list `id` into T (one warp: parallel loads, then lane 0 scans smem)
+__device__ void load_ltab(const Cfg& c, int id, LTab& T) {
+  const int lane = threadIdx.x & 31, off = c.loff[id], len = c.loff[id + 1] - off;
+  for (int i = lane; i < len; i += 32) {
+    T.dur[i] = c.lns[off + i];
+    T.kind[i] = (uint8_t)(c.lkind[off + i] != 0);
   }
-  return L;
+  __syncwarp();
+  if (lane == 0) {
+    T.len = len;
+    T.firstc = T.lastc = T.firstm = -1;
+    int64_t a = 0;
+    int lastk[2] = {-1, -1};
+    for (int i = 0; i < len; ++i) {
+      T.koff[i] = a;
+      a += T.dur[i];
+      const int k = T.kind[i];
+      if (k == 0) {
+        if (T.firstc < 0) T.firstc = i;
+        T.lastc = i;
+      } else if (T.firstm < 0) {
+        T.firstm = i;
+      }
+      if (lastk[k] >= 0) T.nsame[lastk[k]] = (int16_t)i;
+      lastk[k] = i;
+      T.nsame[i] = -1;
+    }
+    T.sum = a;
+  }
+  __syncwarp();
 }
 
+// The kernels of stage s in time order: kernel kk is kernel i of layer pass
+// rep of op q.  Its gap to the next kernel of the same kind (R6): after a
+// compute kernel the compute-free interval (end, next compute start), after
+// a comm kernel the comm-free piece clipped to [w, z].  Returns 1 / 2 for a
+// compute / comm interval (lo, hi), 0 for none.
+__device__ __forceinline__ int gap_after(const LTab& Lf, const LTab& Lb, const int64_t* ost, const uint8_t* opfwd,
+                                         int nops, int lc, int q, int r, int64_t w, int64_t z, int64_t& lo,
+                                         int64_t& hi) {
+  const LTab& L = opfwd[q] ? Lf : Lb;
+  const int rep = r / L.len, i = r - rep * L.len;
+  const int kind = L.kind[i];
+  const int64_t base = ost[q] + (int64_t)rep * L.sum;
+  const int64_t en = base + L.koff[i] + L.dur[i];
+  int64_t nxt = kInf;
+  const int j = L.nsame[i];
+  if (j >= 0) {
+    nxt = base + L.koff[j];
+  } else if (rep < lc - 1) {
+    const int f = kind == 0 ? L.firstc : L.firstm;
+    nxt = base + L.sum + L.koff[f];
+  } else if (q < nops - 1) {
+    const LTab& L2 = opfwd[q + 1] ? Lf : Lb;
+    const int f = kind == 0 ? L2.firstc : L2.firstm;
+    if (f >= 0) nxt = ost[q + 1] + L2.koff[f];
+  }
+  if (kind == 0) {
+    if (nxt != kInf && nxt > en) { lo = en; hi = nxt; return 1; }  // compute-free gap
+  } else {
+    const int64_t a = max(en, w), b = min(nxt, z);
+    if (b > a) { lo = a; hi = b; return 2; }  // comm-free piece inside [w, z]
+  }
+  return 0;
+}
+
+// k0_intervals, one block per LLM stage: every thread takes a contiguous
+// run of the stage's kernels, counts its intervals, one block scan gives
+// the output offsets, a second pass writes them (time order is kernel order).
 __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
-  using Scan = cub::BlockScan<int, kIvThreads>;
+  using Scan = cub::BlockScan<unsigned long long, kIvThreads>;
   __shared__ typename Scan::TempStorage tmp;
+  __shared__ LTab Lf, Lb;
   __shared__ int run_c, run_m;
-  extern __shared__ int opoff[];  // [nops + 1] kernel offset of each op
+  extern __shared__ int opoff[];  // [nops + 1] kernel offset of each op, then [nops] op is forward
   if (c.scal[2] == 0) return;     // template failed (deadlock): nothing to emit
-  const int s = blockIdx.x;
+  const int s = blockIdx.x, warp = threadIdx.x >> 5;
   const int p = c.p, v = c.v, n = c.n, nops = c.nops, lc = c.lc;
   const int Ws = c.W[s];
-  const ListInfo Lf = list_info(c, 0), Lb = list_info(c, 1);
-  const int64_t* ost = c.opstart + (int64_t)s * nops;
+  uint8_t* opfwd = reinterpret_cast<uint8_t*>(opoff + nops + 1);
+  if (warp == 0) load_ltab(c, 0, Lf);
+  if (warp == 1) load_ltab(c, 1, Lb);
+  for (int q = threadIdx.x; q < nops; q += blockDim.x) opfwd[q] = (uint8_t)op_at(p, v, n, Ws, q).fwd;
+  __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int q = 0; q < nops; ++q) {
       opoff[q] = acc;
-      acc += lc * (op_at(p, v, n, Ws, q).fwd ? Lf.len : Lb.len);
+      acc += lc * (opfwd[q] ? Lf.len : Lb.len);
     }
     opoff[nops] = acc;
     run_c = run_m = 0;
   }
   __syncthreads();
   const int K = opoff[nops];
+  const int64_t* ost = c.opstart + (int64_t)s * nops;
   // first op is always a forward, last always a backward
-  const int64_t w = ost[0] + [&] { int64_t a = 0; for (int i = 0; i < Lf.firstc; ++i) a += c.lns[Lf.off + i]; return a; }();
-  const int64_t z = ost[nops - 1] + (int64_t)(lc - 1) * Lb.sum +
-                    [&] { int64_t a = 0; for (int i = 0; i <= Lb.lastc; ++i) a += c.lns[Lb.off + i]; return a; }();
+  const int64_t w = ost[0] + Lf.koff[Lf.firstc];
+  const int64_t z = ost[nops - 1] + (int64_t)(lc - 1) * Lb.sum + Lb.koff[Lb.lastc] + Lb.dur[Lb.lastc];
   if (threadIdx.x == 0) { c.w[s] = w; c.z[s] = z; }
   int64_t* clo = c.comp_lo + (int64_t)s * c.icapc;
   int64_t* chi = c.comp_hi + (int64_t)s * c.icapc;
@@ -391,74 +455,41 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   // head comm-free piece [w, first comm start) (R6), emitted first
   if (threadIdx.x == 0) {
     int64_t first_comm = kInf;
-    if (Lf.firstm >= 0) {
-      int64_t a = 0;
-      for (int i = 0; i < Lf.firstm; ++i) a += c.lns[Lf.off + i];
-      first_comm = ost[0] + a;
-    } else if (Lb.firstm >= 0) {
-      first_comm = -1;  // unreachable: validated (both lists have comm or neither)
-    }
-    int64_t hi = min(first_comm, z);
+    if (Lf.firstm >= 0) first_comm = ost[0] + Lf.koff[Lf.firstm];
+    const int64_t hi = min(first_comm, z);  // (both lists have comm or neither: validated)
     if (hi > w) { mlo[0] = w; mhi[0] = hi; run_m = 1; }
   }
   __syncthreads();
-  // offset of kernel i of list L within a layer pass
-  auto koff = [&](const ListInfo& L, int i) {
-    int64_t a = 0;
-    for (int q = 0; q < i; ++q) a += c.lns[L.off + q];
-    return a;
-  };
-  for (int base = 0; base < K; base += kIvThreads) {
-    const int kk = base + threadIdx.x;
-    int ec = 0, em = 0;
-    int64_t clo_v = 0, chi_v = 0, mlo_v = 0, mhi_v = 0;
-    if (kk < K) {
-      // locate the op (binary search on opoff)
-      int lo = 0, hi = nops - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (opoff[mid] <= kk) lo = mid; else hi = mid - 1;
-      }
-      const int q = lo;
-      const bool fwd = op_at(p, v, n, Ws, q).fwd;
-      const ListInfo& L = fwd ? Lf : Lb;
-      const int r = kk - opoff[q], rep = r / L.len, i = r % L.len;
-      const int kind = c.lkind[L.off + i];
-      const int64_t st = ost[q] + (int64_t)rep * L.sum + koff(L, i);
-      const int64_t en = st + c.lns[L.off + i];
-      // start of the next kernel of the same kind
-      int64_t nxt = kInf;
-      int j = -1;
-      for (int t = i + 1; t < L.len; ++t)
-        if (c.lkind[L.off + t] == kind) { j = t; break; }
-      if (j >= 0) {
-        nxt = ost[q] + (int64_t)rep * L.sum + koff(L, j);
-      } else if (rep < lc - 1) {
-        int f = kind == 0 ? L.firstc : L.firstm;
-        nxt = ost[q] + (int64_t)(rep + 1) * L.sum + koff(L, f);
-      } else if (q < nops - 1) {
-        const ListInfo& L2 = op_at(p, v, n, Ws, q + 1).fwd ? Lf : Lb;
-        int f = kind == 0 ? L2.firstc : L2.firstm;
-        if (f >= 0) nxt = ost[q + 1] + koff(L2, f);
-      }
-      if (kind == 0) {
-        if (nxt != kInf && nxt > en) { ec = 1; clo_v = en; chi_v = nxt; }  // compute-free gap
-      } else {
-        int64_t a = max(en, w), b = min(nxt, z);
-        if (b > a) { em = 1; mlo_v = a; mhi_v = b; }  // comm-free piece inside [w, z]
-      }
+  const int C = (K + kIvThreads - 1) / kIvThreads, k0 = min(K, (int)threadIdx.x * C), k1 = min(K, k0 + C);
+  int q0 = 0;
+  {  // op of kernel k0
+    int lo = 0, hi = nops - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (opoff[mid] <= k0) lo = mid; else hi = mid - 1;
     }
-    int pc, pm, tc, tm;
-    Scan(tmp).ExclusiveSum(ec, pc, tc);
-    __syncthreads();
-    Scan(tmp).ExclusiveSum(em, pm, tm);
-    const int bc = run_c, bm = run_m;
-    if (ec) { clo[bc + pc] = clo_v; chi[bc + pc] = chi_v; }
-    if (em) { mlo[bm + pm] = mlo_v; mhi[bm + pm] = mhi_v; }
-    __syncthreads();
-    if (threadIdx.x == 0) { run_c = bc + tc; run_m = bm + tm; }
-    __syncthreads();
+    q0 = lo;
   }
+  unsigned long long cnt = 0;  // compute | comm << 32
+  for (int kk = k0, q = q0; kk < k1; ++kk) {
+    while (kk >= opoff[q + 1]) ++q;
+    int64_t lo, hi;
+    const int g = gap_after(Lf, Lb, ost, opfwd, nops, lc, q, kk - opoff[q], w, z, lo, hi);
+    cnt += g == 1 ? 1ull : g == 2 ? (1ull << 32) : 0ull;
+  }
+  unsigned long long off, tot;
+  Scan(tmp).ExclusiveSum(cnt, off, tot);
+  int oc = run_c + (int)(off & 0xffffffffu), om = run_m + (int)(off >> 32);
+  for (int kk = k0, q = q0; kk < k1; ++kk) {
+    while (kk >= opoff[q + 1]) ++q;
+    int64_t lo, hi;
+    const int g = gap_after(Lf, Lb, ost, opfwd, nops, lc, q, kk - opoff[q], w, z, lo, hi);
+    if (g == 1) { clo[oc] = lo; chi[oc] = hi; ++oc; }
+    if (g == 2) { mlo[om] = lo; mhi[om] = hi; ++om; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { run_c += (int)(tot & 0xffffffffu); run_m += (int)(tot >> 32); }
+  __syncthreads();
   if (threadIdx.x == 0) { c.ncomp[s] = run_c; c.ncomm[s] = run_m; }
   __syncthreads();
   // per 32-interval block, the largest base capacity hi - lo, in time order
@@ -496,7 +527,7 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
   const int nsim = 1 + c.k0_trials;
   k0_wave<<<(nsim + wpb - 1) / wpb, 32 * kSimWarps, smem, st>>>(c, nsim, wpb);
   k0_final<<<1, 32 * kSimWarps, smem, st>>>(c, wpb);
-  k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int), st>>>(c);
+  k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int) + c.nops, st>>>(c);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
