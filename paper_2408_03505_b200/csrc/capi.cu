@@ -54,14 +54,14 @@ struct Prep {
   std::vector<HostPlan> plans;
   uint64_t total = 0;
   int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0, n_flags = 0;
-  std::vector<int32_t> units;
+  std::vector<int32_t> units, k2order;
   int kmax_all = 0;
   int nk_max = 0;
   int k0_trials = 0;
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_partials, o_counter, o_stats, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, total_bytes;
   int grid;
 };
 
@@ -219,6 +219,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
       if (d.count) {
         d.kmax = X.n - d.m + 1;  // most microbatches one pipeline can hold
         const int64_t np1 = X.n + 1;
+        toff = (toff + 15) & ~int64_t(15);  // own 128-byte lines: K2 reads a plan's tables while K1 writes others
         d.preF = toff; toff += (int64_t)P * np1;
         d.preB = toff; toff += (int64_t)P * np1;
         d.devF = toff; toff += (int64_t)d.rp * np1;
@@ -240,17 +241,26 @@ int prepare(const optimus_problem* pb, Prep& X) {
     }
   }
   X.total = first;
-  // K1 unit list: forward units, then backward units ordered by kf (the
-  // ones that can start at once first)
+  if (X.plans.size() > (size_t)kMaxE) return fail(OPTIMUS_ERANGE, "%zu encoder plans (> %d supported)", X.plans.size(), kMaxE);
+  // K1 work list: forward units, the plan tables, then backward units
+  // ordered by kf (the ones that can start at once first)
   for (size_t e = 0; e < X.plans.size(); ++e)
     if (X.plans[e].d.count)
       for (int a = 0; a < X.plans[e].d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8));
+  for (size_t e = 0; e < X.plans.size(); ++e)
+    if (X.plans[e].d.count) X.units.push_back((int32_t)(2u << 30 | e << 16));
   for (int kf = 0; kf <= X.kmax_all; ++kf)
     for (size_t e = 0; e < X.plans.size(); ++e) {
       const PlanDesc& d = X.plans[e].d;
       if (d.count && kf <= d.kmax)
-        for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8 | kf));
+        for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(1u << 30 | e << 16 | a << 8 | kf));
     }
+  // K2 takes plans with more stages first: their chains are shorter, so K1
+  // finishes them earlier
+  for (size_t e = 0; e < X.plans.size(); ++e)
+    if (X.plans[e].d.count) X.k2order.push_back((int32_t)e);
+  std::stable_sort(X.k2order.begin(), X.k2order.end(),
+                   [&](int32_t x, int32_t y) { return X.plans[x].d.P > X.plans[y].d.P; });
   X.n_flags = std::max<int64_t>(X.n_flags, 1);
   X.n_tables = std::max<int64_t>(toff, 1);
   X.n_slots = std::max<int64_t>(slot, 1);
@@ -265,6 +275,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_binom = take(X.binom.size() * 8);
   X.o_plans = take(X.plans.size() * sizeof(PlanDesc));
   X.o_units = take(std::max<size_t>(X.units.size(), 1) * 4);
+  X.o_k2order = take(std::max<size_t>(X.k2order.size(), 1) * 4);
   X.inputs_bytes = o;
   X.o_W = take(X.p * 4);
   X.o_Wdef = take(X.p * 4);
@@ -287,6 +298,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_k1flags = take((size_t)X.n_flags * 4);
+  X.o_sync = take(16 + (size_t)kMaxE * (4 + 8));  // k1next, pdone[E], pclaim[E]
   X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
@@ -356,6 +368,12 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.snap_own = (int8_t*)(ws + X.o_snap_own);
   c.k1flags = (int32_t*)(ws + X.o_k1flags);
   c.k1units = (const int32_t*)(ws + X.o_units);
+  c.k1_total = (int32_t)X.units.size();
+  c.k1next = (int32_t*)(ws + X.o_sync);
+  c.pdone = (int32_t*)(ws + X.o_sync + 16);
+  c.pclaim = (unsigned long long*)(ws + X.o_sync + 16 + (size_t)kMaxE * 4);
+  c.k2order = (const int32_t*)(ws + X.o_k2order);
+  c.n_k2order = (int32_t)X.k2order.size();
   return c;
 }
 
@@ -363,7 +381,7 @@ int build(optimus_ctx* c, cudaStream_t st) {
   c->build_launches = 0;
   if (c->timing) CK(cudaEventRecord(c->ev[0], st));
   CK(launch_template(c->cfg, st, &c->build_launches));
-  CK(launch_chain_tables(c->cfg, c->X.fwd_units, c->X.bwd_units, st, &c->build_launches));
+  CK(launch_chain_tables(c->cfg, st, &c->build_launches));
   if (c->timing) CK(cudaEventRecord(c->ev[1], st));
   return OPTIMUS_OK;
 }
@@ -415,6 +433,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   }
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
+  c->cfg.sms = sms;
   cudaStream_t st = (cudaStream_t)cuda_stream;
   // one host->device copy of the packed inputs (the problem's cost tables)
   std::vector<char> h(X.inputs_bytes, 0);
@@ -425,10 +444,12 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   memcpy(h.data() + X.o_binom, X.binom.data(), X.binom.size() * 8);
   for (size_t i = 0; i < X.plans.size(); ++i) memcpy(h.data() + X.o_plans + i * sizeof(PlanDesc), &X.plans[i].d, sizeof(PlanDesc));
   memcpy(h.data() + X.o_units, X.units.data(), X.units.size() * 4);
+  memcpy(h.data() + X.o_k2order, X.k2order.data(), X.k2order.size() * 4);
   e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 16 + (size_t)kMaxE * 12, st);  // K1/K2 counters
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);
@@ -478,6 +499,8 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.mode = c->mode;
   a.grid = c->mode == 1 ? c->grid_thread : c->grid;
   a.stats = (unsigned long long*)(c->ws + c->X.o_stats);
+  a.pclaim = c->cfg.pclaim;
+  a.nplans = c->cfg.E;
   a.ev0 = c->timing ? c->ev[2] : nullptr;
   a.ev1 = c->timing ? c->ev[3] : nullptr;
   c->eval_launches = 0;

@@ -159,7 +159,7 @@ struct Win {
   int base, cur;
   bool dirty;
   int64_t lo, hi, nlo, nhi;
-  int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative); chi = -inf when cur < 0
+  int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative); both -inf when cur < 0
 };
 
 template <bool M>
@@ -178,6 +178,7 @@ template <bool M>
 __device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
   w.base = b;
   w.cur = -1;
+  w.clo = kNegInf;  // no current interval: the fast path's max-plus terms must stay inert
   w.chi = kNegInf;
   w.dirty = false;
   win_fetch(V, b, w.lo, w.hi);
@@ -187,6 +188,7 @@ __device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
 __device__ __forceinline__ void win_sync_cur(Win& w) {
   if (w.cur >= 0 && (threadIdx.x & 31) == w.cur - w.base) w.lo = w.clo;
   w.cur = -1;
+  w.clo = kNegInf;
   w.chi = kNegInf;
 }
 
@@ -550,8 +552,11 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
     const int64_t T_end = c.scal[1];
     const int q = a * P + s;
     const int64_t ws = M ? T_end - c.z[q] : c.w[q];
+    // every decision on a value another warp may change is taken from lane
+    // 0's read (broadcast), so that the warp never splits before its
+    // full-mask collectives
     for (int k = 0; k < pd.kmax; ++k) {
-      if (k >= *stop) break;
+      if (k >= __shfl_sync(FULL, *stop, 0)) break;
       int64_t ready = ws;
       if (s > 0) {  // wait for chain k of the upstream stage
         int st;
@@ -559,8 +564,10 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
 #ifdef K1_STATS
         const long long tw0 = clock64();
 #endif
-        while ((st = status[(s - 1) * L.KM + k]) == 0) {
-          if (k >= *stop) { quit = true; break; }
+        for (;;) {
+          st = __shfl_sync(FULL, status[(s - 1) * L.KM + k], 0);
+          if (st != 0) break;
+          if (k >= __shfl_sync(FULL, *stop, 0)) { quit = true; break; }
           __nanosleep(20);
         }
 #ifdef K1_STATS
@@ -601,7 +608,7 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   }
 #ifdef K1_STATS
   K1ST(6, clock64() - tk0);
-  if (active && lane == 0 && k1st[s][6] > 300000)
+  if (active && lane == 0 && k1st[s][6] > 200000)
     printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d prolog=%llu setup=%llu slow=%llu x=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
            (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
 #endif
@@ -619,23 +626,60 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   }
 }
 
-// block size 32 * p: register budgets per p range (MAXT threads, MINB blocks per SM)
+// Persistent: every block takes work items in list order (forward units
+// first, so a backward unit only ever waits on items already taken by
+// running blocks) until the list is exhausted, and counts each finished
+// item in its plan's pdone (release).  The launch lets the dependent K2
+// start at once (programmatic dependent launch): K2 takes a plan's
+// candidates once pdone says its tables are complete.
+// Block size 32 * p: register budgets per p range (MAXT threads, MINB blocks per SM).
 template <int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, int64_t fwd_units, int64_t units, K1Launch L) {
-  if ((int64_t)blockIdx.x >= units) {  // the per-plan tables ride along (only K2 reads them)
-    plan_tables(c, (int)(blockIdx.x - units));
-    return;
+__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ int item;
+  for (;;) {
+    if (threadIdx.x == 0) item = atomicAdd(c.k1next, 1);
+    __syncthreads();
+    const int it = item;
+    __syncthreads();
+    if (it >= c.k1_total) break;
+    const uint32_t u = (uint32_t)c.k1units[it];
+    const int type = u >> 30, e = (u >> 16) & 0x3FFF, a = (u >> 8) & 255, kf = u & 255;
+    if (type == 2) plan_tables(c, e);
+    else if (type == 0) k1_unit<false>(c, L, e, a, 0);
+    else k1_unit<true>(c, L, e, a, kf);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&c.pdone[e], 1);
+    }
   }
-  const int32_t u = c.k1units[blockIdx.x];
-  if ((int64_t)blockIdx.x < fwd_units) k1_unit<false>(c, L, u >> 16, (u >> 8) & 255, 0);
-  else k1_unit<true>(c, L, u >> 16, (u >> 8) & 255, u & 255);
+}
+
+template <int MAXT, int MINB>
+static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  static int per = 0, per_nt = -1;
+  static size_t per_smem = 0;
+  const int nt = 32 * c.p;
+  if (!attr) {  // opt in to large dynamic shared memory once per process
+    cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  if (nt != per_nt || smem != per_smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, nt, smem);
+    per_nt = nt;
+    per_smem = smem;
+  }
+  const int grid = std::max(1, std::min(c.k1_total, std::max(1, per) * c.sms));
+  k1_chains<MAXT, MINB><<<grid, nt, smem, st>>>(c, L);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 
-cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st,
-                                int* launches) {
+cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
   K1Launch L;
   L.NK = c.nk_max;
   L.Pmax = c.p;
@@ -643,23 +687,10 @@ cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_uni
   L.KM = std::max(1, c.kmax_all);
   const size_t smem = k1_smem_bytes(L);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
-  static bool attrs = false;  // opt in to large dynamic shared memory once per process
-  if (!attrs) {
-    cudaFuncSetAttribute(k1_chains<384, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k1_chains<512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k1_chains<1024, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attrs = true;
-  }
-  // one block per unit (forward units first: their blocks are dispatched
-  // before any backward block that waits on them), one warp per stage of
-  // the widest plan
-  const int64_t units = fwd_units + bwd_units;
-  const unsigned nb = (unsigned)(units + c.E), nt = 32 * c.p;
-  if (c.p <= 12) k1_chains<384, 2><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
-  else if (c.p <= 16) k1_chains<512, 1><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
-  else k1_chains<1024, 1><<<nb, nt, smem, st>>>(c, fwd_units, units, L);
   if (launches) *launches += 1;
-  return cudaGetLastError();
+  if (c.p <= 12) return launch_k1<384, 2>(c, L, smem, st);
+  if (c.p <= 16) return launch_k1<512, 1>(c, L, smem, st);
+  return launch_k1<1024, 1>(c, L, smem, st);
 }
 
 }  // namespace optimus

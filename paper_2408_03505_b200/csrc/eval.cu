@@ -470,6 +470,7 @@ __global__ void k3_reduce(EvalArgs A) {
     A.best2[1] = l_sm[0] == INT64_MAX ? -1 : (int64_t)g_sm[0];
     *A.counter = 0;  // ready for the next eval on this stream
   }
+  for (int e = threadIdx.x; e < A.nplans; e += blockDim.x) A.pclaim[e] = 0;
 }
 
 }  // namespace

@@ -502,6 +502,18 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   return T_end + Df + Delta;  // R16
 }
 
+// positions of this rank (block-cyclic over [begin, end)) below global index x >= begin
+__device__ __forceinline__ uint64_t rank_pos(const EvalArgs& A, uint64_t x) {
+  const uint64_t r = x - A.begin, fb = r / A.block, rem = r - fb * A.block, k = fb % A.world;
+  return (fb / A.world) * A.block + (k > A.rank ? A.block : 0) + (k == A.rank ? rem : 0);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, uint64_t& bg) {
   if (lat < bl || (lat == bl && g < bg)) { bl = lat; bg = g; }
 }
@@ -512,12 +524,23 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
   __shared__ int64_t G[kMaxN], D[kMaxN];
   __shared__ long long bl_sm[kTThreads / 32];
   __shared__ unsigned long long bg_sm[kTThreads / 32];
+  __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
+  __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     G[i] = c.F[i] - c.L;          // EF_i + L <= F_i
     D[i] = T_end - c.B[i] - c.L;  // EB_i >= B_i + L (mirrored)
   }
+  if (!EXPLICIT)
+    for (int e = threadIdx.x; e < c.E; e += blockDim.x) {  // this rank's positions of plan e
+      const PlanDesc& d = c.plans[e];
+      const uint64_t x0 = max(A.begin, d.first), x1 = min(A.end, d.first + d.count);
+      const uint64_t lo = x0 < x1 ? rank_pos(A, x0) : 0, hi = x0 < x1 ? rank_pos(A, x1) : 0;
+      plo[e] = lo;
+      pn[e] = hi - lo;
+      pstate[e] = 0;
+    }
   __syncthreads();
   TS s = ts_at(tsm + (size_t)threadIdx.x * kTStride);
   TPlan p;
@@ -525,15 +548,14 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
   int64_t bl = INT64_MAX;
   uint64_t bg = UINT64_MAX;
-  const uint64_t per_warp = 32ull * (EXPLICIT ? 1 : kTRun);
-  const uint64_t nchunks = (A.count + per_warp - 1) / per_warp;
-  for (;;) {
-    unsigned long long ch = 0;
-    if (lane == 0) ch = atomicAdd(A.counter, 1ull);
-    ch = __shfl_sync(0xffffffffu, ch, 0);
-    if (ch >= nchunks) break;
-    if (EXPLICIT) {
-      const uint64_t i = ch * per_warp + lane;
+  if (EXPLICIT) {
+    const uint64_t nchunks = (A.count + 31) / 32;
+    for (;;) {
+      unsigned long long ch = 0;
+      if (lane == 0) ch = atomicAdd(A.counter, 1ull);
+      ch = __shfl_sync(0xffffffffu, ch, 0);
+      if (ch >= nchunks) break;
+      const uint64_t i = ch * 32 + lane;
       if (i < A.count) {
         const uint64_t g = A.index[i];
         const int e = tfind_plan(c, g);
@@ -545,28 +567,55 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
           tbetter(lat, g, bl, bg);
         }
       }
-    } else {
-      // this rank's positions [pos, pos + kTRun) -> global indices (block-cyclic over ranks)
-      const uint64_t pos = ch * per_warp + (uint64_t)lane * kTRun;
-      const uint64_t rb = pos / A.block, offb = pos % A.block;
-      uint64_t g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + offb;
-      const uint64_t gend = min(g + kTRun, A.end);
-      if (g < gend) {
-        int e = tfind_plan(c, g);
-        if (e != p.e) tplan(c, e, p);
-        tunrank(c, n, p.m, g - p.first, s);
+    }
+  } else {
+    // Plan by plan in k2order, each plan once K1 has completed it (this
+    // launch may overlap K1).  This rank's positions: block-cyclic over
+    // [begin, end); plan e's are [plo[e], plo[e] + pn[e]).  A warp claims
+    // 32 * kTRun consecutive positions of one plan at a time.
+    constexpr uint64_t per_warp = 32ull * kTRun;
+    for (;;) {
+      int e = -1;
+      unsigned long long chunk = 0;
+      if (lane == 0) {
+        volatile int* pst = pstate;  // shared by the block's warps; only ever raised
         for (;;) {
-          const int64_t lat = teval(c, p, G, D, T_end, s, st);
-          if (A.lat_out) A.lat_out[g - A.begin] = lat;
-          tbetter(lat, g, bl, bg);
-          if (++g >= gend) break;
-          if (g >= p.first + p.count) {
-            tplan(c, tfind_plan(c, g), p);
-            tunrank(c, n, p.m, 0, s);
-          } else {
-            tnext(p.m, s);
+          bool pending = false;
+          for (int k = 0; k < c.n_k2order; ++k) {
+            const int e2 = c.k2order[k];
+            const int ps = pst[e2];
+            if (ps == 2 || pn[e2] == 0) continue;
+            if (ps == 0) {
+              if (ld_acquire(&c.pdone[e2]) < plan_items(c.plans[e2])) { pending = true; continue; }
+              pst[e2] = 1;
+            }
+            const unsigned long long cl = atomicAdd(&c.pclaim[e2], 1ull);
+            if (cl < (pn[e2] + per_warp - 1) / per_warp) { e = e2; chunk = cl; break; }
+            pst[e2] = 2;
           }
+          if (e >= 0 || !pending) break;
+          __nanosleep(500);
         }
+      }
+      e = __shfl_sync(0xffffffffu, e, 0);
+      chunk = __shfl_sync(0xffffffffu, chunk, 0);
+      __syncwarp();  // the lanes' table reads follow lane 0's acquire
+      if (e < 0) break;
+      if (e != p.e) tplan(c, e, p);
+      const uint64_t p0 = plo[e] + chunk * per_warp + (uint64_t)lane * kTRun, pend = plo[e] + pn[e];
+      uint64_t g = 0;
+      for (uint64_t q = p0; q < min(p0 + kTRun, pend); ++q) {
+        if (q == p0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
+          const uint64_t rb = q / A.block;
+          g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
+          tunrank(c, n, p.m, g - p.first, s);
+        } else {
+          ++g;
+          tnext(p.m, s);
+        }
+        const int64_t lat = teval(c, p, G, D, T_end, s, st);
+        if (A.lat_out) A.lat_out[g - A.begin] = lat;
+        tbetter(lat, g, bl, bg);
       }
     }
   }
@@ -605,9 +654,23 @@ int eval_thread_grid(int sms) {
 
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
   const size_t smem = (size_t)kTThreads * kTStride;
-  if (a.index) k2_eval_thread<true><<<a.grid, kTThreads, smem, st>>>(c, a);
-  else k2_eval_thread<false><<<a.grid, kTThreads, smem, st>>>(c, a);
-  return cudaGetLastError();
+  if (a.index) {
+    k2_eval_thread<true><<<a.grid, kTThreads, smem, st>>>(c, a);
+    return cudaGetLastError();
+  }
+  // programmatic dependent launch: may start while K1 (which triggers at its
+  // start) still runs; plan readiness is K1's pdone counters
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.grid);
+  cfg.blockDim = dim3(kTThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false>, c, a);
 }
 
 }  // namespace optimus

@@ -15,6 +15,8 @@ constexpr int kMaxN = 32;                 // microbatches per LLM pipeline in K2
 // 2 + 2*(branch*ntp + ti) = encoder layer fwd at TP option ti, +1 = bwd.
 __host__ __device__ inline int enc_list_id(int b, int ti, int ntp, int bwd) { return 2 + 2 * (b * ntp + ti) + bwd; }
 
+constexpr int kMaxE = 128;  // plans (validated at load)
+
 // Per-plan descriptor (host-built at load, copied to the workspace).
 struct PlanDesc {
   int32_t P, T, ti, m, rp, rt, kmax, pad;
@@ -25,6 +27,10 @@ struct PlanDesc {
   int64_t slot_base;  // first K1 scratch slot of this plan
   int64_t flag_base;  // first K1 flag of this plan: per row [kmax + 1] (0: forward done, v: stages that published version v)
 };
+
+// K1 work items of a plan (forward rows, backward (row, kf), its tables):
+// K2 evaluates the plan's candidates once pdone reaches this
+__host__ __device__ inline int plan_items(const PlanDesc& d) { return d.rp + d.rp * (d.kmax + 1) + 1; }
 
 // Everything a kernel needs: scalars + device pointers into the workspace.
 struct Cfg {
@@ -67,7 +73,14 @@ struct Cfg {
   int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
   int8_t* snap_own;       // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
   int32_t* k1flags;       // K1 forward -> backward progress flags (PlanDesc::flag_base); zeroed by k0_final
-  const int32_t* k1units; // K1 units: forward (plan, row) first, then backward (plan, row, kf) by kf; e<<16|a<<8|kf
+  const int32_t* k1units; // K1 work list: type << 30 | e << 16 | a << 8 | kf (type 0 forward, 1 backward, 2 plan tables)
+  int32_t k1_total;       // K1 work items
+  int32_t sms;            // SM count of the device (persistent grids)
+  int32_t* k1next;        // K1 work counter (persistent blocks); zeroed by k0_final
+  int32_t* pdone;         // [E] K1 work items of each plan completed (release); zeroed by k0_final
+  unsigned long long* pclaim;  // [E] K2 chunks of each plan claimed; zeroed by K3
+  const int32_t* k2order; // plans with candidates, in the order K2 takes them (short chains first)
+  int32_t n_k2order;
   const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
 };
 
@@ -101,7 +114,7 @@ __host__ __device__ inline OpRef op_at(int p, int v, int n, int W, int pos) {
 // Host launchers (defined in the .cu files).
 namespace optimus {
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
-cudaError_t launch_chain_tables(const Cfg& c, int64_t fwd_units, int64_t bwd_units, cudaStream_t st, int* launches);
+cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches);
 struct EvalArgs {
   uint64_t begin, end;       // global index range (eval_candidates)
   uint32_t rank, world, block;
@@ -115,6 +128,8 @@ struct EvalArgs {
   int grid;
   int mode;                   // 0: one candidate per warp (eval.cu), 1: one per thread (eval_thread.cu)
   cudaEvent_t ev0, ev1;       // optional: recorded around K2 for per-kernel timing
+  unsigned long long* pclaim;  // [nplans] K2 per-plan chunk counters, reset by K3
+  int nplans;
   unsigned long long* stats;  // [6] cumulative: candidates, algorithmic ops, fwd iters, fwd attempts, bwd iters, bwd attempts
 };
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);

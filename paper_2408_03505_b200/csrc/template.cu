@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
     c.scal[3] = 0;  // reset for the next build's wave
   }
   for (int i = threadIdx.x; i < c.nflags; i += blockDim.x) c.k1flags[i] = 0;  // K1 progress flags
+  for (int i = threadIdx.x; i < c.E; i += blockDim.x) c.pdone[i] = 0;        // K1 -> K2 plan completion
+  if (threadIdx.x == 0) *c.k1next = 0;                                         // K1 work counter
   if (span_def < 0) {  // default schedule deadlocks: template fails
     if (threadIdx.x == 0) c.scal[2] = 0;
     return;

@@ -225,3 +225,30 @@ def test_degenerate_problems(dev, oracle_mod, mode):
         torch.cuda.synchronize()
         ref = oracle_mod.Oracle(prob).eval(np.arange(total, dtype=np.uint64))
         assert np.array_equal(lat.cpu().numpy(), ref), prob["name"]
+
+
+def test_rebuild_determinism(dev, oracle_mod):
+    """Full-size chain tables are identical across rebuilds, whatever ran on
+    the GPU in between (another context's K2 leaves different registers and
+    shared memory behind), and match the oracle's row chains."""
+    torch = dev
+    prob = config_problem(4)
+    ctx, other = _load(prob), _load(prob)
+    total, n_plans = ctx.num_candidates()
+
+    def tables():
+        torch.cuda.synchronize()
+        return [ctx.debug_plan_tables(e) for e in range(n_plans)]
+
+    base = tables()
+    o = oracle_mod.Oracle(prob)
+    for e, t in enumerate(base):
+        if t is not None:
+            assert t["INB_F"][0] == o.row_chains(e, 0, -1, t["kmax"]), e
+    idx = torch.from_numpy(np.array(sample_indices(7, 2048, total), dtype=np.int64)).cuda()
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    for it in range(4):
+        (other if it % 2 else ctx).eval_indices(idx, b2)
+        other.eval_candidates(0, min(total, 100000), b2)
+        ctx.rebuild()
+        assert tables() == base, it
