@@ -213,6 +213,12 @@ def main():
     if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
         os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the single JSON line
     dist = None
+    # stdout carries exactly one JSON line: anything native code prints while
+    # NCCL comes up (communicator creation is lazy: until after the warm-up)
+    # goes to stderr
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -243,6 +249,9 @@ def main():
         flush.zero_()
         step()
     torch.cuda.synchronize()
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
+    os.close(saved_stdout)
     stats0 = ctx.eval_stats()
 
     sampler = ClockSampler(local) if (not args.profile) else None
