@@ -242,25 +242,24 @@ int prepare(const optimus_problem* pb, Prep& X) {
   }
   X.total = first;
   if (X.plans.size() > (size_t)kMaxE) return fail(OPTIMUS_ERANGE, "%zu encoder plans (> %d supported)", X.plans.size(), kMaxE);
-  // K1 work list: forward units, the plan tables, then backward units
-  // ordered by kf (the ones that can start at once first)
-  for (size_t e = 0; e < X.plans.size(); ++e)
-    if (X.plans[e].d.count)
-      for (int a = 0; a < X.plans[e].d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8));
-  for (size_t e = 0; e < X.plans.size(); ++e)
-    if (X.plans[e].d.count) X.units.push_back((int32_t)(2u << 30 | e << 16));
-  for (int kf = 0; kf <= X.kmax_all; ++kf)
-    for (size_t e = 0; e < X.plans.size(); ++e) {
-      const PlanDesc& d = X.plans[e].d;
-      if (d.count && kf <= d.kmax)
-        for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(1u << 30 | e << 16 | a << 8 | kf));
-    }
   // K2 takes plans with more stages first: their chains are shorter, so K1
-  // finishes them earlier
+  // can finish them first
   for (size_t e = 0; e < X.plans.size(); ++e)
     if (X.plans[e].d.count) X.k2order.push_back((int32_t)e);
   std::stable_sort(X.k2order.begin(), X.k2order.end(),
                    [&](int32_t x, int32_t y) { return X.plans[x].d.P > X.plans[y].d.P; });
+  // K1 work list: every forward unit first (all start at once; a backward
+  // unit only waits on forward units already taken), then plan by plan in
+  // K2's order its tables and backward units by kf, so that plans complete
+  // one after the other while K2 already evaluates the finished ones
+  for (int32_t e : X.k2order)
+    for (int a = 0; a < X.plans[e].d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8));
+  for (int32_t e : X.k2order) {
+    const PlanDesc& d = X.plans[e].d;
+    X.units.push_back((int32_t)(2u << 30 | e << 16));
+    for (int kf = 0; kf <= d.kmax; ++kf)
+      for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(1u << 30 | e << 16 | a << 8 | kf));
+  }
   X.n_flags = std::max<int64_t>(X.n_flags, 1);
   X.n_tables = std::max<int64_t>(toff, 1);
   X.n_slots = std::max<int64_t>(slot, 1);
@@ -298,7 +297,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_snap = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_k1flags = take((size_t)X.n_flags * 4);
-  X.o_sync = take(16 + (size_t)kMaxE * (4 + 8));  // k1next, pdone[E], pclaim[E]
+  X.o_sync = take(64 + (size_t)kMaxE * (4 + 8));  // k1next (+ development probes), pdone[E], pclaim[E]
   X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
@@ -370,8 +369,8 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.k1units = (const int32_t*)(ws + X.o_units);
   c.k1_total = (int32_t)X.units.size();
   c.k1next = (int32_t*)(ws + X.o_sync);
-  c.pdone = (int32_t*)(ws + X.o_sync + 16);
-  c.pclaim = (unsigned long long*)(ws + X.o_sync + 16 + (size_t)kMaxE * 4);
+  c.pdone = (int32_t*)(ws + X.o_sync + 64);
+  c.pclaim = (unsigned long long*)(ws + X.o_sync + 64 + (size_t)kMaxE * 4);
   c.k2order = (const int32_t*)(ws + X.o_k2order);
   c.n_k2order = (int32_t)X.k2order.size();
   return c;
@@ -449,7 +448,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 16 + (size_t)kMaxE * 12, st);  // K1/K2 counters
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 64 + (size_t)kMaxE * 12, st);  // K1/K2 counters
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);

@@ -636,13 +636,30 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
 template <int MAXT, int MINB>
 __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef PDL_PROBE  // development: K1 / K2 timeline (globaltimer ns) in the sync words
+  unsigned long long* probe = reinterpret_cast<unsigned long long*>(c.k1next) + 1;
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&probe[0], t);
+  }
+#endif
   __shared__ int item;
   for (;;) {
     if (threadIdx.x == 0) item = atomicAdd(c.k1next, 1);
     __syncthreads();
     const int it = item;
     __syncthreads();
-    if (it >= c.k1_total) break;
+    if (it >= c.k1_total) {
+#ifdef PDL_PROBE
+      if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&probe[1], t);
+      }
+#endif
+      break;
+    }
     const uint32_t u = (uint32_t)c.k1units[it];
     const int type = u >> 30, e = (u >> 16) & 0x3FFF, a = (u >> 8) & 255, kf = u & 255;
     if (type == 2) plan_tables(c, e);
@@ -651,7 +668,16 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
+#ifdef PDL_PROBE
+      if (atomicAdd(&c.pdone[e], 1) == plan_items(c.plans[e]) - 1) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        printf("PLANREADY e=%d P=%d count=%llu at +%llu us\n", e, c.plans[e].P, (unsigned long long)c.plans[e].count,
+               (t - probe[0]) / 1000);
+      }
+#else
       atomicAdd(&c.pdone[e], 1);
+#endif
     }
   }
 }
@@ -664,6 +690,10 @@ static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaS
   const int nt = 32 * c.p;
   if (!attr) {  // opt in to large dynamic shared memory once per process
     cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    // the whole unified L1 as shared memory: K2 blocks must fit next to the
+    // K1 blocks while both run
+    cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     attr = true;
   }
   if (nt != per_nt || smem != per_smem) {
@@ -671,7 +701,12 @@ static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaS
     per_nt = nt;
     per_smem = smem;
   }
-  const int grid = std::max(1, std::min(c.k1_total, std::max(1, per) * c.sms));
+#ifndef K1_PER_SM
+#define K1_PER_SM 1
+#endif
+  // one block per SM (occupancy permitting) leaves room on every SM for K2
+  // blocks, which start as soon as the first plans are complete
+  const int grid = std::max(1, std::min(c.k1_total, std::max(1, std::min(per, K1_PER_SM)) * c.sms));
   k1_chains<MAXT, MINB><<<grid, nt, smem, st>>>(c, L);
   return cudaGetLastError();
 }

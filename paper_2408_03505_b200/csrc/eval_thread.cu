@@ -542,6 +542,13 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
       pstate[e] = 0;
     }
   __syncthreads();
+#ifdef PDL_PROBE
+  if (!EXPLICIT && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(reinterpret_cast<unsigned long long*>(c.k1next) + 3, t);
+  }
+#endif
   TS s = ts_at(tsm + (size_t)threadIdx.x * kTStride);
   TPlan p;
   p.e = -1;
@@ -647,6 +654,8 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
 int eval_thread_grid(int sms) {
   int per = 0;
   cudaFuncSetAttribute(k2_eval_thread<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
+  cudaFuncSetAttribute(k2_eval_thread<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(k2_eval_thread<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false>, kTThreads, kTThreads * kTStride);
   return max(1, per) * sms;

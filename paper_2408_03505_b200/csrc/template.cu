@@ -259,6 +259,14 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   for (int i = threadIdx.x; i < c.nflags; i += blockDim.x) c.k1flags[i] = 0;  // K1 progress flags
   for (int i = threadIdx.x; i < c.E; i += blockDim.x) c.pdone[i] = 0;        // K1 -> K2 plan completion
   if (threadIdx.x == 0) *c.k1next = 0;                                         // K1 work counter
+#ifdef PDL_PROBE
+  if (threadIdx.x == 0) {
+    unsigned long long* probe = reinterpret_cast<unsigned long long*>(c.k1next) + 1;
+    printf("PROBE k1start %llu k1end %llu (+%llu us) k2start (+%llu us)\n", probe[0], probe[1],
+           (probe[1] - probe[0]) / 1000, (probe[2] - probe[0]) / 1000);
+    probe[0] = ~0ull; probe[1] = 0; probe[2] = ~0ull;
+  }
+#endif
   if (span_def < 0) {  // default schedule deadlocks: template fails
     if (threadIdx.x == 0) c.scal[2] = 0;
     return;
