@@ -26,6 +26,7 @@
 // base+i) and one ballot tests all 32, skipping blocks that end before the
 // ready time or cannot hold the kernel.
 #include <algorithm>
+#include <cstdio>
 
 #include "optimus_dev.cuh"
 

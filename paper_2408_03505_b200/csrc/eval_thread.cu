@@ -579,11 +579,13 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
     // Plan by plan in k2order, each plan once K1 has completed it (this
     // launch may overlap K1).  This rank's positions: block-cyclic over
     // [begin, end); plan e's are [plo[e], plo[e] + pn[e]).  A warp claims
-    // 32 * kTRun consecutive positions of one plan at a time.
-    constexpr uint64_t per_warp = 32ull * kTRun;
+    // 32 * r consecutive positions of one plan at a time (r consecutive
+    // candidates per lane), r from 8 down to 1 as the plan's remaining work
+    // shrinks (guided self-scheduling: no long tail when work is scarce).
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kTThreads / 32);
     for (;;) {
       int e = -1;
-      unsigned long long chunk = 0;
+      unsigned long long chunk = 0, take = 0;
       if (lane == 0) {
         volatile int* pst = pstate;  // shared by the block's warps; only ever raised
         for (;;) {
@@ -596,8 +598,11 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
               if (ld_acquire(&c.pdone[e2]) < plan_items(c.plans[e2])) { pending = true; continue; }
               pst[e2] = 1;
             }
-            const unsigned long long cl = atomicAdd(&c.pclaim[e2], 1ull);
-            if (cl < (pn[e2] + per_warp - 1) / per_warp) { e = e2; chunk = cl; break; }
+            const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
+            const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
+            const unsigned long long tk = min(32ull * kTRun, max(32ull, rem / (2 * nwarps) / 32 * 32));
+            const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
+            if (st0 < pn[e2]) { e = e2; chunk = st0; take = tk; break; }
             pst[e2] = 2;
           }
           if (e >= 0 || !pending) break;
@@ -606,12 +611,14 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
       }
       e = __shfl_sync(0xffffffffu, e, 0);
       chunk = __shfl_sync(0xffffffffu, chunk, 0);
+      take = __shfl_sync(0xffffffffu, take, 0);
       __syncwarp();  // the lanes' table reads follow lane 0's acquire
       if (e < 0) break;
       if (e != p.e) tplan(c, e, p);
-      const uint64_t p0 = plo[e] + chunk * per_warp + (uint64_t)lane * kTRun, pend = plo[e] + pn[e];
+      const uint64_t r = take / 32;
+      const uint64_t p0 = plo[e] + chunk + (uint64_t)lane * r, pend = plo[e] + pn[e];
       uint64_t g = 0;
-      for (uint64_t q = p0; q < min(p0 + kTRun, pend); ++q) {
+      for (uint64_t q = p0; q < min(p0 + r, pend); ++q) {
         if (q == p0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
           const uint64_t rb = q / A.block;
           g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
