@@ -693,8 +693,10 @@ static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaS
     cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     // the whole unified L1 as shared memory: K2 blocks must fit next to the
     // K1 blocks while both run
+#ifndef K1_NO_CARVEOUT
     cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
+#endif
     attr = true;
   }
   if (nt != per_nt || smem != per_smem) {
