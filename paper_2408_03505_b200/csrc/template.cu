@@ -135,7 +135,8 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
   uint32_t op = pos < nops ? tab[pos] : 0;
   int64_t polled = 0;
   for (int round = 0;; ++round) {
-    if (poll && (round & 7) == 0 && lane == 0) polled = *(volatile int64_t*)&c.scal[3];  // used 8 rounds later
+    if (poll && (round & 7) == 0 && lane == 0)  // used 8 rounds later
+      asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(polled) : "l"(&c.scal[3]));
     const int dep = (op >> 15) & 0x7FFF;
     const int64_t de = pos >= nops ? -1 : dep == 0x7FFF ? 0 : endv[dep];
     if (de >= 0) {  // one op per stage per round (running ahead serialises the warp)
@@ -145,15 +146,7 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
       const int64_t t = dep == 0x7FFF ? tprev : max(tprev, de + ((op >> 31) ? pp2p : 0));
       const int64_t e = t + (fwd ? dur_f : dur_b);
       endv[self] = e;
-      if (record) {
-        c.opstart[(int64_t)s * nops + pos] = t;
-        const int us = self - self / (S + 1);  // unpadded slot
-        const int mb = us % n, ch = (us / n) % v;
-        if (s == 0 && ch == 0) {
-          if (fwd) c.F[mb] = t;      // F_i: start of F(stage 0, chunk 0, i) (R4)
-          else c.B[mb] = e;          // B_i: end of B(stage 0, chunk 0, i)
-        }
-      }
+      if (record) c.opstart[(int64_t)s * nops + pos] = t;
       tprev = e;
       ++pos;
       op = nxt;
@@ -173,6 +166,19 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
         if (b > 0) bound = b - 1;
       }
       if (__any_sync(0xffffffffu, tprev > bound)) return -3;
+    }
+  }
+  if (record) {  // F_i / B_i (R4): start of F / end of B of (stage 0, chunk 0, microbatch i)
+    __syncwarp();
+    for (int pos = lane; pos < nops; pos += 32) {
+      int self, dep, fwd, cross;
+      op_slots(p, v, n, 0, pos, W[0], vch, vmb, self, dep, fwd, cross);
+      const int mb = self % n, ch = (self / n) % v;
+      if (ch == 0) {
+        const int64_t t = c.opstart[pos];
+        if (fwd) c.F[mb] = t;
+        else c.B[mb] = t + dur_b;
+      }
     }
   }
   return warp_max64(tprev);  // lanes >= p hold T_ag <= every end
