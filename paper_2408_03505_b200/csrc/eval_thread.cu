@@ -340,16 +340,16 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_
 // the order is (t, j), slot of (t, j) gets rank N_j - t + 1; own/rk are not
 // materialised.
 __device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, int m, TS& s) {
-  uint8_t* act = s.seen;
-  for (int j = 0; j < m; ++j) act[j] = (uint8_t)j;
+  uint8_t* actN = s.seen;  // N_j of the pipelines still active, in pipeline order
+  for (int j = 0; j < m; ++j) actN[j] = s.N[j];
   int na = m, pos = 0;
   int64_t best = kNegInf;
   for (int t = 1; na > 0; ++t) {
     int nn = 0;
     for (int q = 0; q < na; ++q) {
-      const int j = act[q], Nj = s.N[j];
+      const int Nj = actN[q];
       best = max(best, __ldg(&p.preBEF[Nj - t + 1]) - D[pos++]);
-      if (Nj > t) act[nn++] = (uint8_t)j;
+      if (Nj > t) actN[nn++] = (uint8_t)Nj;
     }
     na = nn;
   }
@@ -423,7 +423,13 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
   int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
-  int64_t dep = tdep_fwd(p, G, n, sumc, n + 1, s, 0);
+  // initial forward shift (no thresholds, no trial): the first slot of each
+  // level t sits at position sum_{t' < t} cnt[t'] (tdep_fwd with M = 0)
+  int64_t dep = kNegInf;
+  for (int t = 1, pos = 0; pos < n; ++t) {
+    dep = max(dep, __ldg(&p.preEF[t]) - G[pos]);
+    pos += s.cnt[t];
+  }
   int64_t Delta;
   for (;;) {
     ++itf;

@@ -252,3 +252,47 @@ def test_rebuild_determinism(dev, oracle_mod):
         other.eval_candidates(0, min(total, 100000), b2)
         ctx.rebuild()
         assert tables() == base, it
+
+
+def _wide_problem(seed, pp, v, k):
+    """A random problem re-planned onto a wide LLM pipeline (PP 16..32: the
+    K1 launch variants for more than 12 stage warps per block)."""
+    q = random_problem(seed, max_p=8, max_t=2, max_n=8)
+    lc = 1
+    q["name"] = f"wide_pp{pp}_v{v}_{seed}"
+    q["llm"] = {"dp": 2, "pp": pp, "tp": q["llm"]["tp"], "v": v}
+    q["llm_layers"] = pp * v * lc
+    q["n_mb"] = pp * k
+    q["n_gpu"] = pp * q["llm"]["tp"] * 2
+    return q
+
+
+WIDE = [_wide_problem(3, 16, 2, 2), _wide_problem(5, 24, 1, 1), _wide_problem(8, 32, 1, 1)]
+
+
+@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+def test_wide_pipelines(dev, oracle_mod, prob):
+    """Template, every plan's chain tables and sampled candidates for LLM
+    pipelines of 16, 24 and 32 stages."""
+    torch = dev
+    ctx = _load(prob)
+    g = ctx.debug_template()
+    o = oracle_mod.template(prob)
+    for k in ("T_end", "W", "F", "B", "w", "z"):
+        assert g[k] == o[k], k
+    orc = oracle_mod.Oracle(prob)
+    total, n_plans = ctx.num_candidates()
+    for e in range(n_plans):
+        t = ctx.debug_plan_tables(e)
+        if t is None:
+            continue
+        for a in range(t["rp"]):
+            assert t["INB_F"][a] == orc.row_chains(e, a, -1, t["kmax"]), (e, a)
+            for kf in range(t["lenF"][a] + 1):
+                assert t["INB_B"][a][kf] == orc.row_chains(e, a, kf, t["kmax"]), (e, a, kf)
+    idx = np.array(sample_indices(99, min(total, 512), total), dtype=np.uint64)
+    lat = torch.empty(len(idx), dtype=torch.int64, device="cuda")
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_indices(torch.from_numpy(idx.astype(np.int64)).cuda(), b2, lat_out=lat)
+    torch.cuda.synchronize()
+    assert np.array_equal(lat.cpu().numpy(), orc.eval(idx, threads=THREADS))
