@@ -22,7 +22,7 @@ namespace optimus {
 namespace {
 
 constexpr int kTThreads = 128;
-constexpr int kTRun = 8;                  // consecutive candidates per thread
+constexpr int kTRun = 16;                 // most consecutive candidates per thread and claim
 #ifndef K2T_MINB
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
             }
             const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
             const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
-            const unsigned long long tk = min(32ull * kTRun, max(32ull, rem / (2 * nwarps) / 32 * 32));
+            const unsigned long long tk = min(32ull * kTRun, max(32ull, rem / nwarps / 32 * 32));
             const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
             if (st0 < pn[e2]) { e = e2; chunk = st0; take = tk; break; }
             pst[e2] = 2;
