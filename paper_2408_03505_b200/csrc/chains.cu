@@ -609,7 +609,7 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   }
 #ifdef K1_STATS
   K1ST(6, clock64() - tk0);
-  if (active && lane == 0 && k1st[s][6] > 200000)
+  if (active && lane == 0 && k1st[s][6] > 150000)
     printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d prolog=%llu setup=%llu slow=%llu x=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
            (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
 #endif

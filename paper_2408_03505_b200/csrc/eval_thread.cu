@@ -254,20 +254,33 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
     if (s.c[j] > 0) act[na++] = (uint8_t)j;
   int slot = 0, mi = 0;
   int64_t dep_b = kNegInf;
+  int64_t mv = nm > 0 ? mval(0) : INT64_MAX;  // value of the next moved entry
   for (int t = 1; na > 0; ++t) {
     const int64_t v = __ldg(&p.preEF[t]) - Df;
+    while (mv < v) {  // moved entries below this level's value precede all of it
+      assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
+      ++mi;
+      mv = mi < nm ? mval(mi) : INT64_MAX;
+    }
     int nn = 0;
-    for (int q = 0; q < na; ++q) {
-      const int j = act[q];
-      const int key = (j << 8) | (t - 1);
-      while (mi < nm) {
-        const int64_t mv = mval(mi);
-        if (!(mv < v || (mv == v && mkey(mi) < key))) break;
-        assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
-        ++mi;
+    if (mv == v) {  // equal values: merge by key
+      for (int q = 0; q < na; ++q) {
+        const int j = act[q];
+        const int key = (j << 8) | (t - 1);
+        while (mv == v && mkey(mi) < key) {
+          assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
+          ++mi;
+          mv = mi < nm ? mval(mi) : INT64_MAX;
+        }
+        assign_slot(p, D, s, j, slot, dep_b);
+        if (s.c[j] > t) act[nn++] = (uint8_t)j;
       }
-      assign_slot(p, D, s, j, slot, dep_b);
-      if (s.c[j] > t) act[nn++] = (uint8_t)j;
+    } else {
+      for (int q = 0; q < na; ++q) {
+        const int j = act[q];
+        assign_slot(p, D, s, j, slot, dep_b);
+        if (s.c[j] > t) act[nn++] = (uint8_t)j;
+      }
     }
     na = nn;
   }
