@@ -182,6 +182,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
   if ((size_t)X.p * 2 * X.v * X.n * 8 + (size_t)X.p * X.nops * 8 + 4 * (size_t)X.n * X.v + 16 > 200 * 1024 ||
       (size_t)X.p * 2 * X.v * X.n > 32767)
     return fail(OPTIMUS_ERANGE, "PP*V*N_mb too large for the K0 shared-memory simulation");
+  if ((size_t)(std::max(X.icapc, X.icapm) + 31) / 32 * 32 + (size_t)X.nops * 5 + 64 > 160 * 1024)
+    return fail(OPTIMUS_ERANGE, "too many bubble intervals per stage for the K0 interval kernel");
   {
     const size_t ci = (size_t)(std::max(X.icapc, X.icapm) + 31) / 32;
     const size_t per = (size_t)X.nk_max * 9 + 64 + (size_t)(3 * X.p + 1) * 4 + (size_t)X.p * 2 * ci * 8 +

@@ -412,17 +412,33 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
       const int64_t v = valid ? seq[i + lane] : 0;
       const bool comm = v < 0;
       const int64_t d = v & INT64_MAX;
-      int64_t D = d;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t t = __shfl_up_sync(FULL, D, o);
-        if (lane >= o) D += t;
-      }
+      int64_t D, Dc, Dp;  // inclusive prefix sum; exclusive sums at the first lane of each resource
       const unsigned mc = __ballot_sync(FULL, valid && comm), mp = __ballot_sync(FULL, valid && !comm);
       const int fc = mc ? __ffs(mc) - 1 : 32, fp = mp ? __ffs(mp) - 1 : 32;
-      const int64_t Dex = D - d;
-      const int64_t Ac = w1.clo - __shfl_sync(FULL, Dex, fc & 31);
-      const int64_t Ap = w0.clo - __shfl_sync(FULL, Dex, fp & 31);
+      if (__all_sync(FULL, d < (int64_t(1) << 26))) {  // the usual case: a 32-bit scan cannot overflow
+        unsigned D32 = (unsigned)d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(FULL, D32, o);
+          if (lane >= o) D32 += t;
+        }
+        const unsigned Dex32 = D32 - (unsigned)d;
+        D = D32;
+        Dc = __shfl_sync(FULL, Dex32, fc & 31);
+        Dp = __shfl_sync(FULL, Dex32, fp & 31);
+      } else {
+        D = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t t = __shfl_up_sync(FULL, D, o);
+          if (lane >= o) D += t;
+        }
+        const int64_t Dex = D - d;
+        Dc = __shfl_sync(FULL, Dex, fc & 31);
+        Dp = __shfl_sync(FULL, Dex, fp & 31);
+      }
+      const int64_t Ac = w1.clo - Dc;
+      const int64_t Ap = w0.clo - Dp;
       int64_t st = ready;
       if (lane >= fc) st = max(st, Ac);
       if (lane >= fp) st = max(st, Ap);

@@ -284,13 +284,17 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
     for (int s = 0; s < p; ++s) { firstb[s] = base; base += default_w(p, v, n, s) + 1; }
   }
   __syncthreads();
-  if (c.policy == 1 && threadIdx.x < p) {  // smallest successful w per stage (speculative)
-    const int s = threadIdx.x;
-    int best = INT32_MAX;
-    for (int x = 0; x <= default_w(p, v, n, s); ++x)
-      if (c.k0res[firstb[s] + x] == span_def) { best = x; break; }
-    c.bestw[s] = best;
-  }
+  __shared__ int bestw_sm[kMaxP];
+  if (threadIdx.x < p) bestw_sm[threadIdx.x] = INT32_MAX;
+  __syncthreads();
+  if (c.policy == 1)  // smallest successful w per stage (speculative), all trials in parallel
+    for (int b = threadIdx.x; b < c.k0_trials; b += blockDim.x) {
+      int s = 0, w = b;
+      while (w > default_w(p, v, n, s)) { w -= default_w(p, v, n, s) + 1; ++s; }
+      if (c.k0res[1 + b] == span_def) atomicMin(&bestw_sm[s], w);
+    }
+  __syncthreads();
+  if (c.policy == 1 && threadIdx.x < p) c.bestw[threadIdx.x] = bestw_sm[threadIdx.x];
   __syncthreads();
   if (threadIdx.x == 0) {
     int s = -1;
@@ -430,6 +434,13 @@ __device__ __forceinline__ int gap_after(const LTab& Lf, const LTab& Lb, const i
   return 0;
 }
 
+__host__ __device__ __forceinline__ size_t k0_iv_bmx_offset(int nops) {
+  return ((size_t)(nops + 1) * 4 + nops + 15) & ~size_t(15);
+}
+__host__ __device__ __forceinline__ size_t k0_iv_smem_bytes(int nops, int ci) {
+  return k0_iv_bmx_offset(nops) + (size_t)4 * ci * 8;
+}
+
 // k0_intervals, one block per LLM stage: every thread takes a contiguous
 // run of the stage's kernels, counts its intervals, one block scan gives
 // the output offsets, a second pass writes them (time order is kernel order).
@@ -438,12 +449,17 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   __shared__ typename Scan::TempStorage tmp;
   __shared__ LTab Lf, Lb;
   __shared__ int run_c, run_m;
-  extern __shared__ int opoff[];  // [nops + 1] kernel offset of each op, then [nops] op is forward
+  // dynamic: [nops + 1] kernel offset of each op, [nops] op is forward, then
+  // (8-aligned) bmx[4][ci_n]: the per-block capacity maxima being built
+  extern __shared__ __align__(16) int opoff[];
   if (c.scal[2] == 0) return;     // template failed (deadlock): nothing to emit
   const int s = blockIdx.x, warp = threadIdx.x >> 5;
   const int p = c.p, v = c.v, n = c.n, nops = c.nops, lc = c.lc;
   const int Ws = c.W[s];
   uint8_t* opfwd = reinterpret_cast<uint8_t*>(opoff + nops + 1);
+  const int CI = c.ci_n;
+  long long* bmx = reinterpret_cast<long long*>(reinterpret_cast<unsigned char*>(opoff) + k0_iv_bmx_offset(nops));
+  for (int i = threadIdx.x; i < 4 * CI; i += blockDim.x) bmx[i] = kNegInf;
   if (warp == 0) load_ltab(c, 0, Lf);
   if (warp == 1) load_ltab(c, 1, Lb);
   for (int q = threadIdx.x; q < nops; q += blockDim.x) opfwd[q] = (uint8_t)op_at(p, v, n, Ws, q).fwd;
@@ -496,36 +512,25 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   unsigned long long off, tot;
   Scan(tmp).ExclusiveSum(cnt, off, tot);
   int oc = run_c + (int)(off & 0xffffffffu), om = run_m + (int)(off >> 32);
+  // per 32-interval block, the largest base capacity hi - lo, in time order
+  // (orientation 0) and in mirrored order (1, interval i' = count-1-i): no
+  // kernel longer than it fits anywhere in the block (K1 skips such blocks)
+  const int nc = run_c + (int)(tot & 0xffffffffu), nm = run_m + (int)(tot >> 32);
+  auto note = [&](int r, int idx, int count, int64_t cap) {
+    atomicMax(&bmx[(r * 2 + 0) * CI + (idx >> 5)], (long long)cap);
+    atomicMax(&bmx[(r * 2 + 1) * CI + ((count - 1 - idx) >> 5)], (long long)cap);
+  };
+  if (threadIdx.x == 0 && run_m == 1) note(1, 0, nm, mhi[0] - mlo[0]);  // the head comm-free piece
   for (int kk = k0, q = q0; kk < k1; ++kk) {
     while (kk >= opoff[q + 1]) ++q;
     int64_t lo, hi;
     const int g = gap_after(Lf, Lb, ost, opfwd, nops, lc, q, kk - opoff[q], w, z, lo, hi);
-    if (g == 1) { clo[oc] = lo; chi[oc] = hi; ++oc; }
-    if (g == 2) { mlo[om] = lo; mhi[om] = hi; ++om; }
+    if (g == 1) { clo[oc] = lo; chi[oc] = hi; note(0, oc, nc, hi - lo); ++oc; }
+    if (g == 2) { mlo[om] = lo; mhi[om] = hi; note(1, om, nm, hi - lo); ++om; }
   }
   __syncthreads();
-  if (threadIdx.x == 0) { run_c += (int)(tot & 0xffffffffu); run_m += (int)(tot >> 32); }
-  __syncthreads();
-  if (threadIdx.x == 0) { c.ncomp[s] = run_c; c.ncomm[s] = run_m; }
-  __syncthreads();
-  // per 32-interval block, the largest base capacity hi - lo, in time order
-  // (orientation 0) and in mirrored order (1, interval i' = count-1-i): no
-  // kernel longer than it fits anywhere in the block (K1 skips such blocks)
-  const int CI = c.ci_n, lane = threadIdx.x & 31;
-  for (int t = threadIdx.x >> 5; t < 4 * CI; t += kIvThreads / 32) {
-    const int r = t / (2 * CI), o = (t / CI) & 1, b = t % CI;
-    const int cnt = r == 0 ? run_c : run_m;
-    const int64_t* L = r == 0 ? clo : mlo;
-    const int64_t* H = r == 0 ? chi : mhi;
-    const int i = 32 * b + lane;
-    int64_t cap = kNegInf;
-    if (i < cnt) {
-      const int ri = o == 0 ? i : cnt - 1 - i;
-      cap = H[ri] - L[ri];
-    }
-    cap = warp_max64(cap);
-    if (lane == 0) c.bmax[(((int64_t)s * 2 + r) * 2 + o) * CI + b] = cap;
-  }
+  if (threadIdx.x == 0) { c.ncomp[s] = nc; c.ncomm[s] = nm; }
+  for (int i = threadIdx.x; i < 4 * CI; i += blockDim.x) c.bmax[(int64_t)s * 4 * CI + i] = bmx[i];
 }
 
 }  // namespace
@@ -538,12 +543,13 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
   if (!attrs) {
     cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k0_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);  // + ~11 KB static
     attrs = true;
   }
   const int nsim = 1 + c.k0_trials;
   k0_wave<<<(nsim + wpb - 1) / wpb, 32 * kSimWarps, smem, st>>>(c, nsim, wpb);
   k0_final<<<1, 32 * kSimWarps, smem, st>>>(c, wpb);
-  k0_intervals<<<c.p, kIvThreads, (c.nops + 1) * sizeof(int) + c.nops, st>>>(c);
+  k0_intervals<<<c.p, kIvThreads, k0_iv_smem_bytes(c.nops, c.ci_n), st>>>(c);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
