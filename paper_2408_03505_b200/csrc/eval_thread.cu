@@ -418,22 +418,24 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
                          TStats& st) {
   const int n = c.n, m = p.m, rt = p.rt, kmax = p.kmax;
   // ---------------- coarse init (R9) -------------------------------------
-  for (int t = 0; t <= n + 1; ++t) s.cnt[t] = 0;
+  for (int t = 0; t < (n + 5) / 4; ++t) reinterpret_cast<uint32_t*>(s.cnt)[t] = 0u;  // cnt[0..n+1] (4-aligned)
   // the first findCritical of both phases runs on N: one pass for both keys
   uint32_t kf0 = 0, kb0 = 0;
+  int maxN = 0;
   {
     int base = 0, r = 0;
     for (int j = 0; j < m; ++j) {
       const int Nj = s.N[j];
       s.c[j] = (uint8_t)Nj;
       s.cnt[Nj] += 1;
+      maxN = max(maxN, Nj);
       const uint32_t lo = (uint32_t)(31 - j);
       kf0 = max(kf0, (__ldg(&p.keyF[base + Nj]) << 5) | lo);
       kb0 = max(kb0, (__ldg(&p.keyB[base + Nj]) << 5) | lo);
       if (++r == rt) { r = 0; base += p.np1; }
     }
   }
-  for (int t = n - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
+  for (int t = maxN - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
   int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
   // initial forward shift (no thresholds, no trial): the first slot of each
