@@ -296,3 +296,24 @@ def test_wide_pipelines(dev, oracle_mod, prob):
     ctx.eval_indices(torch.from_numpy(idx.astype(np.int64)).cuda(), b2, lat_out=lat)
     torch.cuda.synchronize()
     assert np.array_equal(lat.cpu().numpy(), orc.eval(idx, threads=THREADS))
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_default_warmup_policy(dev, oracle_mod, seed):
+    """warmup_policy 0 (Megatron default warm-up, no R5 adjustment): template
+    and the full candidate space."""
+    torch = dev
+    prob = random_problem(seed)
+    prob["warmup_policy"] = 0
+    prob["name"] += "_policy0"
+    ctx = _load(prob)
+    g = ctx.debug_template()
+    o = oracle_mod.template(prob)
+    for k in ("T_end", "W", "F", "B", "w", "z"):
+        assert g[k] == o[k], k
+    total, _ = ctx.num_candidates()
+    lat = torch.empty(total, dtype=torch.int64, device="cuda")
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, b2, lat_out=lat)
+    torch.cuda.synchronize()
+    assert np.array_equal(lat.cpu().numpy(), oracle_mod.Oracle(prob).eval(np.arange(total, dtype=np.uint64)))
