@@ -227,6 +227,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
         d.devF = toff; toff += (int64_t)d.rp * np1;
         d.devB = toff; toff += (int64_t)d.rp * np1;
         d.devK = toff; toff += (int64_t)d.rp * np1;
+        d.bpF = toff; toff += (int64_t)d.rp * d.kmax;
         d.inbF = toff; toff += (int64_t)d.rp * d.kmax;
         d.lenF = toff; toff += d.rp;
         d.inbB = toff; toff += (int64_t)d.rp * (d.kmax + 1) * d.kmax;

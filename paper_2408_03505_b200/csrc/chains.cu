@@ -641,6 +641,19 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
       atomicExch(&flags[0], 1);  // forward unit done: versions > lenF never come
     }
   }
+  if (!M) {  // for K2's forward dependency test: the first slot each chain end can precede
+    __syncthreads();
+    const int len = (int)c.tables[pd.lenF + a];
+    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+      const int64_t ef = c.tables[pd.inbF + (int64_t)a * pd.kmax + k];
+      int lo = 0, hi = c.n;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (c.F[mid] - c.L >= ef) hi = mid; else lo = mid + 1;
+      }
+      c.tables[pd.bpF + (int64_t)a * pd.kmax + k] = lo + 1;
+    }
+  }
 }
 
 // Persistent: every block takes work items in list order (forward units

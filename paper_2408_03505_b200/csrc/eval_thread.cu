@@ -79,6 +79,7 @@ struct TPlan {
   const uint32_t* keyF;   // order ranks of devF / devB (0 at count 0)
   const uint32_t* keyB;
   const int64_t* inbF;
+  const int64_t* bpF;
   const int64_t* lenF;
   const int64_t* inbB;
   const int64_t* lenB;
@@ -104,6 +105,7 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.keyF = reinterpret_cast<const uint32_t*>(c.tables + d.devK);
   p.keyB = p.keyF + (int64_t)d.rp * (c.n + 1);
   p.inbF = c.tables + d.inbF;
+  p.bpF = c.tables + d.bpF;
   p.lenF = c.tables + d.lenF;
   p.inbB = c.tables + d.inbB;
   p.lenB = c.tables + d.lenB;
@@ -457,7 +459,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (kfj >= (int)__ldg(&p.lenF[as])) break;  // ScheduleKernels fails (R12)
     const int64_t EF = __ldg(&p.inbF[as * kmax + kfj]);
     ++atf;
-    const int bp = first_ge(G, n, EF);  // EF_i + L <= F_i holds for slots >= bp
+    const int bp = (int)__ldg(&p.bpF[as * kmax + kfj]);  // EF_i + L <= F_i holds for slots >= bp
     s.c[js] = (uint8_t)(cjs - 1);       // trial move
     s.cnt[cjs] -= 1;
     const int64_t dep2 = tdep_fwd(p, G, n, sumc - 1, bp, s, M);

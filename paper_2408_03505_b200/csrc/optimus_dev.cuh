@@ -24,6 +24,7 @@ struct PlanDesc {
   // offsets, in int64 elements, of this plan's tables from Cfg::tables
   int64_t preF, preB, devF, devB, inbF, lenF, inbB, lenB;
   int64_t devK;       // rp*(n+1) words: uint32 order ranks of DEV_F then DEV_B (0 at cnt 0)
+  int64_t bpF;        // [rp][kmax]: first LLM slot (1-based) whose F - L >= INB_F[a][k] (n+1: none)
   int64_t slot_base;  // first K1 scratch slot of this plan
   int64_t flag_base;  // first K1 flag of this plan: per row [kmax + 1] (0: forward done, v: stages that published version v)
 };
