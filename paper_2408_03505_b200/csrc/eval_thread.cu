@@ -22,7 +22,10 @@ namespace optimus {
 namespace {
 
 constexpr int kTThreads = 128;
-constexpr int kTRun = 16;                 // most consecutive candidates per thread and claim
+#ifndef K2T_RUN
+#define K2T_RUN 16
+#endif
+constexpr int kTRun = K2T_RUN;            // most consecutive candidates per thread and claim
 #ifndef K2T_MINB
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
