@@ -755,7 +755,10 @@ cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
   const size_t smem = k1_smem_bytes(L);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (launches) *launches += 1;
-  if (c.p <= 12) return launch_k1<384, 2>(c, L, smem, st);
+#ifndef K1_MINB
+#define K1_MINB 2
+#endif
+  if (c.p <= 12) return launch_k1<384, K1_MINB>(c, L, smem, st);
   if (c.p <= 16) return launch_k1<512, 1>(c, L, smem, st);
   return launch_k1<1024, 1>(c, L, smem, st);
 }
