@@ -493,6 +493,12 @@ __host__ __device__ inline size_t k1_smem_bytes(const K1Launch& L) {
   return unit_smem_bytes(L.NK, L.Pmax, L.CI) + (size_t)L.Pmax * L.KM * (8 + 4) + 16;
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -519,12 +525,15 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   int* flags = c.k1flags + pd.flag_base + (int64_t)a * (pd.kmax + 1);
   if (M && kf > 0) {  // wait for forward version kf of this row
     if (threadIdx.x == 0) {
+      // poll relaxed (an acquire load invalidates the SM's L1, which the
+      // running units on this SM read their intervals through); acquire once
       int ok;
       for (;;) {
-        if (ld_acquire(&flags[kf]) >= P) { ok = 1; break; }
-        if (ld_acquire(&flags[0]) != 0) { ok = ld_acquire(&flags[kf]) >= P; break; }
+        if (ld_relaxed(&flags[kf]) >= P) { ok = 1; break; }
+        if (ld_relaxed(&flags[0]) != 0) { ok = ld_acquire(&flags[kf]) >= P; break; }
         __nanosleep(256);
       }
+      (void)ld_acquire(&flags[kf]);
       go = ok;
     }
     __syncthreads();

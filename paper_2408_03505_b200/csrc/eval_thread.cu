@@ -534,6 +534,12 @@ __device__ __forceinline__ uint64_t rank_pos(const EvalArgs& A, uint64_t x) {
   return (fb / A.world) * A.block + (k > A.rank ? A.block : 0) + (k == A.rank ? rem : 0);
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -620,8 +626,9 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
             const int e2 = c.k2order[k];
             const int ps = pst[e2];
             if (ps == 2 || pn[e2] == 0) continue;
-            if (ps == 0) {
-              if (ld_acquire(&c.pdone[e2]) < plan_items(c.plans[e2])) { pending = true; continue; }
+            if (ps == 0) {  // poll relaxed (an acquire load invalidates L1), acquire once when complete
+              if (ld_relaxed(&c.pdone[e2]) < plan_items(c.plans[e2])) { pending = true; continue; }
+              (void)ld_acquire(&c.pdone[e2]);
               pst[e2] = 1;
             }
             const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
