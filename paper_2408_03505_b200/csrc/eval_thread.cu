@@ -157,7 +157,10 @@ __device__ bool tnext(int m, TS& s) {
   }
   if (jj < 0) return false;
   s.N[jj] += 1;
-  for (int j = jj + 1; j < m - 1; ++j) s.N[j] = 1;
+  int j = jj + 1;  // parts jj+1 .. m-2 become 1 (word stores where aligned; N is 4-byte aligned)
+  for (; j < m - 1 && (j & 3); ++j) s.N[j] = 1;
+  for (; j + 4 <= m - 1; j += 4) *reinterpret_cast<uint32_t*>(s.N + j) = 0x01010101u;
+  for (; j < m - 1; ++j) s.N[j] = 1;
   s.N[m - 1] = (uint8_t)(S - 1 - (m - 2 - jj));
   return true;
 }
