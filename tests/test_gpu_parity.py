@@ -317,3 +317,35 @@ def test_default_warmup_policy(dev, oracle_mod, seed):
     ctx.eval_candidates(0, total, b2, lat_out=lat)
     torch.cuda.synchronize()
     assert np.array_equal(lat.cpu().numpy(), oracle_mod.Oracle(prob).eval(np.arange(total, dtype=np.uint64)))
+
+
+STRESS = [random_problem(s, max_p=8, max_t=8, max_n=16) for s in range(300, 420)]
+
+
+@pytest.mark.parametrize("chunk", range(4))
+def test_stress_sweep(dev, oracle_mod, chunk):
+    """120 wider random problems (PP up to 8, TP up to 8, up to 16
+    microbatches, jittered kernels, P2P latencies): every candidate of the
+    small spaces, 2048 seeded candidates of the large ones, through the
+    overlapped K1/K2 path (eval_candidates) and the explicit path."""
+    torch = dev
+    for prob in STRESS[chunk::4]:
+        ctx = _load(prob)
+        total, _ = ctx.num_candidates()
+        if total == 0:
+            continue
+        o = oracle_mod.Oracle(prob)
+        b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        if total <= 50000:
+            lat = torch.empty(total, dtype=torch.int64, device="cuda")
+            ctx.eval_candidates(0, total, b2, lat_out=lat)
+            torch.cuda.synchronize()
+            ref = o.eval(np.arange(total, dtype=np.uint64), threads=THREADS)
+            assert np.array_equal(lat.cpu().numpy(), ref), prob["name"]
+            assert int(b2[1].item()) == int(np.argmin(ref)), prob["name"]
+        else:
+            idx = np.array(sample_indices(5, 2048, total), dtype=np.uint64)
+            lat = torch.empty(len(idx), dtype=torch.int64, device="cuda")
+            ctx.eval_indices(torch.from_numpy(idx.astype(np.int64)).cuda(), b2, lat_out=lat)
+            torch.cuda.synchronize()
+            assert np.array_equal(lat.cpu().numpy(), o.eval(idx, threads=THREADS)), prob["name"]
