@@ -156,6 +156,21 @@ int optimus_eval_indices(optimus_ctx* c, const uint64_t* d_index, uint64_t count
 int optimus_best_plan(const optimus_ctx* c, const int64_t* h_best2_all_ranks, int32_t world, optimus_result* out,
                       int32_t* counts_out);
 
+/* Schedule decisions of one candidate g (the step after the
+ * argmin; Alg. 2 P:335-354 and §4.2 P:387-400 for the moves):
+ * re-evaluates g on the GPU and returns, in host h_out (int64, cap >= 8 +
+ * 2*N_mb + 3*m, *len = entries written):
+ *   [0] lat  [1] Delta_f  [2] Delta_b  [3] forward moves  [4] backward moves
+ *   [5] plan index  [6] m  [7] N_mb
+ *   [8, 8+N_mb)            pipeline of each committed forward move, in order
+ *   [8+N_mb, 8+2*N_mb)     pipeline of each committed backward move, in order
+ *   then N[m], the coarse forward counts c[m] and coarse backward counts cb[m]
+ *   after both phases.  Pipeline j's k-th forward move is row (j / r_t)'s
+ *   k-th chain (R-FACT), so these decisions and the chain tables fix every
+ *   kernel placement.  ERANGE if g >= total or cap is too small; synchronises
+ *   `cuda_stream`. */
+int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream);
+
 /* Introspection for parity tests (synchronises `cuda_stream`; device->host).
  * Template: h_out = [p, n, T_end, span_def, W'[p], F[n], B[n], w[p], z[p],
  * ncomp[p], ncomm[p], then per stage: compute-free (lo,hi)..., comm-free

@@ -61,7 +61,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, o_explain, total_bytes;
   int grid;
 };
 
@@ -306,6 +306,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
   X.o_stats = take(8 * 8);
+  X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN) * 8);
   X.total_bytes = o;
   return OPTIMUS_OK;
 }
@@ -588,6 +589,30 @@ int optimus_best_plan(const optimus_ctx* c, const int64_t* h_best2_all_ranks, in
     return OPTIMUS_OK;
   }
   return fail(OPTIMUS_ERANGE, "index not in any plan");
+}
+
+int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream) {
+  if (!c || !h_out || !len) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  if (g >= c->X.total) return fail(OPTIMUS_ERANGE, "index %llu >= %llu", (unsigned long long)g, (unsigned long long)c->X.total);
+  int m = 0;
+  for (const auto& hp : c->X.plans)
+    if (hp.d.count && g >= hp.d.first && g < hp.d.first + hp.d.count) m = hp.d.m;
+  const size_t need = 8 + 2 * (size_t)c->X.n + 3 * (size_t)m;
+  if (cap < need) return fail(OPTIMUS_ERANGE, "cap %zu < %zu", cap, need);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int64_t* d = (int64_t*)(c->ws + c->X.o_explain);
+  CK(launch_explain(c->cfg, g, d, st));
+  std::vector<int64_t> buf(8 + 2 * kMaxN + 3 * kMaxN);
+  CK(cudaMemcpyAsync(buf.data(), d, buf.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int n = c->X.n;
+  size_t o = 0;
+  for (int i = 0; i < 8; ++i) h_out[o++] = buf[i];
+  for (int i = 0; i < 2 * n; ++i) h_out[o++] = buf[8 + i];
+  for (int i = 0; i < 3 * m; ++i) h_out[o++] = buf[8 + 2 * n + i];
+  *len = o;
+  return OPTIMUS_OK;
 }
 
 int optimus_debug_template(const optimus_ctx* c, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream) {

@@ -422,8 +422,12 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, 
 }
 
 // One candidate, sequentially in this thread.
+// EXPLAIN (NEXT-1, one candidate): xo[8 + t] = pipeline of the t-th committed
+// forward move, xo[8 + n + t] = of the t-th backward move; xo[1..4] = Df, Db,
+// forward / backward move counts.
+template <bool EXPLAIN = false>
 __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
-                         TStats& st) {
+                         TStats& st, int64_t* xo = nullptr) {
   const int n = c.n, m = p.m, rt = p.rt, kmax = p.kmax;
   // ---------------- coarse init (R9) -------------------------------------
   for (int t = 0; t < (n + 5) / 4; ++t) reinterpret_cast<uint32_t*>(s.cnt)[t] = 0u;  // cnt[0..n+1] (4-aligned)
@@ -474,6 +478,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
       s.cnt[cjs] += 1;
       break;
     }
+    if (EXPLAIN) xo[8 + M] = js;
     int q = M++;  // commit: insert the threshold
     while (q > 0 && s.thr[q - 1] > bp) {
       s.thr[q] = s.thr[q - 1];
@@ -517,8 +522,20 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (dep2 > Delta) break;
     for (int i = 0; i < n; ++i) s.Qcb[i] += (s.own[i] == js && EFb <= D[i]) ? 1 : 0;
     s.cb[js] -= 1;
+    if (EXPLAIN) xo[8 + n + (n - sumcb)] = js;
     dep_b = dep2;
     --sumcb;
+  }
+  if (EXPLAIN) {
+    xo[1] = Df;
+    xo[2] = Delta;
+    xo[3] = M;
+    xo[4] = n - sumcb;
+    for (int j = 0; j < m; ++j) {
+      xo[8 + 2 * n + j] = s.N[j];
+      xo[8 + 2 * n + m + j] = s.c[j];
+      xo[8 + 2 * n + 2 * m + j] = init_b ? s.cb[j] : s.N[j];
+    }
   }
   st.v[0] += 1;
   st.v[1] += m;
@@ -692,6 +709,35 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
   }
 }
 
+// NEXT-1: one candidate's decisions (the schedule's moves), for emission.
+// out: [0] lat, [1] Df, [2] Db, [3] forward moves, [4] backward moves,
+// [5] plan, [6] m, [7] n, [8, 8+n) forward move pipelines, [8+n, 8+2n)
+// backward ones, then N[m], c_final[m], cb_final[m].  One thread works.
+__global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64_t* out) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  __shared__ int64_t G[kMaxN], D[kMaxN];
+  const int n = c.n;
+  const int64_t T_end = c.scal[1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    G[i] = c.F[i] - c.L;
+    D[i] = T_end - c.B[i] - c.L;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const int e = tfind_plan(c, g);
+  out[0] = -1;
+  if (e < 0) return;
+  TPlan p;
+  tplan(c, e, p);
+  TS s = ts_at(tsm);
+  tunrank(c, n, p.m, g - p.first, s);
+  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
+  out[5] = e;
+  out[6] = p.m;
+  out[7] = n;
+  out[0] = teval<true>(c, p, G, D, T_end, s, st, out);
+}
+
 }  // namespace
 
 int eval_thread_grid(int sms) {
@@ -702,6 +748,11 @@ int eval_thread_grid(int sms) {
   cudaFuncSetAttribute(k2_eval_thread<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false>, kTThreads, kTThreads * kTStride);
   return max(1, per) * sms;
+}
+
+cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
+  k2_explain<<<1, kTThreads, (size_t)kTThreads * kTStride, st>>>(c, g, d_out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {

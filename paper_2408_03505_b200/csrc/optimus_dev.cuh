@@ -135,6 +135,7 @@ struct EvalArgs {
 };
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
+cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
 int eval_thread_grid(int sms);
 }  // namespace optimus

@@ -21,7 +21,8 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_set_eval_mode",
+    "optimus_explain", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count",
+    "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
 ]
@@ -85,6 +86,7 @@ def lib():
             "optimus_eval_indices": [vp, vp, ctypes.c_uint64, vp, vp, vp],
             "optimus_best_plan": [vp, P(ctypes.c_int64), ctypes.c_int32, P(optimus_result), P(ctypes.c_int32)],
             "optimus_debug_template": [vp, P(ctypes.c_int64), sz, P(sz), vp],
+            "optimus_explain": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_set_timing": [vp, ctypes.c_int],
@@ -228,6 +230,19 @@ class Ctx:
                                        ctypes.byref(r), counts))
         return {"lat_ns": r.lat_ns, "index": r.index, "enc": (r.enc.dp, r.enc.pp, r.enc.tp), "m": r.m,
                 "counts": list(counts)[:r.m]}
+
+    def explain(self, g: int, stream=None) -> dict:
+        """The committed moves of candidate g (optimus_explain; NEXT-1)."""
+        buf = (ctypes.c_int64 * (8 + 2 * 32 + 3 * 32))()
+        n = ctypes.c_size_t()
+        _check(lib().optimus_explain(self.h, ctypes.c_uint64(g), buf, len(buf), ctypes.byref(n),
+                                     ctypes.c_void_p(_stream(stream))))
+        v = list(buf[: n.value])
+        nf, nb, m, nmb = v[3], v[4], v[6], v[7]
+        return {"lat": v[0], "df": v[1], "db": v[2], "mf": nf, "mb": nb, "plan": v[5], "m": m,
+                "moves_f": v[8:8 + nf], "moves_b": v[8 + nmb:8 + nmb + nb],
+                "N": v[8 + 2 * nmb:8 + 2 * nmb + m], "c_final": v[8 + 2 * nmb + m:8 + 2 * nmb + 2 * m],
+                "cb_final": v[8 + 2 * nmb + 2 * m:8 + 2 * nmb + 3 * m]}
 
     def debug_template(self, stream=None) -> dict:
         cap = 1 << 24

@@ -349,3 +349,28 @@ def test_stress_sweep(dev, oracle_mod, chunk):
             ctx.eval_indices(torch.from_numpy(idx.astype(np.int64)).cuda(), b2, lat_out=lat)
             torch.cuda.synchronize()
             assert np.array_equal(lat.cpu().numpy(), o.eval(idx, threads=THREADS)), prob["name"]
+
+
+@pytest.mark.parametrize("prob", [config_problem(2), config_problem(4)] + [random_problem(s) for s in range(20)],
+                         ids=lambda p: p["name"])
+def test_explain_matches_oracle_trace(dev, oracle_mod, prob):
+    """optimus_explain (NEXT-1 decisions) against the oracle's trace: lat,
+    shifts, move counts and order (the trace's placement records carry the
+    moving pipeline and the move number), composition and coarse counts."""
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    o = oracle_mod.Oracle(prob)
+    idx = sample_indices(17, min(total, 64), total)
+    lat, aux = o.eval(np.array(idx, dtype=np.uint64), aux=True)
+    aux = np.asarray(aux)
+    picks = list(idx[:8]) + [int(idx[i]) for i in np.argsort(-(aux[:, 2] + aux[:, 3]))[:8]]
+    for g in picks:
+        x = ctx.explain(int(g))
+        t = o.trace(int(g))
+        assert (x["lat"], x["df"], x["db"], x["mf"], x["mb"]) == (t["lat"], t["df"], t["db"], t["mf"], t["mb"]), g
+        assert x["N"] == t["N"] and x["c_final"] == t["c_final"] and x["cb_final"] == t["cb_final"], g
+        for key, recs in (("moves_f", t["fwd_place"]), ("moves_b", t["bwd_place"])):
+            seq = {}
+            for r in recs:
+                seq.setdefault(r[5], r[0])
+            assert x[key] == [seq[k] for k in sorted(seq)], (g, key)
