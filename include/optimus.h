@@ -171,6 +171,19 @@ int optimus_best_plan(const optimus_ctx* c, const int64_t* h_best2_all_ranks, in
  *   `cuda_stream`. */
 int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream);
 
+/* Schedule emission for candidate g: every encoder kernel
+ * placed into the LLM bubbles by g's committed moves, replayed on the GPU
+ * from the build's chain state (§4.2 ScheduleKernels P:347-400; R12, R15).
+ * h_out (host int64, cap entries) receives records of 6 values
+ *   [pipeline j, encoder stage, kind (0 compute, 1 comm), start, end, move t]
+ * in real LLM-template time: first the forward moves in commit order, then
+ * the backward ones; within a move, kernels in placement order (stage by
+ * stage).  n_records[0] / [1] = forward / backward records.  Coarse (pre/
+ * post-LLM) work is not listed: it is the GPipe fill of R9.  ERANGE if cap
+ * is too small; synchronises `cuda_stream`. */
+int optimus_emit_schedule(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* n_records,
+                          void* cuda_stream);
+
 /* Introspection for parity tests (synchronises `cuda_stream`; device->host).
  * Template: h_out = [p, n, T_end, span_def, W'[p], F[n], B[n], w[p], z[p],
  * ncomp[p], ncomm[p], then per stage: compute-free (lo,hi)..., comm-free

@@ -61,7 +61,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, o_explain, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, o_explain, o_rec, total_bytes;
   int grid;
 };
 
@@ -307,6 +307,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_counter = take(8);
   X.o_stats = take(8 * 8);
   X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN) * 8);
+  X.o_rec = take((size_t)std::max(1, X.kmax_all) * std::max(1, X.nk_max) * 4 * 8);
   X.total_bytes = o;
   return OPTIMUS_OK;
 }
@@ -612,6 +613,84 @@ int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap
   for (int i = 0; i < 2 * n; ++i) h_out[o++] = buf[8 + i];
   for (int i = 0; i < 3 * m; ++i) h_out[o++] = buf[8 + 2 * n + i];
   *len = o;
+  return OPTIMUS_OK;
+}
+
+int optimus_emit_schedule(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* n_records,
+                          void* cuda_stream) {
+  if (!c || !h_out || !n_records) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  const Prep& X = c->X;
+  std::vector<int64_t> x(8 + 2 * kMaxN + 3 * kMaxN);
+  size_t xl = 0;
+  int rc = optimus_explain(c, g, x.data(), x.size(), &xl, cuda_stream);
+  if (rc != OPTIMUS_OK) return rc;
+  const int n = X.n, e = (int)x[5], m = (int)x[6], nf = (int)x[3], nbk = (int)x[4];
+  const PlanDesc& d = X.plans[e].d;
+  const int64_t* N = &x[8 + 2 * n];
+  const int64_t* cf = N + m;
+  const int64_t* cbf = N + 2 * m;
+  auto nk = [&](int bwd) {  // kernels of one chain (whole encoder, R8)
+    int64_t t = 0;
+    for (int b = 0; b < X.nb; ++b) {
+      const int id = enc_list_id(b, d.ti, X.ntp, bwd);
+      t += (int64_t)X.blayers[b] * (X.loff[id + 1] - X.loff[id]);
+    }
+    return t;
+  };
+  const int64_t nkF = nk(0), nkB = nk(1);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int64_t T_end = 0;
+  CK(cudaMemcpyAsync(&T_end, c->cfg.scal + 1, 8, cudaMemcpyDeviceToHost, st));
+  int64_t* drec = (int64_t*)(c->ws + X.o_rec);
+  size_t out = 0;
+  auto emit = [&](bool bwd, const std::vector<int64_t>& moves) -> int {
+    // replays per (row, kf), as many chains as the row's pipelines need
+    std::vector<int> taken(m, 0);
+    std::vector<std::pair<int, int>> units;  // (row, kf)
+    std::vector<int> need;
+    for (int j = 0; j < m; ++j) {
+      const int k = bwd ? (int)(N[j] - cbf[j]) : (int)(N[j] - cf[j]);
+      if (k <= 0) continue;
+      const std::pair<int, int> u{j / d.rt, bwd ? (int)(N[j] - cf[j]) : -1};
+      size_t q = 0;
+      while (q < units.size() && units[q] != u) ++q;
+      if (q == units.size()) { units.push_back(u); need.push_back(0); }
+      need[q] = std::max(need[q], k);
+    }
+    const int64_t per = bwd ? nkB : nkF;
+    std::vector<std::vector<int64_t>> recs(units.size());
+    for (size_t q = 0; q < units.size(); ++q) {
+      CK(launch_record(c->cfg, e, units[q].first, units[q].second, need[q], drec, st));
+      recs[q].resize((size_t)need[q] * per * 4);
+      CK(cudaMemcpyAsync(recs[q].data(), drec, recs[q].size() * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (size_t t = 0; t < moves.size(); ++t) {
+      const int js = (int)moves[t];
+      const std::pair<int, int> u{js / d.rt, bwd ? (int)(N[js] - cf[js]) : -1};
+      size_t q = 0;
+      while (units[q] != u) ++q;
+      const int k = taken[js]++;
+      for (int64_t i = 0; i < per; ++i) {
+        const int64_t* r = &recs[q][((size_t)k * per + i) * 4];
+        if (out + 6 > cap) return fail(OPTIMUS_ERANGE, "cap too small for the schedule");
+        h_out[out++] = js;
+        h_out[out++] = r[0];
+        h_out[out++] = r[1];
+        h_out[out++] = bwd ? T_end - r[3] : r[2];  // backward: mirrored time back to real time (R15)
+        h_out[out++] = bwd ? T_end - r[2] : r[3];
+        h_out[out++] = (int64_t)t;
+      }
+    }
+    return OPTIMUS_OK;
+  };
+  std::vector<int64_t> mf(x.begin() + 8, x.begin() + 8 + nf), mb(x.begin() + 8 + n, x.begin() + 8 + n + nbk);
+  if ((rc = emit(false, mf)) != OPTIMUS_OK) return rc;
+  const size_t nfwd = out / 6;
+  if ((rc = emit(true, mb)) != OPTIMUS_OK) return rc;
+  n_records[0] = nfwd;
+  n_records[1] = out / 6 - nfwd;
   return OPTIMUS_OK;
 }
 

@@ -376,9 +376,11 @@ struct UnitCtx {
 // w' = T_end - z for backward, R15).  On success *end = the stage's last
 // kernel end.  On failure the stage's fill state may be partly modified
 // (the unit stops).
-template <bool M>
+// REC (schedule emission, NEXT-1): rec[q] = {stage, comm, start, end} of
+// kernel q of the chain (q = index in the flattened stage-major list).
+template <bool M, bool REC = false>
 __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, UnitSm& U, int s, int k,
-                            int64_t ready, int64_t* end) {
+                            int64_t ready, int64_t* end, int64_t* rec = nullptr) {
 #ifdef K1_STATS
   const long long tp0 = clock64();
 #endif
@@ -446,6 +448,13 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
       const unsigned bad = __ballot_sync(FULL, valid && e > (comm ? w1.chi : w0.chi));
       const int nv = min(32, i1 - i);
       const int f = bad ? __ffs(bad) - 1 : nv;  // kernels placed by this batch
+      if (REC && lane < f) {
+        int64_t* r = rec + (int64_t)(i + lane) * 4;
+        r[0] = s;
+        r[1] = comm;
+        r[2] = e - d;
+        r[3] = e;
+      }
       if (f > 0) {
         ready = __shfl_sync(FULL, e, f - 1);
         const unsigned below = f == 32 ? FULL : ((1u << f) - 1u);
@@ -468,6 +477,13 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
                                        U.bm + (2 * s + 1) * U.CI, U.CI)
                           : place_slow(V0, w0, v & INT64_MAX, ready, U.ci + (2 * s) * U.CI, U.bm + (2 * s) * U.CI,
                                        U.CI);
+    if (REC && ok && (threadIdx.x & 31) == 0) {
+      int64_t* r = rec + (int64_t)i * 4;
+      r[0] = s;
+      r[1] = v < 0;
+      r[2] = ready - (v & INT64_MAX);
+      r[3] = ready;
+    }
 #ifdef K1_STATS
     K1ST(7, clock64() - ts0);
 #endif
@@ -514,8 +530,9 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // mirrored chains on top of forward version kf, started once it is
 // published (or skipped when the forward unit ended with fewer chains).
 // Both stop at the first failure.
-template <bool M>
-__device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, int a, int kf) {
+template <bool M, bool REC = false>
+__device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, int a, int kf, int klimit = 1 << 30,
+                                        int64_t* rec = nullptr) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int stop_at;  // first chain index known to fail (chains >= it are void)
   __shared__ int go;
@@ -581,7 +598,7 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
     // every decision on a value another warp may change is taken from lane
     // 0's read (broadcast), so that the warp never splits before its
     // full-mask collectives
-    for (int k = 0; k < pd.kmax; ++k) {
+    for (int k = 0; k < min(pd.kmax, klimit); ++k) {
       if (k >= __shfl_sync(FULL, *stop, 0)) break;
       int64_t ready = ws;
       if (s > 0) {  // wait for chain k of the upstream stage
@@ -603,7 +620,8 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
         ready = max(endv[(s - 1) * L.KM + k] + c.enc_p2p, ws);
       }
       int64_t end;
-      if (!place_stage<M>(c, pd, X, U, s, k, ready, &end)) {
+      if (!place_stage<M, REC>(c, pd, X, U, s, k, ready, &end,
+                               REC ? rec + (int64_t)k * U.soff[P] * 4 : nullptr)) {
         if (lane == 0) {
           atomicMin(&stop_at, k);
           status[s * L.KM + k] = 2;
@@ -614,13 +632,13 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
         endv[s * L.KM + k] = end;
         __threadfence_block();
         status[s * L.KM + k] = 1;
-        if (s == P - 1) {
+        if (!REC && s == P - 1) {
           if (M) c.tables[pd.inbB + ((int64_t)a * (pd.kmax + 1) + kf) * pd.kmax + k] = end;
           else c.tables[pd.inbF + (int64_t)a * pd.kmax + k] = end;
         }
       }
       __syncwarp();
-      if (!M) {  // publish version k+1 of this stage: the block owner maps after chain k
+      if (!M && !REC) {  // publish version k+1 of this stage: the block owner maps after chain k
         for (int r = 0; r < 2; ++r) {
           const int8_t* own = U.own + (2 * s + r) * U.CI;
           int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
@@ -639,6 +657,7 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
            (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
 #endif
   __syncthreads();
+  if (REC) return;  // emission replay: the build's tables stay as they are
   if (threadIdx.x == 0) {  // chains completed by every stage
     int k = 0;
     while (k < pd.kmax && status[(P - 1) * L.KM + k] == 1) ++k;
@@ -663,6 +682,14 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
       c.tables[pd.bpF + (int64_t)a * pd.kmax + k] = lo + 1;
     }
   }
+}
+
+// Schedule emission (NEXT-1): replay the first klimit chains of one unit
+// (forward: kf < 0; backward on forward version kf) with every kernel's
+// placement recorded; the build's tables and snapshots are only read.
+template <bool M>
+__global__ void k1_record(Cfg c, K1Launch L, int e, int a, int kf, int klimit, int64_t* rec) {
+  k1_unit<M, true>(c, L, e, a, M ? kf : 0, klimit, rec);
 }
 
 // Persistent: every block takes work items in list order (forward units
@@ -754,6 +781,24 @@ static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaS
 
 }  // namespace
 
+
+cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_t* d_rec, cudaStream_t st) {
+  K1Launch L;
+  L.NK = c.nk_max;
+  L.Pmax = c.p;
+  L.CI = (std::max(c.icapc, c.icapm) + 31) / 32;
+  L.KM = std::max(1, c.kmax_all);
+  const size_t smem = k1_smem_bytes(L);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k1_record<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k1_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  if (kf < 0) k1_record<false><<<1, 32 * c.p, smem, st>>>(c, L, e, a, 0, klimit, d_rec);
+  else k1_record<true><<<1, 32 * c.p, smem, st>>>(c, L, e, a, kf, klimit, d_rec);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
   K1Launch L;

@@ -21,7 +21,7 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_explain", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count",
+    "optimus_explain", "optimus_emit_schedule", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count",
     "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
@@ -87,6 +87,7 @@ def lib():
             "optimus_best_plan": [vp, P(ctypes.c_int64), ctypes.c_int32, P(optimus_result), P(ctypes.c_int32)],
             "optimus_debug_template": [vp, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_explain": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
+            "optimus_emit_schedule": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_set_timing": [vp, ctypes.c_int],
@@ -243,6 +244,16 @@ class Ctx:
                 "moves_f": v[8:8 + nf], "moves_b": v[8 + nmb:8 + nmb + nb],
                 "N": v[8 + 2 * nmb:8 + 2 * nmb + m], "c_final": v[8 + 2 * nmb + m:8 + 2 * nmb + 2 * m],
                 "cb_final": v[8 + 2 * nmb + 2 * m:8 + 2 * nmb + 3 * m]}
+
+    def emit_schedule(self, g: int, cap_records: int = 1 << 20, stream=None) -> dict:
+        """In-bubble kernel placements of candidate g (optimus_emit_schedule; NEXT-1)."""
+        import numpy as np
+        out = np.zeros(6 * cap_records, dtype=np.int64)
+        nr = (ctypes.c_size_t * 2)()
+        _check(lib().optimus_emit_schedule(self.h, ctypes.c_uint64(g), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                           out.size, nr, ctypes.c_void_p(_stream(stream))))
+        rec = out[: 6 * (nr[0] + nr[1])].reshape(-1, 6).tolist()
+        return {"fwd_place": rec[: nr[0]], "bwd_place": rec[nr[0]:]}
 
     def debug_template(self, stream=None) -> dict:
         cap = 1 << 24

@@ -374,3 +374,26 @@ def test_explain_matches_oracle_trace(dev, oracle_mod, prob):
             for r in recs:
                 seq.setdefault(r[5], r[0])
             assert x[key] == [seq[k] for k in sorted(seq)], (g, key)
+
+
+@pytest.mark.parametrize("prob", [config_problem(2), config_problem(4)] + [random_problem(s) for s in range(20)],
+                         ids=lambda p: p["name"])
+def test_emit_schedule_matches_oracle_trace(dev, oracle_mod, prob):
+    """optimus_emit_schedule (NEXT-1): every in-bubble kernel placement of the
+    committed moves, record for record, against the oracle's trace."""
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    o = oracle_mod.Oracle(prob)
+    idx = sample_indices(23, min(total, 64), total)
+    lat, aux = o.eval(np.array(idx, dtype=np.uint64), aux=True)
+    aux = np.asarray(aux)
+    picks = [int(idx[i]) for i in np.argsort(-(aux[:, 2] + aux[:, 3]))[:6]] + [int(idx[0])]
+    records = 0
+    for g in picks:
+        x = ctx.emit_schedule(g)
+        t = o.trace(g)
+        assert x["fwd_place"] == t["fwd_place"], g
+        assert x["bwd_place"] == t["bwd_place"], g
+        records += len(x["fwd_place"]) + len(x["bwd_place"])
+    if prob["name"].startswith("c"):
+        assert records > 0  # the paper-shaped configs do move kernels into bubbles
