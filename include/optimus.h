@@ -171,6 +171,14 @@ int optimus_best_plan(const optimus_ctx* c, const int64_t* h_best2_all_ranks, in
  *   `cuda_stream`. */
 int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream);
 
+/* Scheduling efficiency of candidate g (§5.3.2
+ * P:665 Eff_coarse / Eff_fine, reading R-EFF in DESIGN.md §3): host int64
+ * h_out3 = [encoder work inside LLM bubbles with g's moves (fine + coarse),
+ * the same without moves (coarse only), total encoder work], integer ns;
+ * Eff_fine = h_out3[0] / h_out3[2], Eff_coarse = h_out3[1] / h_out3[2].
+ * Synchronises `cuda_stream`. */
+int optimus_efficiency(const optimus_ctx* c, uint64_t g, int64_t* h_out3, void* cuda_stream);
+
 /* Schedule emission for candidate g: every encoder kernel
  * placed into the LLM bubbles by g's committed moves, replayed on the GPU
  * from the build's chain state (§4.2 ScheduleKernels P:347-400; R12, R15).

@@ -306,7 +306,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
   X.o_stats = take(8 * 8);
-  X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN) * 8);
+  X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN + 4) * 8);  // + the efficiency sums
   X.o_rec = take((size_t)std::max(1, X.kmax_all) * std::max(1, X.nk_max) * 4 * 8);
   X.total_bytes = o;
   return OPTIMUS_OK;
@@ -613,6 +613,22 @@ int optimus_explain(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap
   for (int i = 0; i < 2 * n; ++i) h_out[o++] = buf[8 + i];
   for (int i = 0; i < 3 * m; ++i) h_out[o++] = buf[8 + 2 * n + i];
   *len = o;
+  return OPTIMUS_OK;
+}
+
+int optimus_efficiency(const optimus_ctx* c, uint64_t g, int64_t* h_out3, void* cuda_stream) {
+  if (!c || !h_out3) return fail(OPTIMUS_EINVAL, "NULL argument");
+  std::vector<int64_t> x(8 + 2 * kMaxN + 3 * kMaxN);
+  size_t xl = 0;
+  int rc = optimus_explain(c, g, x.data(), x.size(), &xl, cuda_stream);  // leaves its device output in place
+  if (rc != OPTIMUS_OK) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int64_t* d = (int64_t*)(c->ws + c->X.o_explain);
+  unsigned long long* dsum = (unsigned long long*)(d + 8 + 2 * kMaxN + 3 * kMaxN);
+  CK(cudaMemsetAsync(dsum, 0, 3 * 8, st));
+  CK(launch_eff(c->cfg, d, dsum, st));
+  CK(cudaMemcpyAsync(h_out3, dsum, 3 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   return OPTIMUS_OK;
 }
 

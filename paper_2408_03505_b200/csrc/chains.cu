@@ -692,6 +692,56 @@ __global__ void k1_record(Cfg c, K1Launch L, int e, int a, int kf, int klimit, i
   k1_unit<M, true>(c, L, e, a, M ? kf : 0, klimit, rec);
 }
 
+// Scheduling efficiency of one explained candidate (NEXT-1, §5.3.2 P:665,
+// reading R-EFF): xo = optimus_explain's device output.  out (zeroed) gets
+// [in-bubble work with the moves, without them (coarse only), total].
+// Coarse microbatch x of stage s occupies [fill[s][x] - tau[s], fill[s][x])
+// of the plan's GPipe tables (R9); only its part inside the natural bubble
+// [0, w_q) (mirrored [0, T_end - z_q)) counts; moved chains count in full.
+__global__ void k_eff(Cfg c, const int64_t* xo, unsigned long long* out) {
+  const int n = c.n, e = (int)xo[5], m = (int)xo[6];
+  const int64_t* N = xo + 8 + 2 * n;
+  const int64_t* cf = N + m;
+  const int64_t* cb = N + 2 * m;
+  const PlanDesc pd = c.plans[e];
+  const int P = pd.P;
+  __shared__ int64_t tau_f[kMaxP], tau_b[kMaxP];
+  for (int s = threadIdx.x; s < P; s += blockDim.x) {  // stage sums (R8), as the plan tables
+    int64_t tf = 0, tb = 0;
+    for (int b = 0; b < c.nb; ++b) {
+      const int L = c.blayers[b], nl = (s + 1) * L / P - s * L / P;
+      const int idf = enc_list_id(b, pd.ti, c.ntp, 0), idb = enc_list_id(b, pd.ti, c.ntp, 1);
+      int64_t sf = 0, sb = 0;
+      for (int i = c.loff[idf]; i < c.loff[idf + 1]; ++i) sf += c.lns[i];
+      for (int i = c.loff[idb]; i < c.loff[idb + 1]; ++i) sb += c.lns[i];
+      tf += nl * sf;
+      tb += nl * sb;
+    }
+    tau_f[s] = tf;
+    tau_b[s] = tb;
+  }
+  __syncthreads();
+  const int64_t T_end = c.scal[1];
+  const int64_t* fillF = c.tables + pd.preF;
+  const int64_t* fillB = c.tables + pd.preB;
+  auto coarse = [&](const int64_t* fill, int s, int64_t tau, int64_t bubble, int64_t count) {
+    int64_t t = 0;
+    for (int x = 1; x <= count; ++x) {
+      const int64_t hi = fill[s * (n + 1) + x], lo = hi - tau;
+      t += max((int64_t)0, min(hi, bubble) - max(lo, (int64_t)0));
+    }
+    return t;
+  };
+  for (int idx = threadIdx.x; idx < m * P; idx += blockDim.x) {
+    const int j = idx / P, s = idx % P, q = (j / pd.rt) * P + s;
+    const int64_t pre = c.w[q], post = T_end - c.z[q], tf = tau_f[s], tb = tau_b[s];
+    const int64_t fine = (N[j] - cf[j]) * tf + (N[j] - cb[j]) * tb;
+    atomicAdd(&out[0], (unsigned long long)(fine + coarse(fillF, s, tf, pre, cf[j]) + coarse(fillB, s, tb, post, cb[j])));
+    atomicAdd(&out[1], (unsigned long long)(coarse(fillF, s, tf, pre, N[j]) + coarse(fillB, s, tb, post, N[j])));
+    atomicAdd(&out[2], (unsigned long long)(N[j] * (tf + tb)));
+  }
+}
+
 // Persistent: every block takes work items in list order (forward units
 // first, so a backward unit only ever waits on items already taken by
 // running blocks) until the list is exhausted, and counts each finished
@@ -781,6 +831,11 @@ static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaS
 
 }  // namespace
 
+
+cudaError_t launch_eff(const Cfg& c, const int64_t* d_explain, unsigned long long* d_out, cudaStream_t st) {
+  k_eff<<<1, 128, 0, st>>>(c, d_explain, d_out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_t* d_rec, cudaStream_t st) {
   K1Launch L;

@@ -117,6 +117,7 @@ namespace optimus {
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
 cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches);
 cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_t* d_rec, cudaStream_t st);
+cudaError_t launch_eff(const Cfg& c, const int64_t* d_explain, unsigned long long* d_out, cudaStream_t st);
 struct EvalArgs {
   uint64_t begin, end;       // global index range (eval_candidates)
   uint32_t rank, world, block;

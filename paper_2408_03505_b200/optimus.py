@@ -21,7 +21,7 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_explain", "optimus_emit_schedule", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count",
+    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count",
     "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
@@ -88,6 +88,7 @@ def lib():
             "optimus_debug_template": [vp, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_explain": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_emit_schedule": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
+            "optimus_efficiency": [vp, ctypes.c_uint64, P(ctypes.c_int64), vp],
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_set_timing": [vp, ctypes.c_int],
@@ -244,6 +245,12 @@ class Ctx:
                 "moves_f": v[8:8 + nf], "moves_b": v[8 + nmb:8 + nmb + nb],
                 "N": v[8 + 2 * nmb:8 + 2 * nmb + m], "c_final": v[8 + 2 * nmb + m:8 + 2 * nmb + 2 * m],
                 "cb_final": v[8 + 2 * nmb + 2 * m:8 + 2 * nmb + 3 * m]}
+
+    def efficiency(self, g: int, stream=None) -> dict:
+        """Eff_fine / Eff_coarse of candidate g as exact work sums (optimus_efficiency; NEXT-1)."""
+        out = (ctypes.c_int64 * 3)()
+        _check(lib().optimus_efficiency(self.h, ctypes.c_uint64(g), out, ctypes.c_void_p(_stream(stream))))
+        return {"in_bubble_fine": out[0], "in_bubble_coarse": out[1], "total": out[2]}
 
     def emit_schedule(self, g: int, cap_records: int = 1 << 20, stream=None) -> dict:
         """In-bubble kernel placements of candidate g (optimus_emit_schedule; NEXT-1)."""

@@ -397,3 +397,37 @@ def test_emit_schedule_matches_oracle_trace(dev, oracle_mod, prob):
         records += len(x["fwd_place"]) + len(x["bwd_place"])
     if prob["name"].startswith("c"):
         assert records > 0  # the paper-shaped configs do move kernels into bubbles
+
+
+@pytest.mark.parametrize("prob", [config_problem(2), config_problem(4)] + [random_problem(s) for s in range(16)],
+                         ids=lambda p: p["name"])
+def test_efficiency_matches_oracle(dev, oracle_mod, prob):
+    """optimus_efficiency (NEXT-1, R-EFF) against oracle/eff.py, exact integers."""
+    from oracle import eff as E
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    o = oracle_mod.Oracle(prob)
+    for g in sample_indices(29, min(total, 12), total):
+        assert ctx.efficiency(int(g)) == E.efficiency(prob, int(g), o), g
+
+
+def test_efficiency_trend_table7(dev):
+    """Table 7's direction: with the global batch fixed, fewer
+    microbatches per LLM pipeline give higher Eff_coarse and Eff_fine for the
+    chosen schedule.  The paper's setting has LLM PP = 8, so the
+    PP-8 config 3 stands in at N_mb = 32, 24, 16."""
+    torch = dev
+    effs = []
+    for n_mb in (32, 24, 16):
+        prob = config_problem(3, n_mb=n_mb)
+        ctx = _load(prob)
+        total, _ = ctx.num_candidates()
+        b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(0, total, b2)
+        torch.cuda.synchronize()
+        r = ctx.efficiency(int(b2[1].item()))
+        effs.append((r["in_bubble_coarse"] / r["total"], r["in_bubble_fine"] / r["total"]))
+    print("Eff (coarse, fine) at N_mb 32/24/16:", effs)
+    for (c0, f0), (c1, f1) in zip(effs, effs[1:]):
+        assert c1 >= c0 and f1 >= f0
+    assert all(f >= c for c, f in effs)
