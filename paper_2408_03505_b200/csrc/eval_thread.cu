@@ -21,7 +21,10 @@
 namespace optimus {
 namespace {
 
-constexpr int kTThreads = 128;
+#ifndef K2T_THREADS
+#define K2T_THREADS 128
+#endif
+constexpr int kTThreads = K2T_THREADS;
 #ifndef K2T_RUN
 #define K2T_RUN 16
 #endif
