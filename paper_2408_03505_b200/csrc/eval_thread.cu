@@ -168,16 +168,6 @@ __device__ bool tnext(int m, TS& s) {
   return true;
 }
 
-// first slot (1-based) whose deadline G is >= v; n+1 if none
-__device__ __forceinline__ int first_ge(const int64_t* G, int n, int64_t v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (G[mid] >= v) hi = mid; else lo = mid + 1;
-  }
-  return lo + 1;
-}
-
 // Forward dependency shift (R10).  Slot i needs sorted pre position
 // need_i = i - q(i), q(i) = #{thresholds <= i} (the M committed ones plus
 // the trial one bp; n+1 = never); INF if some need_i > sum c; else the max
