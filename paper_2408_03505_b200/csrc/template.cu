@@ -146,7 +146,6 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
       const int64_t t = dep == 0x7FFF ? tprev : max(tprev, de + ((op >> 31) ? pp2p : 0));
       const int64_t e = t + (fwd ? dur_f : dur_b);
       endv[self] = e;
-      if (record) c.opstart[(int64_t)s * nops + pos] = t;
       tprev = e;
       ++pos;
       op = nxt;
@@ -168,16 +167,21 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
       if (__any_sync(0xffffffffu, tprev > bound)) return -3;
     }
   }
-  if (record) {  // F_i / B_i (R4): start of F / end of B of (stage 0, chunk 0, microbatch i)
+  if (record) {  // op starts from the ends; F_i / B_i (R4): start of F / end of B of (stage 0, chunk 0, i)
     __syncwarp();
-    for (int pos = lane; pos < nops; pos += 32) {
-      int self, dep, fwd, cross;
-      op_slots(p, v, n, 0, pos, W[0], vch, vmb, self, dep, fwd, cross);
-      const int mb = self % n, ch = (self / n) % v;
-      if (ch == 0) {
-        const int64_t t = c.opstart[pos];
-        if (fwd) c.F[mb] = t;
-        else c.B[mb] = t + dur_b;
+    for (int idx = lane; idx < p * nops; idx += 32) {
+      const int st = idx / nops, pos = idx - st * nops;
+      const uint32_t op = optab[(size_t)st * (nops + 1) + pos];
+      const bool fwd = (op >> 30) & 1;
+      const int64_t e = endv[op & 0x7FFF], t = e - (fwd ? dur_f : dur_b);
+      c.opstart[idx] = t;
+      if (st == 0) {
+        const int us = (int)(op & 0x7FFF) - (int)(op & 0x7FFF) / (S + 1);  // unpadded slot
+        const int mb = us % n, ch = (us / n) % v;
+        if (ch == 0) {
+          if (fwd) c.F[mb] = t;
+          else c.B[mb] = e;
+        }
       }
     }
   }
