@@ -155,7 +155,7 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
     if ((round & 7) == 7) {  // periodic checks: done, deadlock, default span exceeded
       const unsigned left = __ballot_sync(0xffffffffu, pos < nops), any = __ballot_sync(0xffffffffu, prog);
 #ifdef K0_STATS
-      if (!left && lane == 0 && record) printf("K0ROUNDS %d\n", round);
+      if (!left && lane == 0) printf("K0ROUNDS %d rec=%d\n", round, (int)record);
 #endif
       if (!left) break;
       if (!any) return -1;  // no progress in 8 rounds: deadlock
