@@ -91,7 +91,7 @@ def _taus(prob, plan, bwd):
 
 
 @MODES
-@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p["name"])
+@pytest.mark.parametrize("prob", SMALL + [config_problem(5, 16)], ids=lambda p: p["name"])
 def test_full_space_parity(dev, oracle_mod, prob, mode):
     torch = dev
     ctx = _load(prob, mode)
