@@ -61,7 +61,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_partials, o_counter, o_stats, o_explain, o_rec, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_rec, total_bytes;
   int grid;
 };
 
@@ -301,6 +301,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_bfill = take((size_t)X.n_slots * (X.icapc + X.icapm) * 8);
   X.o_k1flags = take((size_t)X.n_flags * 4);
   X.o_sync = take(64 + (size_t)kMaxE * (4 + 8));  // k1next (+ development probes), pdone[E], pclaim[E]
+  X.o_iv = take((size_t)X.p * 8 * (8 + 4));          // k0_intervals block exchange
   X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
@@ -377,6 +378,8 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.pdone = (int32_t*)(ws + X.o_sync + 64);
   c.pclaim = (unsigned long long*)(ws + X.o_sync + 64 + (size_t)kMaxE * 4);
   c.k2order = (const int32_t*)(ws + X.o_k2order);
+  c.ivagg = (unsigned long long*)(ws + X.o_iv);
+  c.ivflag = (int32_t*)(ws + X.o_iv + (size_t)X.p * 8 * 8);
   c.n_k2order = (int32_t)X.k2order.size();
   return c;
 }
@@ -454,6 +457,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 64 + (size_t)kMaxE * 12, st);  // K1/K2 counters
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_iv, 0, (size_t)X.p * 8 * 12, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);

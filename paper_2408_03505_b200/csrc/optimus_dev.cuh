@@ -65,6 +65,8 @@ struct Cfg {
   int64_t* comm_lo;       // [p][icapm]
   int64_t* comm_hi;       // [p][icapm]
   int64_t* bmax;          // [p][2 resources][2 orientations][ci_n]: max base capacity (hi - lo) per 32-interval block
+  unsigned long long* ivagg;  // [p][8] k0_intervals per-block interval counts (compute | comm << 32)
+  int32_t* ivflag;            // [p][8] ... published (zeroed by k0_final)
   int32_t* bestw;         // [p] K0 warm-up search: smallest successful w per stage
   int64_t* k0res;         // [1 + k0_trials] K0 wave: span of each simulation, -1 if it deadlocks
   // plans + tables (K1)

@@ -52,6 +52,7 @@ __device__ __forceinline__ int64_t warp_max64(int64_t v) {
 // odd (2vn+1, nops+1) so that the 32 lanes (stages) hit distinct banks.
 constexpr int kNone = 0xFFFF;
 constexpr int kSimWarps = 8;  // simulations per block
+constexpr int kIvBlocks = 8;  // k0_intervals blocks per LLM stage (capi sizes the exchange for 8)
 
 __host__ __device__ __forceinline__ size_t k0_vtab_bytes(int n, int v) { return ((size_t)4 * n * v + 15) & ~size_t(15); }
 __host__ __device__ __forceinline__ size_t k0_warp_bytes(int p, int v, int n) {
@@ -269,6 +270,8 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   for (int i = threadIdx.x; i < c.nflags; i += blockDim.x) c.k1flags[i] = 0;  // K1 progress flags
   for (int i = threadIdx.x; i < c.E; i += blockDim.x) c.pdone[i] = 0;        // K1 -> K2 plan completion
   if (threadIdx.x == 0) *c.k1next = 0;                                         // K1 work counter
+  for (int i = threadIdx.x; i < c.p * kIvBlocks; i += blockDim.x) c.ivflag[i] = 0;  // k0_intervals exchange
+  for (int i = threadIdx.x; i < c.p * 4 * c.ci_n; i += blockDim.x) c.bmax[i] = kNegInf;
 #ifdef PDL_PROBE
   if (threadIdx.x == 0) {
     unsigned long long* probe = reinterpret_cast<unsigned long long*>(c.k1next) + 1;
@@ -452,12 +455,14 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   using Scan = cub::BlockScan<unsigned long long, kIvThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ LTab Lf, Lb;
-  __shared__ int run_c, run_m;
+  __shared__ int run_c, run_m, head_m, tot_c, tot_m;
   // dynamic: [nops + 1] kernel offset of each op, [nops] op is forward, then
   // (8-aligned) bmx[4][ci_n]: the per-block capacity maxima being built
   extern __shared__ __align__(16) int opoff[];
   if (c.scal[2] == 0) return;     // template failed (deadlock): nothing to emit
-  const int s = blockIdx.x, warp = threadIdx.x >> 5;
+  // kIvBlocks blocks per stage, each a contiguous share of its kernels; the
+  // blocks of a stage exchange their interval counts through ivagg/ivflag
+  const int s = blockIdx.x / kIvBlocks, bi = blockIdx.x % kIvBlocks, warp = threadIdx.x >> 5;
   const int p = c.p, v = c.v, n = c.n, nops = c.nops, lc = c.lc;
   const int Ws = c.W[s];
   uint8_t* opfwd = reinterpret_cast<uint8_t*>(opoff + nops + 1);
@@ -468,14 +473,20 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   if (warp == 1) load_ltab(c, 1, Lb);
   for (int q = threadIdx.x; q < nops; q += blockDim.x) opfwd[q] = (uint8_t)op_at(p, v, n, Ws, q).fwd;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (nops <= kIvThreads) {  // kernel offset of each op: one block scan
+    const int q = threadIdx.x;
+    const unsigned long long x = q < nops ? (unsigned long long)(lc * (opfwd[q] ? Lf.len : Lb.len)) : 0ull;
+    unsigned long long ex, all;
+    Scan(tmp).ExclusiveSum(x, ex, all);
+    if (q < nops) opoff[q] = (int)ex;
+    if (q == 0) opoff[nops] = (int)all;
+  } else if (threadIdx.x == 0) {
     int acc = 0;
     for (int q = 0; q < nops; ++q) {
       opoff[q] = acc;
       acc += lc * (opfwd[q] ? Lf.len : Lb.len);
     }
     opoff[nops] = acc;
-    run_c = run_m = 0;
   }
   __syncthreads();
   const int K = opoff[nops];
@@ -483,7 +494,7 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   // first op is always a forward, last always a backward
   const int64_t w = ost[0] + Lf.koff[Lf.firstc];
   const int64_t z = ost[nops - 1] + (int64_t)(lc - 1) * Lb.sum + Lb.koff[Lb.lastc] + Lb.dur[Lb.lastc];
-  if (threadIdx.x == 0) { c.w[s] = w; c.z[s] = z; }
+  if (threadIdx.x == 0 && bi == 0) { c.w[s] = w; c.z[s] = z; }
   int64_t* clo = c.comp_lo + (int64_t)s * c.icapc;
   int64_t* chi = c.comp_hi + (int64_t)s * c.icapc;
   int64_t* mlo = c.comm_lo + (int64_t)s * c.icapm;
@@ -493,10 +504,13 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
     int64_t first_comm = kInf;
     if (Lf.firstm >= 0) first_comm = ost[0] + Lf.koff[Lf.firstm];
     const int64_t hi = min(first_comm, z);  // (both lists have comm or neither: validated)
-    if (hi > w) { mlo[0] = w; mhi[0] = hi; run_m = 1; }
+    head_m = hi > w;
+    if (hi > w && bi == 0) { mlo[0] = w; mhi[0] = hi; }
   }
   __syncthreads();
-  const int C = (K + kIvThreads - 1) / kIvThreads, k0 = min(K, (int)threadIdx.x * C), k1 = min(K, k0 + C);
+  const int Kb0 = (int)((int64_t)K * bi / kIvBlocks), Kb1 = (int)((int64_t)K * (bi + 1) / kIvBlocks);
+  const int C = (Kb1 - Kb0 + kIvThreads - 1) / kIvThreads;
+  const int k0 = min(Kb1, Kb0 + (int)threadIdx.x * C), k1 = min(Kb1, k0 + C);
   int q0 = 0;
   {  // op of kernel k0
     int lo = 0, hi = nops - 1;
@@ -515,16 +529,36 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
   }
   unsigned long long off, tot;
   Scan(tmp).ExclusiveSum(cnt, off, tot);
+  if (threadIdx.x == 0) {  // publish this block's counts, then gather the stage's
+    unsigned long long* agg = c.ivagg + (int64_t)s * kIvBlocks;
+    int* flag = c.ivflag + (int64_t)s * kIvBlocks;
+    agg[bi] = tot;
+    __threadfence();
+    atomicExch(&flag[bi], 1);
+    unsigned long long pre = 0, all = 0;
+    for (int b = 0; b < kIvBlocks; ++b) {
+      while (*(volatile int*)&flag[b] == 0) __nanosleep(64);
+      __threadfence();
+      const unsigned long long x = *(volatile unsigned long long*)&agg[b];
+      all += x;
+      if (b < bi) pre += x;
+    }
+    run_c = (int)(pre & 0xffffffffu);
+    run_m = head_m + (int)(pre >> 32);
+    tot_c = (int)(all & 0xffffffffu);
+    tot_m = head_m + (int)(all >> 32);
+  }
+  __syncthreads();
   int oc = run_c + (int)(off & 0xffffffffu), om = run_m + (int)(off >> 32);
   // per 32-interval block, the largest base capacity hi - lo, in time order
   // (orientation 0) and in mirrored order (1, interval i' = count-1-i): no
   // kernel longer than it fits anywhere in the block (K1 skips such blocks)
-  const int nc = run_c + (int)(tot & 0xffffffffu), nm = run_m + (int)(tot >> 32);
+  const int nc = tot_c, nm = tot_m;
   auto note = [&](int r, int idx, int count, int64_t cap) {
     atomicMax(&bmx[(r * 2 + 0) * CI + (idx >> 5)], (long long)cap);
     atomicMax(&bmx[(r * 2 + 1) * CI + ((count - 1 - idx) >> 5)], (long long)cap);
   };
-  if (threadIdx.x == 0 && run_m == 1) note(1, 0, nm, mhi[0] - mlo[0]);  // the head comm-free piece
+  if (threadIdx.x == 0 && bi == 0 && head_m) note(1, 0, nm, mhi[0] - mlo[0]);  // the head comm-free piece
   for (int kk = k0, q = q0; kk < k1; ++kk) {
     while (kk >= opoff[q + 1]) ++q;
     int64_t lo, hi;
@@ -533,8 +567,9 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
     if (g == 2) { mlo[om] = lo; mhi[om] = hi; note(1, om, nm, hi - lo); ++om; }
   }
   __syncthreads();
-  if (threadIdx.x == 0) { c.ncomp[s] = nc; c.ncomm[s] = nm; }
-  for (int i = threadIdx.x; i < 4 * CI; i += blockDim.x) c.bmax[(int64_t)s * 4 * CI + i] = bmx[i];
+  if (threadIdx.x == 0 && bi == 0) { c.ncomp[s] = nc; c.ncomm[s] = nm; }
+  for (int i = threadIdx.x; i < 4 * CI; i += blockDim.x)  // (c.bmax starts at -inf: k0_final)
+    if (bmx[i] != kNegInf) atomicMax(reinterpret_cast<long long*>(&c.bmax[(int64_t)s * 4 * CI + i]), bmx[i]);
 }
 
 }  // namespace
@@ -553,7 +588,7 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
   const int nsim = 1 + c.k0_trials;
   k0_wave<<<(nsim + wpb - 1) / wpb, 32 * kSimWarps, smem, st>>>(c, nsim, wpb);
   k0_final<<<1, 32 * kSimWarps, smem, st>>>(c, wpb);
-  k0_intervals<<<c.p, kIvThreads, k0_iv_smem_bytes(c.nops, c.ci_n), st>>>(c);
+  k0_intervals<<<c.p * kIvBlocks, kIvThreads, k0_iv_smem_bytes(c.nops, c.ci_n), st>>>(c);
   if (launches) *launches += 3;
   return cudaGetLastError();
 }
