@@ -185,7 +185,11 @@ def cpu_baseline(ctx, prob, torch):
     ctx.eval_indices(di, b2, lat_out=lat)
     torch.cuda.synchronize()
     mism = int((lat.cpu().numpy() != ref).sum())
-    return ({"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    one = idx[:max(200, min(count, int(rate / cores * 2.0)))]  # ~2 s on one core (T and 1 thread)
+    t0 = time.perf_counter()
+    orc.eval(one, threads=1)
+    rate1 = len(one) / (time.perf_counter() - t0)
+    return ({"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "value_1thread": rate1,
              "sample": f"{count} seeded splitmix64 indices of the {orc.total}-candidate space, oracle C++ -O2, "
                        f"{cores} threads, {dt:.1f} s"},
             {"sample": count, "mismatches": mism})

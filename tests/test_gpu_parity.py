@@ -109,6 +109,36 @@ def test_full_space_parity(dev, oracle_mod, prob, mode):
     assert (int(b[0]), int(b[1])) == (int(ref.min()), int(np.argmin(ref)))
 
 
+@pytest.fixture(scope="module")
+def config4_oracle_lat(oracle_mod):
+    """Oracle lat of every one of config 4's 5,845,247 candidates (SURVEY §8(d):
+    full-space oracle parity for configs 1, 2 and 4; ~30 s on 16 host cores)."""
+    prob = config_problem(4)
+    o = oracle_mod.Oracle(prob)
+    return prob, o.eval_range(0, o.total, threads=THREADS)
+
+
+@MODES
+def test_full_space_parity_config4(dev, config4_oracle_lat, mode):
+    """The bench workload, every candidate: the lat dump of the launch bench.py
+    times (eval_candidates over the whole range) equals the oracle element by
+    element, and the argmin equals the oracle's first minimum."""
+    torch = dev
+    prob, ref = config4_oracle_lat
+    ctx = _load(prob, mode)
+    total, _ = ctx.num_candidates()
+    assert total == len(ref) == 5845247
+    lat = torch.full((total,), -7, dtype=torch.int64, device="cuda")
+    best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, best2, lat_out=lat)
+    torch.cuda.synchronize()
+    got = lat.cpu().numpy()
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first g={bad[:5].tolist()}"
+    b = best2.cpu().numpy()
+    assert (int(b[0]), int(b[1])) == (int(ref.min()), int(np.argmin(ref)))
+
+
 @MODES
 @pytest.mark.parametrize("prob", BIG, ids=lambda p: p["name"])
 def test_sampled_parity_full_size(dev, oracle_mod, prob, mode):
