@@ -29,6 +29,17 @@ constexpr int kTThreads = K2T_THREADS;
 #define K2T_RUN 16
 #endif
 constexpr int kTRun = K2T_RUN;            // most consecutive candidates per thread and claim
+#ifndef K2T_MINRUN
+#define K2T_MINRUN 1
+#endif
+constexpr int kTMinRun = K2T_MINRUN;      // fewest consecutive candidates per thread and claim
+#ifndef K2T_GSS
+#define K2T_GSS 1
+#endif
+#ifndef K2T_GSS_DEN
+#define K2T_GSS_DEN 1
+#endif
+constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remaining * GSS / (GSS_DEN * warps), capped
 #ifndef K2T_MINB
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
@@ -646,7 +657,7 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
             }
             const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
             const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
-            const unsigned long long tk = min(32ull * kTRun, max(32ull, rem / nwarps / 32 * 32));
+            const unsigned long long tk = min(32ull * kTRun, max(32ull * kTMinRun, rem * kTGss / (kTGssDen * nwarps) / 32 * 32));
             const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
             if (st0 < pn[e2]) { e = e2; chunk = st0; take = tk; break; }
             pst[e2] = 2;
