@@ -122,3 +122,14 @@ def test_rank_share_tiles(L):
     from paper_2408_03505_b200.dist import rank_share
     for n, world, block in [(20703, 8, 4096), (5845247, 8, 4096), (1000, 3, 64), (64, 4, 64), (0, 2, 64)]:
         assert sum(rank_share(0, n, r, world, block) for r in range(world)) == n
+
+
+@pytest.mark.parametrize("n_mb", [64, 128])
+def test_config5_wide_sweep_points_refused(L, oracle_mod, n_mb):
+    """Config 5's sweep points N_mb = 64 and 128 exceed the GPU path's n <= 32
+    (round-2 gap): load refuses them with ERANGE naming the limit,
+    while the oracle covers them (its plan totals match SURVEY Appendix A)."""
+    prob = config_problem(5, n_mb)
+    code, msg = _err(L, prob)
+    assert code == -5 and "exceeds the supported 32" in msg
+    assert oracle_mod.plans(prob)["total"] == {64: 2213201944, 128: 357426663480}[n_mb]
