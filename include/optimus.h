@@ -71,7 +71,7 @@ typedef struct {
   int32_t bytes_per_param;    /* k in MEM_model (6 for bf16 params+fp32 grads)   */
   optimus_plan llm;           /* LLM (DP, PP, TP, V); interleaved 1F1B needs N_mb % PP == 0 */
   int32_t llm_layers;         /* multiple of PP * V                                      */
-  int32_t n_mb;               /* N_mb, microbatches per LLM pipeline             */
+  int32_t n_mb;               /* N_mb, microbatches per LLM pipeline; <= 128 (ERANGE) */
   int32_t warmup_policy;      /* 0 = Megatron default warm-up, 1 = adjusted (§4.3) */
   optimus_seq llm_fwd_layer;  /* one LLM layer forward, >= 1 compute, <= 256 kernels     */
   optimus_seq llm_bwd_layer;  /* one LLM layer backward, >= 1 compute, <= 256 kernels    */
@@ -209,7 +209,10 @@ int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t*
 
 /* K2 variant used by the eval calls: 1 (default) = one candidate per thread
  * (eval_thread.cu), 0 = one candidate per warp (eval.cu).  Both compute the
- * same lat for every candidate (bit-exact); they differ only in speed. */
+ * same lat for every candidate (bit-exact); they differ only in speed.
+ * Mode 0 puts one LLM slot on each lane and takes N_mb <= 32: the eval calls
+ * return OPTIMUS_ERANGE for mode 0 at larger N_mb.  Mode 1 takes N_mb <= 128
+ * (a compact per-thread scratch for N_mb <= 32, a wide one above). */
 int optimus_set_eval_mode(optimus_ctx* c, int mode);
 
 /* Per-kernel timing: when on, the library records CUDA events around each

@@ -190,9 +190,12 @@ int prepare(const optimus_problem* pb, Prep& X) {
                        (size_t)X.p * (X.n + 1) * 12 + 64;
     if (per > 200 * 1024) return fail(OPTIMUS_ERANGE, "K1 shared-memory footprint %zu B exceeds 200 KB", per);
   }
-  X.binom.assign((kMaxN + 1) * (kMaxN + 1), 0);
-  for (int a = 0; a <= kMaxN; ++a)
-    for (int b = 0; b <= kMaxN; ++b) X.binom[a * (kMaxN + 1) + b] = binom_sat(a, b);
+  {  // row stride 33 for n <= 32 (both K2 modes), 129 for the wide instance
+    const int S = X.n <= kMaxNWarp ? kMaxNWarp + 1 : kMaxN + 1;
+    X.binom.assign((size_t)S * S, 0);
+    for (int a = 0; a < S; ++a)
+      for (int b = 0; b < S; ++b) X.binom[a * S + b] = binom_sat(a, b);
+  }
 
   // model planner: encoder plans (P | PP_llm, T | TP_llm), memory prune (R17, R19)
   int64_t phi_enc = 0;
@@ -429,14 +432,15 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = sms;
   {  // occupancy-derived persistent grids, computed once per process and SM count
-    static int cached_sms = -1, cached_grid = 0, cached_grid_thread = 0;
+    static int cached_sms = -1, cached_grid = 0, cached_grid_thread = 0, cached_grid_wide = 0;
     if (cached_sms != sms) {
       cached_grid = std::min(4096, eval_grid(sms));
-      cached_grid_thread = std::min(4096, eval_thread_grid(sms));
+      cached_grid_thread = std::min(4096, eval_thread_grid(sms, false));
+      cached_grid_wide = std::min(cached_grid_thread, eval_thread_grid(sms, true));
       cached_sms = sms;
     }
     c->grid = cached_grid;
-    c->grid_thread = cached_grid_thread;
+    c->grid_thread = X.n <= kMaxNWarp ? cached_grid_thread : cached_grid_wide;
   }
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
@@ -505,6 +509,8 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.counter = (unsigned long long*)(c->ws + c->X.o_counter);
   a.total = c->X.total;
   a.mode = c->mode;
+  if (c->mode == 0 && c->X.n > kMaxNWarp)
+    return fail(OPTIMUS_ERANGE, "eval mode 0 (one lane per slot) takes n_mb <= %d; n_mb = %d needs mode 1", kMaxNWarp, c->X.n);
   a.grid = c->mode == 1 ? c->grid_thread : c->grid;
   a.stats = (unsigned long long*)(c->ws + c->X.o_stats);
   a.pclaim = c->cfg.pclaim;

@@ -91,7 +91,7 @@ __device__ int unrank_lane(const Cfg& c, int n, int m, uint64_t rank) {
     const int parts = m - j;
     int x = 1;
     for (; x <= rem - (parts - 1); ++x) {
-      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (kMaxN + 1) + (parts - 2)]);
+      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (kMaxNWarp + 1) + (parts - 2)]);
       if (rank < cnt) break;
       rank -= cnt;
     }
@@ -167,7 +167,7 @@ struct Comp {
 };
 
 __device__ void comp_init(const Cfg& c, const PlanCache& pc, int N, Comp& s) {
-  __shared__ int hist_sm[kEvalThreads / 32][kMaxN + 2];
+  __shared__ int hist_sm[kEvalThreads / 32][kMaxNWarp + 2];
   const int lane = threadIdx.x & 31, np1 = c.n + 1;
   int* sm = hist_sm[threadIdx.x >> 5];
   const bool isp = lane < pc.m;
@@ -220,7 +220,7 @@ __device__ bool comp_next(const Cfg& c, const PlanCache& pc, Comp& s) {
 // One candidate: returns lat (uniform across the warp).
 __device__ int64_t eval_one(const Cfg& c, const PlanCache& pc, const Comp& base, int64_t G, int64_t D, int64_t T_end,
                             Stats& st) {
-  __shared__ int ord_sm[kEvalThreads / 32][kMaxN + 2];
+  __shared__ int ord_sm[kEvalThreads / 32][kMaxNWarp + 2];
   const int lane = threadIdx.x & 31;
   const int n = c.n, m = pc.m, kmax = pc.kmax, np1 = n + 1;
   const bool isp = lane < m;

@@ -43,11 +43,13 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #ifndef K2T_MINB
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
-constexpr int kTStrideW = 65;             // per-thread scratch: 65 words (odd)
-constexpr int kTStride = kTStrideW * 4;   // = 260 bytes
+// per-thread scratch: B = 32 (n, m <= 32): 65 words (odd) = 260 bytes;
+// B = 128 (wide, n, m <= 128): 257 words = 1028 bytes
+template <int B>
+__host__ __device__ constexpr int tstride() { return (8 * B + 4) | 4; }
 
-// Per-thread scratch (bytes 0..255).  The three phases of one candidate use
-// disjoint live sets, so bytes 64..255 are shared between them:
+// Per-thread scratch (bytes 0..8B-1, B = 32 shown).  The three phases of one
+// candidate use disjoint live sets, so bytes 2B..8B-1 are shared between them:
 //   all      N[0..31] c[32..63]
 //   forward  cnt[64..97] thr[98..129]
 //   ordering seen[64..95] kb[96..127] mvj[128..159] mvk[160..191] own[192..223] rk[224..255]
@@ -67,20 +69,21 @@ struct TS {
   uint8_t* mvk;   //                                                  chain index
 };
 
+template <int B>
 __device__ __forceinline__ TS ts_at(unsigned char* b) {
   TS s;
   s.N = b;
-  s.c = b + 32;
-  s.cnt = b + 64;
-  s.thr = b + 98;
-  s.seen = b + 64;
-  s.kb = b + 96;
-  s.mvj = b + 128;
-  s.mvk = b + 160;
-  s.own = b + 192;
-  s.rk = b + 224;
-  s.cb = b + 64;
-  s.Qcb = b + 96;
+  s.c = b + B;
+  s.cnt = b + 2 * B;
+  s.thr = b + 3 * B + 2;
+  s.seen = b + 2 * B;
+  s.kb = b + 3 * B;
+  s.mvj = b + 4 * B;
+  s.mvk = b + 5 * B;
+  s.own = b + 6 * B;
+  s.rk = b + 7 * B;
+  s.cb = b + 2 * B;
+  s.Qcb = b + 3 * B;
   return s;
 }
 
@@ -138,14 +141,15 @@ __device__ int tfind_plan(const Cfg& c, uint64_t g) {
   return -1;
 }
 
-// Lexicographic unranking (R17) into N[0..m).
+// Lexicographic unranking (R17) into N[0..m); binomial rows of stride B + 1.
+template <int B>
 __device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
   int rem = n;
   for (int j = 0; j < m - 1; ++j) {
     const int parts = m - j;
     int x = 1;
     for (; x <= rem - (parts - 1); ++x) {
-      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (kMaxN + 1) + (parts - 2)]);
+      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (B + 1) + (parts - 2)]);
       if (rank < cnt) break;
       rank -= cnt;
     }
@@ -403,8 +407,8 @@ struct TStats {
 // decode a findCritical key: pipeline js and its DEV value (-inf, js = -1 if none)
 __device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev, const uint8_t* cnt8, uint32_t best,
                                               int& js) {
-  if (best < 32u) { js = -1; return kNegInf; }
-  js = 31 - (int)(best & 31u);
+  if (best < 128u) { js = -1; return kNegInf; }
+  js = 127 - (int)(best & 127u);
   return __ldg(&dev[row_of(p, js) * p.np1 + cnt8[js]]);
 }
 
@@ -419,7 +423,7 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, 
   int base = 0, r = 0;
 #pragma unroll 4
   for (int j = 0; j < m; ++j) {
-    best = max(best, (__ldg(&key[base + cnt8[j]]) << 5) | (uint32_t)(31 - j));
+    best = max(best, (__ldg(&key[base + cnt8[j]]) << 7) | (uint32_t)(127 - j));
     if (++r == rt) { r = 0; base += np1; }
   }
   return crit_value(p, dev, cnt8, best, js);
@@ -445,9 +449,9 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
       s.c[j] = (uint8_t)Nj;
       s.cnt[Nj] += 1;
       maxN = max(maxN, Nj);
-      const uint32_t lo = (uint32_t)(31 - j);
-      kf0 = max(kf0, (__ldg(&p.keyF[base + Nj]) << 5) | lo);
-      kb0 = max(kb0, (__ldg(&p.keyB[base + Nj]) << 5) | lo);
+      const uint32_t lo = (uint32_t)(127 - j);
+      kf0 = max(kf0, (__ldg(&p.keyF[base + Nj]) << 7) | lo);
+      kb0 = max(kb0, (__ldg(&p.keyB[base + Nj]) << 7) | lo);
       if (++r == rt) { r = 0; base += p.np1; }
     }
   }
@@ -574,10 +578,10 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
   if (lat < bl || (lat == bl && g < bg)) { bl = lat; bg = g; }
 }
 
-template <bool EXPLICIT>
-__global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, EvalArgs A) {
+template <bool EXPLICIT, int B>
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : 1) k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  __shared__ int64_t G[kMaxN], D[kMaxN];
+  __shared__ int64_t G[B], D[B];
   __shared__ long long bl_sm[kTThreads / 32];
   __shared__ unsigned long long bg_sm[kTThreads / 32];
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
@@ -605,7 +609,7 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
     atomicMin(reinterpret_cast<unsigned long long*>(c.k1next) + 3, t);
   }
 #endif
-  TS s = ts_at(tsm + (size_t)threadIdx.x * kTStride);
+  TS s = ts_at<B>(tsm + (size_t)threadIdx.x * tstride<B>());
   TPlan p;
   p.e = -1;
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
@@ -624,7 +628,7 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
         const int e = tfind_plan(c, g);
         if (e >= 0) {
           if (e != p.e) tplan(c, e, p);
-          tunrank(c, n, p.m, g - p.first, s);
+          tunrank<B>(c, n, p.m, g - p.first, s);
           const int64_t lat = teval(c, p, G, D, T_end, s, st);
           if (A.lat_out) A.lat_out[i] = lat;
           tbetter(lat, g, bl, bg);
@@ -679,7 +683,7 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
         if (q == p0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
           const uint64_t rb = q / A.block;
           g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
-          tunrank(c, n, p.m, g - p.first, s);
+          tunrank<B>(c, n, p.m, g - p.first, s);
         } else {
           ++g;
           tnext(p.m, s);
@@ -717,9 +721,10 @@ __global__ void __launch_bounds__(kTThreads, K2T_MINB) k2_eval_thread(Cfg c, Eva
 // out: [0] lat, [1] Df, [2] Db, [3] forward moves, [4] backward moves,
 // [5] plan, [6] m, [7] n, [8, 8+n) forward move pipelines, [8+n, 8+2n)
 // backward ones, then N[m], c_final[m], cb_final[m].  One thread works.
+template <int B>
 __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64_t* out) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  __shared__ int64_t G[kMaxN], D[kMaxN];
+  __shared__ int64_t G[B], D[B];
   const int n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -733,8 +738,8 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   if (e < 0) return;
   TPlan p;
   tplan(c, e, p);
-  TS s = ts_at(tsm);
-  tunrank(c, n, p.m, g - p.first, s);
+  TS s = ts_at<B>(tsm);
+  tunrank<B>(c, n, p.m, g - p.first, s);
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
   out[5] = e;
   out[6] = p.m;
@@ -744,25 +749,46 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
 
 }  // namespace
 
-int eval_thread_grid(int sms) {
-  int per = 0;
-  cudaFuncSetAttribute(k2_eval_thread<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
-  cudaFuncSetAttribute(k2_eval_thread<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+template <int B>
+static void k2t_attrs() {
+  constexpr int smem = kTThreads * tstride<B>();
+  cudaFuncSetAttribute(k2_eval_thread<false, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_eval_thread<false, B>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_eval_thread<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTThreads * kTStride);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false>, kTThreads, kTThreads * kTStride);
+  cudaFuncSetAttribute(k2_eval_thread<true, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_eval_thread<true, B>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(k2_explain<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+// persistent grid of the compact (n <= 32) or wide (n <= 128) instance
+int eval_thread_grid(int sms, bool wide) {
+  int per = 0;
+  if (wide) {
+    k2t_attrs<kMaxN>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, kMaxN>, kTThreads,
+                                                  kTThreads * tstride<kMaxN>());
+  } else {
+    k2t_attrs<kMaxNWarp>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, kMaxNWarp>, kTThreads,
+                                                  kTThreads * tstride<kMaxNWarp>());
+  }
   return max(1, per) * sms;
 }
 
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
-  k2_explain<<<1, kTThreads, (size_t)kTThreads * kTStride, st>>>(c, g, d_out);
+  if (c.n <= kMaxNWarp)
+    k2_explain<kMaxNWarp><<<1, kTThreads, (size_t)kTThreads * tstride<kMaxNWarp>(), st>>>(c, g, d_out);
+  else
+    k2_explain<kMaxN><<<1, kTThreads, (size_t)kTThreads * tstride<kMaxN>(), st>>>(c, g, d_out);
   return cudaGetLastError();
 }
 
-cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kTThreads * kTStride;
+template <int B>
+static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)kTThreads * tstride<B>();
   if (a.index) {
-    k2_eval_thread<true><<<a.grid, kTThreads, smem, st>>>(c, a);
+    k2_eval_thread<true, B><<<a.grid, kTThreads, smem, st>>>(c, a);
     return cudaGetLastError();
   }
   // programmatic dependent launch: may start while K1 (which triggers at its
@@ -777,7 +803,11 @@ cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st)
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false>, c, a);
+  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false, B>, c, a);
+}
+
+cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
+  return c.n <= kMaxNWarp ? launch_eval_thread_b<kMaxNWarp>(c, a, st) : launch_eval_thread_b<kMaxN>(c, a, st);
 }
 
 }  // namespace optimus

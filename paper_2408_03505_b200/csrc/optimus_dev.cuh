@@ -9,7 +9,8 @@ namespace optimus {
 constexpr int64_t kInf = INT64_MAX / 4;   // "no finite shift" / +infinity
 constexpr int64_t kNegInf = -(INT64_MAX / 4);
 constexpr int kMaxP = 32;                 // LLM pipeline stages handled (one lane per stage in K0)
-constexpr int kMaxN = 32;                 // microbatches per LLM pipeline in K2 (one lane per slot)
+constexpr int kMaxN = 128;                // microbatches per LLM pipeline (K2 mode 1; mode 0, one lane per slot, takes n <= 32)
+constexpr int kMaxNWarp = 32;             // n handled by K2 mode 0 (eval.cu) and K2 mode 1's compact scratch
 
 // List ids in the packed input: 0 = LLM layer fwd, 1 = LLM layer bwd,
 // 2 + 2*(branch*ntp + ti) = encoder layer fwd at TP option ti, +1 = bwd.
@@ -141,5 +142,5 @@ cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* l
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
-int eval_thread_grid(int sms);
+int eval_thread_grid(int sms, bool wide);
 }  // namespace optimus

@@ -125,11 +125,22 @@ def test_rank_share_tiles(L):
 
 
 @pytest.mark.parametrize("n_mb", [64, 128])
-def test_config5_wide_sweep_points_refused(L, oracle_mod, n_mb):
-    """Config 5's sweep points N_mb = 64 and 128 exceed the GPU path's n <= 32
-    (round-2 gap): load refuses them with ERANGE naming the limit,
-    while the oracle covers them (its plan totals match SURVEY Appendix A)."""
+def test_config5_wide_sweep_points_plans(L, oracle_mod, n_mb):
+    """Config 5's sweep points N_mb = 64 and 128 (K2 mode 1's wide instance,
+    n <= 128): the library enumerates the oracle's plans and totals (SURVEY
+    Appendix A: 2,213,201,944 and 357,426,663,480 candidates)."""
     prob = config_problem(5, n_mb)
-    code, msg = _err(L, prob)
-    assert code == -5 and "exceeds the supported 32" in msg
-    assert oracle_mod.plans(prob)["total"] == {64: 2213201944, 128: 357426663480}[n_mb]
+    ctx = L.optimus_plan_only(prob)
+    total, n = ctx.num_candidates()
+    ref = oracle_mod.plans(prob)
+    assert total == ref["total"] == {64: 2213201944, 128: 357426663480}[n_mb]
+    for i, r in enumerate(ref["plans"]):
+        g = ctx.get_plan(i)
+        assert (g["pp"], g["tp"], g["m"], g["count"], g["first"]) == (r["P"], r["T"], r["m"], r["count"], r["first"])
+
+
+def test_n_mb_limit(L):
+    p = config_problem(5, 128)
+    p["n_mb"] = 136
+    code, msg = _err(L, p)
+    assert code == -5 and "exceeds the supported 128" in msg

@@ -461,3 +461,51 @@ def test_efficiency_trend_table7(dev):
     for (c0, f0), (c1, f1) in zip(effs, effs[1:]):
         assert c1 >= c0 and f1 >= f0
     assert all(f >= c for c, f in effs)
+
+
+# ---------------------------------------------------------------------------
+# N_mb 64 / 128 (config 5's sweep): K2 mode 1's wide instance (n, m <= 128)
+WIDE = [config_problem(5, 64), config_problem(5, 128)]
+
+
+@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+def test_wide_template_parity(dev, oracle_mod, prob):
+    test_template_parity(dev, oracle_mod, prob)
+
+
+@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+def test_wide_sampled_parity(dev, oracle_mod, prob):
+    """4096 seeded indices of the 2.2e9 / 3.6e11 spaces through eval_indices."""
+    test_sampled_parity_full_size(dev, oracle_mod, prob, 1)
+
+
+@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+def test_wide_contiguous_ranges(dev, oracle_mod, prob):
+    """The range path (overlapped with K1, claims per plan) on windows that
+    straddle plan boundaries, plus the very first and last candidates."""
+    torch = dev
+    ctx = _load(prob, 1)
+    total, n_plans = ctx.num_candidates()
+    firsts = [ctx.get_plan(i)["first"] for i in range(n_plans) if ctx.get_plan(i)["count"]]
+    o = oracle_mod.Oracle(prob)
+    wins = [(max(0, f - 700), min(total, f + 901)) for f in firsts[1:4]] + [(0, 1500), (total - 1300, total)]
+    for begin, end in wins:
+        lat = torch.empty(end - begin, dtype=torch.int64, device="cuda")
+        best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(begin, end, best2, lat_out=lat)
+        torch.cuda.synchronize()
+        ref = o.eval_range(begin, end, threads=THREADS)
+        got = lat.cpu().numpy()
+        assert np.array_equal(got, ref), (begin, end, int((got != ref).sum()))
+        b = best2.cpu().numpy()
+        assert (int(b[0]), int(b[1])) == (int(ref.min()), begin + int(np.argmin(ref)))
+
+
+def test_wide_mode0_refused(dev):
+    from paper_2408_03505_b200.optimus import OptimusError
+    torch = dev
+    ctx = _load(config_problem(5, 64), 0)
+    best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    with pytest.raises(OptimusError) as ei:
+        ctx.eval_candidates(0, 100, best2)
+    assert ei.value.code == -5
