@@ -190,8 +190,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
                        (size_t)X.p * (X.n + 1) * 12 + 64;
     if (per > 200 * 1024) return fail(OPTIMUS_ERANGE, "K1 shared-memory footprint %zu B exceeds 200 KB", per);
   }
-  {  // row stride 33 for n <= 32 (both K2 modes), 129 for the wide instance
-    const int S = X.n <= kMaxNWarp ? kMaxNWarp + 1 : kMaxN + 1;
+  {  // row stride 33 / 65 / 129 by K2 mode 1 instance (mode 0 runs only at 33)
+    const int S = (X.n <= 32 ? 32 : X.n <= 64 ? 64 : 128) + 1;  // = the K2 mode 1 instance's B + 1
     X.binom.assign((size_t)S * S, 0);
     for (int a = 0; a < S; ++a)
       for (int b = 0; b < S; ++b) X.binom[a * S + b] = binom_sat(a, b);
@@ -432,15 +432,14 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = sms;
   {  // occupancy-derived persistent grids, computed once per process and SM count
-    static int cached_sms = -1, cached_grid = 0, cached_grid_thread = 0, cached_grid_wide = 0;
+    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[3] = {0, 0, 0};
     if (cached_sms != sms) {
       cached_grid = std::min(4096, eval_grid(sms));
-      cached_grid_thread = std::min(4096, eval_thread_grid(sms, false));
-      cached_grid_wide = std::min(cached_grid_thread, eval_thread_grid(sms, true));
+      for (int i = 0; i < 3; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, 32 << i));
       cached_sms = sms;
     }
     c->grid = cached_grid;
-    c->grid_thread = X.n <= kMaxNWarp ? cached_grid_thread : cached_grid_wide;
+    c->grid_thread = cached_grid_thread[X.n <= 32 ? 0 : X.n <= 64 ? 1 : 2];  // K2 mode 1 instance by n
   }
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);

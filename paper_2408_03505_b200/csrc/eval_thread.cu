@@ -44,7 +44,7 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
 // per-thread scratch: B = 32 (n, m <= 32): 65 words (odd) = 260 bytes;
-// B = 128 (wide, n, m <= 128): 257 words = 1028 bytes
+// B = 64: 129 words = 516 bytes; B = 128 (n, m <= 128): 257 words = 1028 bytes
 template <int B>
 __host__ __device__ constexpr int tstride() { return (8 * B + 4) | 4; }
 
@@ -579,7 +579,7 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
 }
 
 template <bool EXPLICIT, int B>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : 1) k2_eval_thread(Cfg c, EvalArgs A) {
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : 1) k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
   __shared__ long long bl_sm[kTThreads / 32];
@@ -761,26 +761,29 @@ static void k2t_attrs() {
   cudaFuncSetAttribute(k2_explain<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-// persistent grid of the compact (n <= 32) or wide (n <= 128) instance
-int eval_thread_grid(int sms, bool wide) {
+// K2 mode 1 instance for n: per-thread arrays of B = 32, 64 or 128 entries
+__host__ __device__ constexpr int tinstance(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+
+template <int B>
+static int grid_b(int sms) {
   int per = 0;
-  if (wide) {
-    k2t_attrs<kMaxN>();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, kMaxN>, kTThreads,
-                                                  kTThreads * tstride<kMaxN>());
-  } else {
-    k2t_attrs<kMaxNWarp>();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, kMaxNWarp>, kTThreads,
-                                                  kTThreads * tstride<kMaxNWarp>());
-  }
+  k2t_attrs<B>();
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B>, kTThreads, kTThreads * tstride<B>());
   return max(1, per) * sms;
 }
 
+// persistent grid of the instance n selects
+int eval_thread_grid(int sms, int n) {
+  const int B = tinstance(n);
+  return B == 32 ? grid_b<32>(sms) : B == 64 ? grid_b<64>(sms) : grid_b<128>(sms);
+}
+
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
-  if (c.n <= kMaxNWarp)
-    k2_explain<kMaxNWarp><<<1, kTThreads, (size_t)kTThreads * tstride<kMaxNWarp>(), st>>>(c, g, d_out);
-  else
-    k2_explain<kMaxN><<<1, kTThreads, (size_t)kTThreads * tstride<kMaxN>(), st>>>(c, g, d_out);
+  switch (tinstance(c.n)) {
+    case 32: k2_explain<32><<<1, kTThreads, (size_t)kTThreads * tstride<32>(), st>>>(c, g, d_out); break;
+    case 64: k2_explain<64><<<1, kTThreads, (size_t)kTThreads * tstride<64>(), st>>>(c, g, d_out); break;
+    default: k2_explain<128><<<1, kTThreads, (size_t)kTThreads * tstride<128>(), st>>>(c, g, d_out); break;
+  }
   return cudaGetLastError();
 }
 
@@ -807,7 +810,11 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStr
 }
 
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
-  return c.n <= kMaxNWarp ? launch_eval_thread_b<kMaxNWarp>(c, a, st) : launch_eval_thread_b<kMaxN>(c, a, st);
+  switch (tinstance(c.n)) {
+    case 32: return launch_eval_thread_b<32>(c, a, st);
+    case 64: return launch_eval_thread_b<64>(c, a, st);
+    default: return launch_eval_thread_b<128>(c, a, st);
+  }
 }
 
 }  // namespace optimus

@@ -142,5 +142,5 @@ cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* l
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
-int eval_thread_grid(int sms, bool wide);
+int eval_thread_grid(int sms, int n);
 }  // namespace optimus
