@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "candidate schedules evaluated/sec"
+SAMPLE_SEED = 20241019  # --sample: g_i = splitmix64(SAMPLE_SEED + i) mod total
 UNIT = "candidates/s"
 
 
@@ -48,6 +49,9 @@ def parse_args():
     ap.add_argument("--config", type=int, default=4, help="BASELINE.json config (1-5)")
     ap.add_argument("--n-mb", type=int, default=None, help="microbatches (config 5 sweep)")
     ap.add_argument("--block", type=int, default=4096)
+    ap.add_argument("--sample", type=int, default=0,
+                    help="evaluate K seeded splitmix64 indices (resident in HBM) instead of the whole space, "
+                         "e.g. config 5 at N_mb 128 (3.6e11 candidates)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/cpu/e2e legs")
@@ -157,7 +161,10 @@ def workload_config(prob, name, world, args, total):
             "llm_plan": f"DP{llm['dp']} PP{llm['pp']} TP{llm['tp']} V{llm['v']}",
             "simulated_gpus": prob["n_gpu"], "encoders": [b["layers"] for b in prob["branches"]],
             "l2": "flushed before every timed step (256 MiB memset, outside the step events)",
-            "sharding": f"block-cyclic, block={args.block}", "parallelism": f"candidates-dp{world}"}
+            "sharding": (f"contiguous slices of {args.sample} seeded splitmix64 indices (seed {SAMPLE_SEED})"
+                         if getattr(args, "sample", 0) else f"block-cyclic, block={args.block}"),
+            "evaluated_per_step": int(args.sample) if getattr(args, "sample", 0) else int(total),
+            "parallelism": f"candidates-dp{world}"}
 
 
 # ---------------------------------------------------------------- cpu leg
@@ -241,10 +248,21 @@ def main():
     total, n_plans = ctx.num_candidates()
     best2 = torch.empty(2, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    units = total
+    hidx = didx = None
+    if args.sample:  # this rank's contiguous slice of the seeded stream, resident in HBM
+        from workload import sample_indices_np
+        units = args.sample
+        lo, hi = rank * units // world, (rank + 1) * units // world
+        hidx = torch.from_numpy(sample_indices_np(SAMPLE_SEED + lo, hi - lo, total).view("int64")).pin_memory()
+        didx = hidx.to("cuda")
 
     def step():
         ctx.rebuild(stream)
-        ctx.eval_candidates(0, total, best2, rank=rank, world=world, block=args.block, stream=stream)
+        if didx is not None:
+            ctx.eval_indices(didx, best2, stream=stream)
+        else:
+            ctx.eval_candidates(0, total, best2, rank=rank, world=world, block=args.block, stream=stream)
         if world > 1:
             return gather_best(best2)
         return best2.view(1, 2)
@@ -301,7 +319,7 @@ def main():
     if dist:
         dist.all_reduce(sum_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(sum_ms.item()) / args.steps
-    value = total / (ms_per_step / 1000.0)
+    value = units / (ms_per_step / 1000.0)
 
     # ---- e2e through the public API from host inputs, every step
     e2e = None
@@ -315,7 +333,10 @@ def main():
             t0 = time.perf_counter()
             c2 = OP.Ctx(OP.Problem(prob), ws, stream)          # H2D copy + build
             b2 = torch.empty(2, dtype=torch.int64, device="cuda")
-            c2.eval_candidates(0, total, b2, rank=rank, world=world, block=args.block, stream=stream)
+            if hidx is not None:  # the step's indices come from pinned host memory
+                c2.eval_indices(hidx.to("cuda", non_blocking=True), b2, stream=stream)
+            else:
+                c2.eval_candidates(0, total, b2, rank=rank, world=world, block=args.block, stream=stream)
             gg = gather_best(b2) if world > 1 else b2.view(1, 2)
             res = c2.best_plan(gg.cpu().numpy())                # D2H + decode
             c2.free()
@@ -327,7 +348,9 @@ def main():
         if dist:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item()) / args.steps
-        e2e = {"value": total / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        if hidx is not None:
+            h2d += hidx.numel() * 8
+        e2e = {"value": units / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h) * world, "ms_per_step": e2e_s * 1000}
 
     # ---- roofline of the dominant kernel (K2), alu-bound

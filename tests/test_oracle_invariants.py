@@ -152,3 +152,11 @@ def test_oracle_deterministic_and_thread_invariant(oracle_mod):
     a = o.eval(idx, threads=1)
     b = o.eval(idx, threads=4)
     assert a.tolist() == b.tolist()
+
+
+def test_vectorised_sample_stream_matches_scalar():
+    """bench.py --sample draws its indices with the vectorised splitmix64; it
+    must be the scalar stream SURVEY §8(d) defines, index for index."""
+    from workload import sample_indices, sample_indices_np
+    for seed, count, total in [(7, 3000, 357426663480), (2**64 - 5, 40, 12345), (20241019, 1000, 2213201944)]:
+        assert sample_indices_np(seed, count, total).tolist() == sample_indices(seed, count, total)

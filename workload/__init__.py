@@ -13,5 +13,6 @@ from .gen import (  # noqa: F401
     random_problem,
     splitmix64,
     sample_indices,
+    sample_indices_np,
     problem_summary,
 )

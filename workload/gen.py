@@ -39,6 +39,16 @@ def sample_indices(seed: int, count: int, total: int) -> list[int]:
     return [splitmix64((seed + i) & MASK64) % total for i in range(count)]
 
 
+def sample_indices_np(seed: int, count: int, total: int):
+    """The same stream as sample_indices, vectorised (numpy uint64 wraps mod 2^64)."""
+    import numpy as np
+    z = np.arange(count, dtype=np.uint64) + np.uint64(seed & MASK64) + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    z = z ^ (z >> np.uint64(31))
+    return z % np.uint64(total)
+
+
 def _rhu(x: Fraction) -> int:
     """Round half-up to an integer, minimum 1 (durations are >= 1 ns, R1)."""
     v = (x.numerator * 2 + x.denominator) // (2 * x.denominator)
