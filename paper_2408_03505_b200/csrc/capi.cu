@@ -336,9 +336,18 @@ struct optimus_ctx {
 
 namespace {
 
+// largest m over plans with candidates (sizes K2 mode 1's per-thread scratch)
+static int plans_mmax(const Prep& X) {
+  int mm = 1;
+  for (const auto& h : X.plans)
+    if (h.d.count) mm = std::max(mm, (int)h.d.m);
+  return mm;
+}
+
 Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   Cfg c;
   memset(&c, 0, sizeof c);
+  c.mmax = plans_mmax(X);
   c.p = X.p; c.t = X.t; c.v = X.v; c.n = X.n; c.lc = X.lc; c.policy = pb->warmup_policy;
   c.nb = X.nb; c.ntp = X.ntp; c.E = (int)X.plans.size(); c.nops = X.nops;
   c.icapc = X.icapc; c.icapm = X.icapm; c.kmax_all = X.kmax_all; c.nk_max = std::max(1, X.nk_max);
@@ -432,14 +441,14 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = sms;
   {  // occupancy-derived persistent grids, computed once per process and SM count
-    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[3] = {0, 0, 0};
+    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[4] = {0, 0, 0, 0};
     if (cached_sms != sms) {
       cached_grid = std::min(4096, eval_grid(sms));
-      for (int i = 0; i < 3; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, 32 << i));
+      for (int i = 0; i < 4; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
       cached_sms = sms;
     }
     c->grid = cached_grid;
-    c->grid_thread = cached_grid_thread[X.n <= 32 ? 0 : X.n <= 64 ? 1 : 2];  // K2 mode 1 instance by n
+    c->grid_thread = cached_grid_thread[eval_thread_instance(X.n, plans_mmax(X))];  // K2 mode 1 instance
   }
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);

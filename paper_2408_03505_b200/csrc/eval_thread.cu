@@ -43,10 +43,11 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #ifndef K2T_MINB
 #define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
 #endif
-// per-thread scratch: B = 32 (n, m <= 32): 65 words (odd) = 260 bytes;
-// B = 64: 129 words = 516 bytes; B = 128 (n, m <= 128): 257 words = 1028 bytes
-template <int B>
-__host__ __device__ constexpr int tstride() { return (8 * B + 4) | 4; }
+// per-thread scratch for n <= B slots and m <= BM pipelines: 4 BM + 4 B
+// bytes plus one odd word: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 772;
+// (128, 128) 1028
+template <int B, int BM = B>
+__host__ __device__ constexpr int tstride() { return (4 * BM + 4 * B + 4) | 4; }
 
 // Per-thread scratch (bytes 0..8B-1, B = 32 shown).  The three phases of one
 // candidate use disjoint live sets, so bytes 2B..8B-1 are shared between them:
@@ -69,21 +70,22 @@ struct TS {
   uint8_t* mvk;   //                                                  chain index
 };
 
-template <int B>
+template <int B, int BM>
 __device__ __forceinline__ TS ts_at(unsigned char* b) {
   TS s;
-  s.N = b;
-  s.c = b + B;
-  s.cnt = b + 2 * B;
-  s.thr = b + 3 * B + 2;
-  s.seen = b + 2 * B;
-  s.kb = b + 3 * B;
-  s.mvj = b + 4 * B;
-  s.mvk = b + 5 * B;
-  s.own = b + 6 * B;
-  s.rk = b + 7 * B;
-  s.cb = b + 2 * B;
-  s.Qcb = b + 3 * B;
+  s.N = b;                             // [BM]
+  s.c = b + BM;                        // [BM]
+  unsigned char* x = b + 2 * BM;       // phase-shared region
+  s.cnt = x;                           // [B + 2]
+  s.thr = x + B + 2;                   // [B]
+  s.seen = x;                          // [BM]
+  s.kb = x + BM;                       // [BM]
+  s.mvj = x + 2 * BM;                  // [B]
+  s.mvk = x + 2 * BM + B;              // [B]
+  s.own = x + 2 * BM + 2 * B;          // [B]
+  s.rk = x + 2 * BM + 3 * B;           // [B]
+  s.cb = x;                            // [BM]
+  s.Qcb = x + BM;                      // [B], ends before own
   return s;
 }
 
@@ -578,8 +580,9 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
   if (lat < bl || (lat == bl && g < bg)) { bl = lat; bg = g; }
 }
 
-template <bool EXPLICIT, int B>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : 1) k2_eval_thread(Cfg c, EvalArgs A) {
+template <bool EXPLICIT, int B, int BM>
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : BM == 64 ? 2 : 1)
+    k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
   __shared__ long long bl_sm[kTThreads / 32];
@@ -609,7 +612,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : 
     atomicMin(reinterpret_cast<unsigned long long*>(c.k1next) + 3, t);
   }
 #endif
-  TS s = ts_at<B>(tsm + (size_t)threadIdx.x * tstride<B>());
+  TS s = ts_at<B, BM>(tsm + (size_t)threadIdx.x * tstride<B, BM>());
   TPlan p;
   p.e = -1;
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : 
 // out: [0] lat, [1] Df, [2] Db, [3] forward moves, [4] backward moves,
 // [5] plan, [6] m, [7] n, [8, 8+n) forward move pipelines, [8+n, 8+2n)
 // backward ones, then N[m], c_final[m], cb_final[m].  One thread works.
-template <int B>
+template <int B, int BM>
 __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64_t* out) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
@@ -738,7 +741,7 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   if (e < 0) return;
   TPlan p;
   tplan(c, e, p);
-  TS s = ts_at<B>(tsm);
+  TS s = ts_at<B, BM>(tsm);
   tunrank<B>(c, n, p.m, g - p.first, s);
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
   out[5] = e;
@@ -749,49 +752,65 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
 
 }  // namespace
 
-template <int B>
+template <int B, int BM>
 static void k2t_attrs() {
-  constexpr int smem = kTThreads * tstride<B>();
-  cudaFuncSetAttribute(k2_eval_thread<false, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k2_eval_thread<false, B>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  constexpr int smem = kTThreads * tstride<B, BM>();
+  cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_eval_thread<true, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k2_eval_thread<true, B>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaFuncSetAttribute(k2_eval_thread<true, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_eval_thread<true, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_explain<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_explain<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-// K2 mode 1 instance for n: per-thread arrays of B = 32, 64 or 128 entries
-__host__ __device__ constexpr int tinstance(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : 128; }
+// K2 mode 1 instance for n slots and at most mmax pipelines in a plan with
+// candidates: 0 = (32, 32), 1 = (64, 64), 2 = (128, 64), 3 = (128, 128)
+__host__ __device__ constexpr int tinstance(int n, int mmax) {
+  return n <= 32 ? 0 : n <= 64 ? 1 : mmax <= 64 ? 2 : 3;
+}
 
-template <int B>
+template <int B, int BM>
 static int grid_b(int sms) {
   int per = 0;
-  k2t_attrs<B>();
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B>, kTThreads, kTThreads * tstride<B>());
+  k2t_attrs<B, BM>();
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B, BM>, kTThreads,
+                                                kTThreads * tstride<B, BM>());
   return max(1, per) * sms;
 }
 
-// persistent grid of the instance n selects
-int eval_thread_grid(int sms, int n) {
-  const int B = tinstance(n);
-  return B == 32 ? grid_b<32>(sms) : B == 64 ? grid_b<64>(sms) : grid_b<128>(sms);
+int eval_thread_instance(int n, int mmax) { return tinstance(n, mmax); }
+
+// persistent grid of instance i
+int eval_thread_grid(int sms, int i) {
+  switch (i) {
+    case 0: return grid_b<32, 32>(sms);
+    case 1: return grid_b<64, 64>(sms);
+    case 2: return grid_b<128, 64>(sms);
+    default: return grid_b<128, 128>(sms);
+  }
+}
+
+template <int B, int BM>
+static void explain_b(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
+  k2_explain<B, BM><<<1, kTThreads, (size_t)kTThreads * tstride<B, BM>(), st>>>(c, g, d_out);
 }
 
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
-  switch (tinstance(c.n)) {
-    case 32: k2_explain<32><<<1, kTThreads, (size_t)kTThreads * tstride<32>(), st>>>(c, g, d_out); break;
-    case 64: k2_explain<64><<<1, kTThreads, (size_t)kTThreads * tstride<64>(), st>>>(c, g, d_out); break;
-    default: k2_explain<128><<<1, kTThreads, (size_t)kTThreads * tstride<128>(), st>>>(c, g, d_out); break;
+  switch (tinstance(c.n, c.mmax)) {
+    case 0: explain_b<32, 32>(c, g, d_out, st); break;
+    case 1: explain_b<64, 64>(c, g, d_out, st); break;
+    case 2: explain_b<128, 64>(c, g, d_out, st); break;
+    default: explain_b<128, 128>(c, g, d_out, st); break;
   }
   return cudaGetLastError();
 }
 
-template <int B>
+template <int B, int BM>
 static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kTThreads * tstride<B>();
+  const size_t smem = (size_t)kTThreads * tstride<B, BM>();
   if (a.index) {
-    k2_eval_thread<true, B><<<a.grid, kTThreads, smem, st>>>(c, a);
+    k2_eval_thread<true, B, BM><<<a.grid, kTThreads, smem, st>>>(c, a);
     return cudaGetLastError();
   }
   // programmatic dependent launch: may start while K1 (which triggers at its
@@ -806,14 +825,15 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStr
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false, B>, c, a);
+  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false, B, BM>, c, a);
 }
 
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
-  switch (tinstance(c.n)) {
-    case 32: return launch_eval_thread_b<32>(c, a, st);
-    case 64: return launch_eval_thread_b<64>(c, a, st);
-    default: return launch_eval_thread_b<128>(c, a, st);
+  switch (tinstance(c.n, c.mmax)) {
+    case 0: return launch_eval_thread_b<32, 32>(c, a, st);
+    case 1: return launch_eval_thread_b<64, 64>(c, a, st);
+    case 2: return launch_eval_thread_b<128, 64>(c, a, st);
+    default: return launch_eval_thread_b<128, 128>(c, a, st);
   }
 }
 

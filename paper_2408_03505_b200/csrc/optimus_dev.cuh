@@ -44,6 +44,7 @@ struct Cfg {
   int32_t nk_max;        // max over TP options of the encoder's total kernel count (all layers, all branches)
   int32_t ci_n;          // 32-interval blocks per interval list: ceil(max(icapc, icapm) / 32)
   int32_t nflags;        // K1 flags (zeroed by k0_final)
+  int32_t mmax;          // largest m over plans with candidates (K2 mode 1 scratch instance)
   int64_t T_ag, T_rs, pp_p2p, enc_p2p, L;
   // packed inputs
   const int32_t* lkind;   // kernel kinds, all lists concatenated
@@ -142,5 +143,6 @@ cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* l
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
-int eval_thread_grid(int sms, int n);
+int eval_thread_grid(int sms, int instance);
+int eval_thread_instance(int n, int mmax);
 }  // namespace optimus
