@@ -441,10 +441,10 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = sms;
   {  // occupancy-derived persistent grids, computed once per process and SM count
-    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[4] = {0, 0, 0, 0};
+    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[6] = {0, 0, 0, 0, 0, 0};
     if (cached_sms != sms) {
       cached_grid = std::min(4096, eval_grid(sms));
-      for (int i = 0; i < 4; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
+      for (int i = 0; i < 6; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
       cached_sms = sms;
     }
     c->grid = cached_grid;

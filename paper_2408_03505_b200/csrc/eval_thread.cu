@@ -45,7 +45,7 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #endif
 // per-thread scratch for n <= B slots and m <= BM pipelines: 4 BM + 4 B
 // bytes plus one odd word: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 772;
-// (128, 128) 1028
+// (128, 128) 1028; (64, 16) 324; (128, 16) 580
 template <int B, int BM = B>
 __host__ __device__ constexpr int tstride() { return (4 * BM + 4 * B + 4) | 4; }
 
@@ -581,7 +581,7 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
 }
 
 template <bool EXPLICIT, int B, int BM>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : B == 64 ? 3 : BM == 64 ? 2 : 1)
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? 4 : B == 64 ? 3 : BM == 64 ? 2 : 1)
     k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
@@ -765,9 +765,10 @@ static void k2t_attrs() {
 }
 
 // K2 mode 1 instance for n slots and at most mmax pipelines in a plan with
-// candidates: 0 = (32, 32), 1 = (64, 64), 2 = (128, 64), 3 = (128, 128)
+// candidates: 0 = (32, 32), 1 = (64, 64), 2 = (128, 64), 3 = (128, 128),
+// 4 = (64, 16), 5 = (128, 16)
 __host__ __device__ constexpr int tinstance(int n, int mmax) {
-  return n <= 32 ? 0 : n <= 64 ? 1 : mmax <= 64 ? 2 : 3;
+  return n <= 32 ? 0 : n <= 64 ? (mmax <= 16 ? 4 : 1) : mmax <= 16 ? 5 : mmax <= 64 ? 2 : 3;
 }
 
 template <int B, int BM>
@@ -787,6 +788,8 @@ int eval_thread_grid(int sms, int i) {
     case 0: return grid_b<32, 32>(sms);
     case 1: return grid_b<64, 64>(sms);
     case 2: return grid_b<128, 64>(sms);
+    case 4: return grid_b<64, 16>(sms);
+    case 5: return grid_b<128, 16>(sms);
     default: return grid_b<128, 128>(sms);
   }
 }
@@ -801,6 +804,8 @@ cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_
     case 0: explain_b<32, 32>(c, g, d_out, st); break;
     case 1: explain_b<64, 64>(c, g, d_out, st); break;
     case 2: explain_b<128, 64>(c, g, d_out, st); break;
+    case 4: explain_b<64, 16>(c, g, d_out, st); break;
+    case 5: explain_b<128, 16>(c, g, d_out, st); break;
     default: explain_b<128, 128>(c, g, d_out, st); break;
   }
   return cudaGetLastError();
@@ -833,6 +838,8 @@ cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st)
     case 0: return launch_eval_thread_b<32, 32>(c, a, st);
     case 1: return launch_eval_thread_b<64, 64>(c, a, st);
     case 2: return launch_eval_thread_b<128, 64>(c, a, st);
+    case 4: return launch_eval_thread_b<64, 16>(c, a, st);
+    case 5: return launch_eval_thread_b<128, 16>(c, a, st);
     default: return launch_eval_thread_b<128, 128>(c, a, st);
   }
 }
