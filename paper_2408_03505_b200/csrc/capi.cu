@@ -9,6 +9,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -184,12 +186,6 @@ int prepare(const optimus_problem* pb, Prep& X) {
     return fail(OPTIMUS_ERANGE, "PP*V*N_mb too large for the K0 shared-memory simulation");
   if ((size_t)(std::max(X.icapc, X.icapm) + 31) / 32 * 32 + (size_t)X.nops * 5 + 64 > 160 * 1024)
     return fail(OPTIMUS_ERANGE, "too many bubble intervals per stage for the K0 interval kernel");
-  {
-    const size_t ci = (size_t)(std::max(X.icapc, X.icapm) + 31) / 32;
-    const size_t per = (size_t)X.nk_max * 9 + 64 + (size_t)(3 * X.p + 1) * 4 + (size_t)X.p * 2 * ci * 8 +
-                       (size_t)X.p * (X.n + 1) * 12 + 64;
-    if (per > 200 * 1024) return fail(OPTIMUS_ERANGE, "K1 shared-memory footprint %zu B exceeds 200 KB", per);
-  }
   {  // row stride 33 / 65 / 129 by K2 mode 1 instance (mode 0 runs only at 33)
     const int S = (X.n <= 32 ? 32 : X.n <= 64 ? 64 : 128) + 1;  // = the K2 mode 1 instance's B + 1
     X.binom.assign((size_t)S * S, 0);
@@ -247,6 +243,10 @@ int prepare(const optimus_problem* pb, Prep& X) {
     }
   }
   X.total = first;
+  {  // K1's per-block shared memory (kernel lists, coarse indices, block owners, chain status)
+    const size_t per = k1_smem_for(X.nk_max, X.p, (std::max(X.icapc, X.icapm) + 31) / 32, X.kmax_all);
+    if (per > 220 * 1024) return fail(OPTIMUS_ERANGE, "K1 shared-memory footprint %zu B exceeds 220 KB", per);
+  }
   if (X.plans.size() > (size_t)kMaxE) return fail(OPTIMUS_ERANGE, "%zu encoder plans (> %d supported)", X.plans.size(), kMaxE);
   // K2 takes plans with more stages first: their chains are shorter, so K1
   // can finish them first
@@ -305,7 +305,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_k1flags = take((size_t)X.n_flags * 4);
   X.o_sync = take(64 + (size_t)kMaxE * (4 + 8));  // k1next (+ development probes), pdone[E], pclaim[E]
   X.o_iv = take((size_t)X.p * 8 * (8 + 4));          // k0_intervals block exchange
-  X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32));
+  X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32) * 2);
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
@@ -335,6 +335,31 @@ struct optimus_ctx {
 };
 
 namespace {
+
+// Per-device launch state.  Function attributes (large dynamic shared memory
+// opt-ins) are per device, so they are set the first time a device is used;
+// the occupancy-derived persistent grids follow.  Guarded for loads from
+// several host threads (distinct ctxs are independent, §8(b)).
+struct DeviceInfo {
+  int grid = 0;
+  int grid_thread[6] = {0, 0, 0, 0, 0, 0};
+};
+
+DeviceInfo device_info(int dev, int sms) {
+  static std::mutex mu;
+  static std::map<int, DeviceInfo> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  template_attrs();
+  chains_attrs();
+  eval_thread_attrs();
+  DeviceInfo d;
+  d.grid = std::min(4096, eval_grid(sms));
+  for (int i = 0; i < 6; ++i) d.grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
+  cache[dev] = d;
+  return d;
+}
 
 // largest m over plans with candidates (sizes K2 mode 1's per-thread scratch)
 static int plans_mmax(const Prep& X) {
@@ -382,7 +407,7 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.tables = (int64_t*)(ws + X.o_tables);
   c.snap = (int64_t*)(ws + X.o_snap);
   c.bfill = (int64_t*)(ws + X.o_bfill);
-  c.snap_own = (int8_t*)(ws + X.o_snap_own);
+  c.snap_own = (int16_t*)(ws + X.o_snap_own);
   c.k1flags = (int32_t*)(ws + X.o_k1flags);
   c.k1units = (const int32_t*)(ws + X.o_units);
   c.k1_total = (int32_t)X.units.size();
@@ -440,19 +465,13 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "no usable CUDA device: %s", cudaGetErrorString(e)); }
   c->sms = sms;
-  {  // occupancy-derived persistent grids, computed once per process and SM count
-    static int cached_sms = -1, cached_grid = 0, cached_grid_thread[6] = {0, 0, 0, 0, 0, 0};
-    if (cached_sms != sms) {
-      cached_grid = std::min(4096, eval_grid(sms));
-      for (int i = 0; i < 6; ++i) cached_grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
-      cached_sms = sms;
-    }
-    c->grid = cached_grid;
-    c->grid_thread = cached_grid_thread[eval_thread_instance(X.n, plans_mmax(X))];  // K2 mode 1 instance
-  }
+  const DeviceInfo di = device_info(dev, sms);  // function attributes + occupancy, once per device
+  c->grid = di.grid;
+  c->grid_thread = di.grid_thread[eval_thread_instance(X.n, plans_mmax(X))];  // K2 mode 1 instance
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
   c->cfg.sms = sms;
+  c->cfg.k1_grid = k1_grid(c->cfg);
   cudaStream_t st = (cudaStream_t)cuda_stream;
   // one host->device copy of the packed inputs (the problem's cost tables)
   std::vector<char> h(X.inputs_bytes, 0);

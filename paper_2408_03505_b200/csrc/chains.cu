@@ -95,7 +95,7 @@ __device__ void plan_tables(const Cfg& c, int e) {
   }
   __syncthreads();
   // order ranks of the DEV entries (K2's findCritical compares 32-bit keys
-  // rank << 5 | 31 - j): rank = #{entries < v}, >= rp for cnt > 0, 0 at cnt 0
+  // rank << 7 | 127 - j): rank = #{entries < v}, >= rp for cnt > 0, 0 at cnt 0
   const int V = pd.rp * (n + 1);
   uint32_t* key = reinterpret_cast<uint32_t*>(c.tables + pd.devK);
   for (int i = threadIdx.x; i < 2 * V; i += blockDim.x) {
@@ -133,7 +133,7 @@ struct VR {
   const int64_t* H;
   int64_t* fill;         // mirror: this unit's fill array
   int64_t* bm;           // largest capacity hi - lo of each 32-block (smem; lowered as blocks fill)
-  int8_t* own;           // owner version per 32-block (smem): forward current, mirror kf's
+  int16_t* own;          // owner version per 32-block (smem): forward current, mirror kf's (-1: never written)
   int64_t* snap0;        // this list in version 0's buffer; version o at + o * vstride
   int64_t vstride;
   int64_t T_end;
@@ -204,7 +204,7 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   if (lane == 0) {
     V.bm[w.base >> 5] = cap;
     if (M) V.wm[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
-    else V.own[w.base >> 5] = (int8_t)V.ver;
+    else V.own[w.base >> 5] = (int16_t)V.ver;
   }
   w.dirty = false;
   __syncwarp();
@@ -269,14 +269,14 @@ struct UnitSm {
   uint32_t* wm;       // [P][2][MW] blocks of the fill arrays written so far
   int64_t* ci;        // [P][2][CI] coarse index: end of the last interval of each 32-block
   int64_t* bm;        // [P][2][CI] largest base capacity of each 32-block (this orientation)
-  int8_t* own;        // [P][2][CI] snapshot block owners (forward: current, mirror: snapshot kf)
+  int16_t* own;       // [P][2][CI] snapshot block owners (forward: current, mirror: snapshot kf); int16: versions reach kmax = n - m + 1 <= 128
   int CI, MW;
 };
 
 __host__ __device__ inline size_t unit_smem_bytes(int NK, int P, int CI) {
   const int MW = (CI + 31) / 32;
   return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
-         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI + 15) / 16 * 16;
+         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI * 2 + 15) / 16 * 16;
 }
 
 __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
@@ -290,7 +290,7 @@ __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
   u.ci = (int64_t*)p;
   u.bm = u.ci + (size_t)P * 2 * CI;
   p += (size_t)P * 2 * CI * 8 * 2;
-  u.own = (int8_t*)p;
+  u.own = (int16_t*)p;
   u.CI = CI;
   u.MW = (CI + 31) / 32;
   return u;
@@ -575,9 +575,9 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   if (active) {
     for (int r = 0; r < 2; ++r) {
       // block owners: forward starts untouched; mirror loads snapshot kf's map
-      int8_t* own = U.own + (2 * s + r) * U.CI;
-      const int8_t* gown = c.snap_own + (slot(kf, s) * 2 + r) * c.ci_n;
-      for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? (int8_t)__ldcg((const signed char*)&gown[b]) : (int8_t)-1;
+      int16_t* own = U.own + (2 * s + r) * U.CI;
+      const int16_t* gown = c.snap_own + (slot(kf, s) * 2 + r) * c.ci_n;
+      for (int b = lane; b < U.CI; b += 32) own[b] = (M && kf > 0) ? (int16_t)__ldcg((const short*)&gown[b]) : (int16_t)-1;
       for (int b = lane; b < U.MW; b += 32) U.wm[(2 * s + r) * U.MW + b] = 0u;
       __syncwarp();
       VR<M> V = make_view<M>(c, pd, a, s, r, nullptr, U, snap0 + (int64_t)s * icap, 0);
@@ -640,8 +640,8 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
       __syncwarp();
       if (!M && !REC) {  // publish version k+1 of this stage: the block owner maps after chain k
         for (int r = 0; r < 2; ++r) {
-          const int8_t* own = U.own + (2 * s + r) * U.CI;
-          int8_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
+          const int16_t* own = U.own + (2 * s + r) * U.CI;
+          int16_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
           for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
         }
         __threadfence();  // this lane's block and map stores before the count
@@ -799,38 +799,44 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
 }
 
 template <int MAXT, int MINB>
-static cudaError_t launch_k1(const Cfg& c, const K1Launch& L, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  static int per = 0, per_nt = -1;
-  static size_t per_smem = 0;
-  const int nt = 32 * c.p;
-  if (!attr) {  // opt in to large dynamic shared memory once per process
-    cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    // the whole unified L1 as shared memory: K2 blocks must fit next to the
-    // K1 blocks while both run
+static void k1_attrs() {
+  cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  // the whole unified L1 as shared memory: K2 blocks must fit next to the
+  // K1 blocks while both run
 #ifndef K1_NO_CARVEOUT
-    cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
 #endif
-    attr = true;
-  }
-  if (nt != per_nt || smem != per_smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, nt, smem);
-    per_nt = nt;
-    per_smem = smem;
-  }
+}
+
+#ifndef K1_MINB
+#define K1_MINB 2
+#endif
 #ifndef K1_PER_SM
 #define K1_PER_SM 1
 #endif
+
+template <int MAXT, int MINB>
+static int k1_grid_b(const Cfg& c, size_t smem) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, 32 * c.p, smem);
   // one block per SM (occupancy permitting) leaves room on every SM for K2
   // blocks, which start as soon as the first plans are complete
-  const int grid = std::max(1, std::min(c.k1_total, std::max(1, std::min(per, K1_PER_SM)) * c.sms));
-  k1_chains<MAXT, MINB><<<grid, nt, smem, st>>>(c, L);
-  return cudaGetLastError();
+  return std::max(1, std::min(c.k1_total, std::max(1, std::min(per, K1_PER_SM)) * c.sms));
 }
 
 }  // namespace
 
+
+// K1 dynamic shared memory per block for the problem's sizes (checked at load)
+size_t k1_smem_for(int nk, int p, int ci, int kmax_all) {
+  K1Launch L;
+  L.NK = std::max(1, nk);
+  L.Pmax = p;
+  L.CI = ci;
+  L.KM = std::max(1, kmax_all);
+  return k1_smem_bytes(L);
+}
 
 cudaError_t launch_eff(const Cfg& c, const int64_t* d_explain, unsigned long long* d_out, cudaStream_t st) {
   k_eff<<<1, 128, 0, st>>>(c, d_explain, d_out);
@@ -844,32 +850,48 @@ cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_
   L.CI = (std::max(c.icapc, c.icapm) + 31) / 32;
   L.KM = std::max(1, c.kmax_all);
   const size_t smem = k1_smem_bytes(L);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k1_record<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k1_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
   if (kf < 0) k1_record<false><<<1, 32 * c.p, smem, st>>>(c, L, e, a, 0, klimit, d_rec);
   else k1_record<true><<<1, 32 * c.p, smem, st>>>(c, L, e, a, kf, klimit, d_rec);
   return cudaGetLastError();
 }
 
-cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
+// large dynamic shared memory opt-in of every K1 variant (once per device, capi's device_info)
+void chains_attrs() {
+  k1_attrs<384, K1_MINB>();
+  k1_attrs<512, 1>();
+  k1_attrs<1024, 1>();
+  cudaFuncSetAttribute(k1_record<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k1_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+}
+
+static K1Launch k1_launch_of(const Cfg& c) {
   K1Launch L;
   L.NK = c.nk_max;
   L.Pmax = c.p;
   L.CI = (std::max(c.icapc, c.icapm) + 31) / 32;
   L.KM = std::max(1, c.kmax_all);
+  return L;
+}
+
+// persistent K1 grid for this problem (computed once at load)
+int k1_grid(const Cfg& c) {
+  const size_t smem = k1_smem_bytes(k1_launch_of(c));
+  if (c.p <= 12) return k1_grid_b<384, K1_MINB>(c, smem);
+  if (c.p <= 16) return k1_grid_b<512, 1>(c, smem);
+  return k1_grid_b<1024, 1>(c, smem);
+}
+
+cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
+  const K1Launch L = k1_launch_of(c);
   const size_t smem = k1_smem_bytes(L);
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (launches) *launches += 1;
-#ifndef K1_MINB
-#define K1_MINB 2
-#endif
-  if (c.p <= 12) return launch_k1<384, K1_MINB>(c, L, smem, st);
-  if (c.p <= 16) return launch_k1<512, 1>(c, L, smem, st);
-  return launch_k1<1024, 1>(c, L, smem, st);
+  const int grid = c.k1_grid;
+  const int nt = 32 * c.p;
+  if (c.p <= 12) k1_chains<384, K1_MINB><<<grid, nt, smem, st>>>(c, L);
+  else if (c.p <= 16) k1_chains<512, 1><<<grid, nt, smem, st>>>(c, L);
+  else k1_chains<1024, 1><<<grid, nt, smem, st>>>(c, L);
+  return cudaGetLastError();
 }
 
 }  // namespace optimus

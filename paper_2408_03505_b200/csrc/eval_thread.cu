@@ -91,7 +91,7 @@ __device__ __forceinline__ TS ts_at(unsigned char* b) {
 
 struct TPlan {
   int e, P, rt, m, kmax, np1;
-  unsigned rtm;            // row of pipeline j = (j * rtm) >> 16 (exact for j < 32, rt <= 32)
+  unsigned rtm;            // row of pipeline j = (j * rtm) >> 16 (exact for j < 128, rt <= 128)
   bool strict;            // PRE_EF strictly increasing: pre entries order by (t, j)
   uint64_t first, count;
   const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
@@ -416,7 +416,7 @@ __device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev
 
 // findCritical (R11): argmax over pipelines with count > 0 of DEV[row][count],
 // ties -> lowest j.  cnt8 = the per-pipeline counts.  Compares the 32-bit
-// keys rank(DEV[row][count]) << 5 | (31 - j) (m <= 32): the max key is the
+// keys rank(DEV[row][count]) << 7 | (127 - j) (m <= 128): the max key is the
 // max DEV at the lowest j; rank 0 (count 0) never wins over a count > 0.
 __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, const uint32_t* key, const uint8_t* cnt8,
                                             int m, int& js) {
@@ -581,7 +581,7 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
 }
 
 template <bool EXPLICIT, int B, int BM>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? 4 : B == 64 ? 3 : BM == 64 ? 2 : 1)
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
     k2_eval_thread(Cfg c, EvalArgs A) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
@@ -774,13 +774,22 @@ __host__ __device__ constexpr int tinstance(int n, int mmax) {
 template <int B, int BM>
 static int grid_b(int sms) {
   int per = 0;
-  k2t_attrs<B, BM>();
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B, BM>, kTThreads,
                                                 kTThreads * tstride<B, BM>());
   return max(1, per) * sms;
 }
 
 int eval_thread_instance(int n, int mmax) { return tinstance(n, mmax); }
+
+// dynamic shared memory opt-in of every instance (once per device, capi's device_info)
+void eval_thread_attrs() {
+  k2t_attrs<32, 32>();
+  k2t_attrs<64, 64>();
+  k2t_attrs<128, 64>();
+  k2t_attrs<128, 128>();
+  k2t_attrs<64, 16>();
+  k2t_attrs<128, 16>();
+}
 
 // persistent grid of instance i
 int eval_thread_grid(int sms, int i) {

@@ -76,17 +76,18 @@ struct Cfg {
   int64_t* tables;
   int64_t* snap;          // [slots][icapc+icapm] forward fill snapshots (slot k=0 is the working copy)
   int64_t* bfill;         // [slots][icapc+icapm] backward (mirrored) fill state
-  int8_t* snap_own;       // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
+  int16_t* snap_own;      // [slots][2][ci_n] owner version of each 32-block of each snapshot (-1 untouched)
   int32_t* k1flags;       // K1 forward -> backward progress flags (PlanDesc::flag_base); zeroed by k0_final
   const int32_t* k1units; // K1 work list: type << 30 | e << 16 | a << 8 | kf (type 0 forward, 1 backward, 2 plan tables)
   int32_t k1_total;       // K1 work items
   int32_t sms;            // SM count of the device (persistent grids)
+  int32_t k1_grid;        // persistent K1 grid (set at load)
   int32_t* k1next;        // K1 work counter (persistent blocks); zeroed by k0_final
   int32_t* pdone;         // [E] K1 work items of each plan completed (release); zeroed by k0_final
   unsigned long long* pclaim;  // [E] K2 chunks of each plan claimed; zeroed by K3
   const int32_t* k2order; // plans with candidates, in the order K2 takes them (short chains first)
   int32_t n_k2order;
-  const uint64_t* binom;  // [(kMaxN+1)*(kMaxN+1)]: C(a, b) at [a*(kMaxN+1)+b]
+  const uint64_t* binom;  // [S*S], S = B + 1 of the K2 mode 1 instance (33 / 65 / 129): C(a, b) at [a*S+b]; mode 0 reads it at S = 33
 };
 
 // Per-op identity in the Megatron interleaved 1F1B order (R2).
@@ -120,6 +121,11 @@ __host__ __device__ inline OpRef op_at(int p, int v, int n, int W, int pos) {
 namespace optimus {
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
 cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches);
+size_t k1_smem_for(int nk, int p, int ci, int kmax_all);
+int k1_grid(const Cfg& c);
+void template_attrs();
+void chains_attrs();
+void eval_thread_attrs();
 cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_t* d_rec, cudaStream_t st);
 cudaError_t launch_eff(const Cfg& c, const int64_t* d_explain, unsigned long long* d_out, cudaStream_t st);
 struct EvalArgs {

@@ -574,17 +574,17 @@ __global__ void __launch_bounds__(kIvThreads) k0_intervals(Cfg c) {
 
 }  // namespace
 
+// opt in to large dynamic shared memory (per device: capi's device_info runs it once per device)
+void template_attrs() {
+  cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k0_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);  // + ~11 KB static
+}
+
 cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
   const int wpb = k0_sim_warps(c.p, c.v, c.n);
   const size_t smem = k0_vtab_bytes(c.n, c.v) + (size_t)wpb * k0_warp_bytes(c.p, c.v, c.n);
   if (smem > 200 * 1024) return cudaErrorInvalidConfiguration;
-  static bool attrs = false;  // opt in to large dynamic shared memory once per process
-  if (!attrs) {
-    cudaFuncSetAttribute(k0_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k0_final, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k0_intervals, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);  // + ~11 KB static
-    attrs = true;
-  }
   const int nsim = 1 + c.k0_trials;
   k0_wave<<<(nsim + wpb - 1) / wpb, 32 * kSimWarps, smem, st>>>(c, nsim, wpb);
   k0_final<<<1, 32 * kSimWarps, smem, st>>>(c, wpb);
