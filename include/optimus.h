@@ -223,9 +223,11 @@ int optimus_set_timing(optimus_ctx* c, int on);
 int optimus_last_timing(const optimus_ctx* c, float* build_ms, float* eval_ms);
 
 /* Cumulative K2 work counters since load (synchronises the stream):
- * h_out[6] = candidates evaluated, algorithmic 32-bit integer lane-ops
+ * h_out[10] = candidates evaluated, algorithmic 32-bit integer lane-ops
  * (DESIGN.md §5), forward loop iterations, forward move attempts, backward
- * iterations, backward attempts. */
+ * iterations, backward attempts, candidates finished by K2 mode 1's fast
+ * path, candidates evaluated by its general path, warp claims and lane
+ * unrankings of its range path (the last four: mode 1 only, 0 in mode 0). */
 int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream);
 
 /* Bytes load copies host->device (the packed problem) and one evaluation

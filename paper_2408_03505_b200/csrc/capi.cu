@@ -227,6 +227,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
         d.devB = toff; toff += (int64_t)d.rp * np1;
         d.devK = toff; toff += (int64_t)d.rp * np1;
         d.bpF = toff; toff += (int64_t)d.rp * d.kmax;
+        d.pflags = toff; toff += 1;
+        d.kj = toff; toff += (int64_t)d.m * np1;
         d.inbF = toff; toff += (int64_t)d.rp * d.kmax;
         d.lenF = toff; toff += d.rp;
         d.inbB = toff; toff += (int64_t)d.rp * (d.kmax + 1) * d.kmax;
@@ -309,7 +311,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
-  X.o_stats = take(8 * 8);
+  X.o_stats = take(16 * 8);
   X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN + 4) * 8);  // + the efficiency sums
   X.o_rec = take((size_t)std::max(1, X.kmax_all) * std::max(1, X.nk_max) * 4 * 8);
   X.total_bytes = o;
@@ -485,7 +487,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   memcpy(h.data() + X.o_k2order, X.k2order.data(), X.k2order.size() * 4);
   e = cudaMemcpyAsync(c->ws, h.data(), h.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_counter, 0, 8, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 8 * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_stats, 0, 16 * 8, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 64 + (size_t)kMaxE * 12, st);  // K1/K2 counters
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_iv, 0, (size_t)X.p * 8 * 12, st);
@@ -854,8 +856,8 @@ int optimus_last_timing(const optimus_ctx* c, float* build_ms, float* eval_ms) {
 int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream) {
   if (!c || !c->ws || !h_out) return fail(OPTIMUS_EINVAL, "NULL argument or host-only ctx");
   CK(cudaStreamSynchronize((cudaStream_t)cuda_stream));
-  uint64_t v[8];
-  CK(cudaMemcpy(v, c->ws + c->X.o_stats, 8 * 8, cudaMemcpyDeviceToHost));
+  uint64_t v[12];
+  CK(cudaMemcpy(v, c->ws + c->X.o_stats, 12 * 8, cudaMemcpyDeviceToHost));
   // algorithmic 32-bit lane-ops per candidate (int64 add/compare/max = 2):
   // (17n + 4 + 2n lg) + 2m + 2 m it_f + 4 it_f + (10n+4) at_f + 2 m it_b + 4 it_b + (9n+4) at_b
   const uint64_t n = (uint64_t)c->X.n;
@@ -868,6 +870,10 @@ int optimus_eval_stats(const optimus_ctx* c, uint64_t* h_out, void* cuda_stream)
   h_out[3] = v[4];
   h_out[4] = v[6];
   h_out[5] = v[7];
+  h_out[6] = v[8];
+  h_out[7] = v[9];
+  h_out[8] = v[10];
+  h_out[9] = v[11];
   return OPTIMUS_OK;
 }
 

@@ -80,6 +80,11 @@ __device__ void plan_tables(const Cfg& c, int e) {
       }
   }
   __syncthreads();
+  if (threadIdx.x == 0) {  // K2's fast path needs PRE_EF strictly increasing (the pre entries of a level then order by j)
+    bool strict = true;
+    for (int t = 1; t < n; ++t) strict = strict && preF[(P - 1) * (n + 1) + t + 1] > preF[(P - 1) * (n + 1) + t];
+    c.tables[pd.pflags] = strict ? 1 : 0;
+  }
   // DEV[a][cnt] = max_s(end(s, cnt) - w_{aP+s}) (forward; w' = T_end - z backward)
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < pd.rp * (n + 1); i += blockDim.x) {
@@ -106,6 +111,15 @@ __device__ void plan_tables(const Cfg& c, int e) {
     if (ii % (n + 1) != 0)
       for (int q = 0; q < V; ++q) r += dv[q] < v ? 1u : 0u;
     key[i] = r;
+  }
+  __syncthreads();
+  // per-pipeline keys with the lowest-j tie rule folded in (K2 mode 1)
+  uint64_t* kj = reinterpret_cast<uint64_t*>(c.tables + pd.kj);
+  for (int i = threadIdx.x; i < pd.m * (n + 1); i += blockDim.x) {
+    const int j = i / (n + 1), cnt = i % (n + 1), a = j / pd.rt;
+    const uint32_t lo = (uint32_t)(127 - j);
+    const uint32_t kf = key[a * (n + 1) + cnt] << 7 | lo, kb = key[V + a * (n + 1) + cnt] << 7 | lo;
+    kj[i] = (uint64_t)kf | (uint64_t)kb << 32;
   }
 }
 

@@ -26,7 +26,7 @@ namespace {
 #endif
 constexpr int kTThreads = K2T_THREADS;
 #ifndef K2T_RUN
-#define K2T_RUN 16
+#define K2T_RUN 32
 #endif
 constexpr int kTRun = K2T_RUN;            // most consecutive candidates per thread and claim
 #ifndef K2T_MINRUN
@@ -40,14 +40,21 @@ constexpr int kTMinRun = K2T_MINRUN;      // fewest consecutive candidates per t
 #define K2T_GSS_DEN 1
 #endif
 constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remaining * GSS / (GSS_DEN * warps), capped
+constexpr int kQCap = 64;                 // per-warp general-path queue (a power of 2 >= 63)
 #ifndef K2T_MINB
-#define K2T_MINB 5  // resident blocks per SM the register cap aims at (smem allows 6)
+#define K2T_MINB 4  // resident blocks per SM the register cap aims at (smem allows 4)
 #endif
 // per-thread scratch for n <= B slots and m <= BM pipelines: 4 BM + 4 B
 // bytes plus one odd word: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 772;
 // (128, 128) 1028; (64, 16) 324; (128, 16) 580
 template <int B, int BM = B>
 __host__ __device__ constexpr int tstride() { return (4 * BM + 4 * B + 4) | 4; }
+// general-path queue entry: a composition of m <= 32 parts at an odd word stride
+template <int BM>
+__host__ __device__ constexpr int tqstride() { return (BM < 32 ? BM : 32) + 4; }
+// dynamic shared memory of a K2 mode 1 block: per-thread scratch + the warps' queues
+template <int B, int BM>
+__host__ __device__ constexpr int tsmem() { return kTThreads * tstride<B, BM>() + (kTThreads / 32) * kQCap * tqstride<BM>(); }
 
 // Per-thread scratch (bytes 0..8B-1, B = 32 shown).  The three phases of one
 // candidate use disjoint live sets, so bytes 2B..8B-1 are shared between them:
@@ -55,27 +62,39 @@ __host__ __device__ constexpr int tstride() { return (4 * BM + 4 * B + 4) | 4; }
 //   forward  cnt[64..97] thr[98..129]
 //   ordering seen[64..95] kb[96..127] mvj[128..159] mvk[160..191] own[192..223] rk[224..255]
 //   backward cb[64..95] Qcb[96..127] own rk   (kb_j = N_j - cb_j is implied)
+// K2 mode 1's dynamic shared memory: per-thread scratch, then the warps'
+// general-path queues.  Scratch arrays are addressed by 32-bit offsets into
+// it (SB), so every access is a shared-window LDS/STS wherever the view goes.
+extern __shared__ __align__(16) unsigned char k2sm[];
+
+struct SB {
+  uint32_t o;  // byte offset in k2sm
+  __device__ __forceinline__ uint8_t& operator[](int i) const { return k2sm[o + i]; }
+  __device__ __forceinline__ uint32_t& w(int i) const { return reinterpret_cast<uint32_t*>(k2sm + o)[i]; }  // o % 4 == 0
+  __device__ __forceinline__ SB operator+(int i) const { return SB{o + (uint32_t)i}; }
+};
+
 struct TS {
-  uint8_t* N;     // composition N_j
-  uint8_t* c;     // coarse (not yet moved) forward microbatches c_j
-  uint8_t* cnt;   // cnt[t] = #{j : c_j >= t}, t = 1..n (cnt[n+1] = 0)
-  uint8_t* thr;   // committed forward thresholds: first slot (1-based) each moved EF counts for, ascending
-  uint8_t* own;   // owner pipeline of LLM microbatch slot i (global ordering)
-  uint8_t* rk;    // rank of D_i within its owner's sorted deadlines
-  uint8_t* cb;    // coarse backward microbatches per pipeline
-  uint8_t* kb;    // ordering: slots given to each pipeline so far
-  uint8_t* Qcb;   // Qcb[i] = #{owner's moved backward EF <= D_i}
-  uint8_t* seen;  // ordering: active pipeline list
-  uint8_t* mvj;   // ordering: moved entries sorted by (value, key): pipeline
-  uint8_t* mvk;   //                                                  chain index
+  SB N;     // composition N_j
+  SB c;     // coarse (not yet moved) forward microbatches c_j
+  SB cnt;   // cnt[t] = #{j : c_j >= t}, t = 1..n (cnt[n+1] = 0)
+  SB thr;   // committed forward thresholds: first slot (1-based) each moved EF counts for, ascending
+  SB own;   // owner pipeline of LLM microbatch slot i (global ordering)
+  SB rk;    // rank of D_i within its owner's sorted deadlines
+  SB cb;    // coarse backward microbatches per pipeline
+  SB kb;    // ordering: slots given to each pipeline so far
+  SB Qcb;   // Qcb[i] = #{owner's moved backward EF <= D_i}
+  SB seen;  // ordering: active pipeline list
+  SB mvj;   // ordering: moved entries sorted by (value, key): pipeline
+  SB mvk;   //                                                  chain index
 };
 
 template <int B, int BM>
-__device__ __forceinline__ TS ts_at(unsigned char* b) {
+__device__ __forceinline__ TS ts_at(uint32_t b) {
   TS s;
-  s.N = b;                             // [BM]
-  s.c = b + BM;                        // [BM]
-  unsigned char* x = b + 2 * BM;       // phase-shared region
+  s.N = SB{b};                         // [BM]
+  s.c = SB{b + BM};                    // [BM]
+  const SB x{b + 2 * BM};              // phase-shared region
   s.cnt = x;                           // [B + 2]
   s.thr = x + B + 2;                   // [B]
   s.seen = x;                          // [BM]
@@ -93,13 +112,13 @@ struct TPlan {
   int e, P, rt, m, kmax, np1;
   unsigned rtm;            // row of pipeline j = (j * rtm) >> 16 (exact for j < 128, rt <= 128)
   bool strict;            // PRE_EF strictly increasing: pre entries order by (t, j)
+  bool fast;              // strict and m <= 32: tfast (pipeline sets as 32-bit masks) applies
   uint64_t first, count;
   const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
   const int64_t* preBEF;  // PREB_EF(t)
   const int64_t* devF;
   const int64_t* devB;
-  const uint32_t* keyF;   // order ranks of devF / devB (0 at count 0)
-  const uint32_t* keyB;
+  const uint64_t* kj;     // findCritical keys per pipeline and count (PlanDesc::kj)
   const int64_t* inbF;
   const int64_t* bpF;
   const int64_t* lenF;
@@ -124,18 +143,18 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.preBEF = c.tables + d.preB + (int64_t)(d.P - 1) * (c.n + 1);
   p.devF = c.tables + d.devF;
   p.devB = c.tables + d.devB;
-  p.keyF = reinterpret_cast<const uint32_t*>(c.tables + d.devK);
-  p.keyB = p.keyF + (int64_t)d.rp * (c.n + 1);
+  p.kj = reinterpret_cast<const uint64_t*>(c.tables + d.kj);
   p.inbF = c.tables + d.inbF;
   p.bpF = c.tables + d.bpF;
   p.lenF = c.tables + d.lenF;
   p.inbB = c.tables + d.inbB;
   p.lenB = c.tables + d.lenB;
-  p.strict = true;
-  for (int t = 1; t < c.n; ++t) p.strict = p.strict && __ldg(&p.preEF[t + 1]) > __ldg(&p.preEF[t]);
+  p.strict = (__ldg(&c.tables[d.pflags]) & 1) != 0;
+  p.fast = p.strict && d.m <= 32;
 }
 
 __device__ int tfind_plan(const Cfg& c, uint64_t g) {
+  #pragma unroll 1
   for (int e = 0; e < c.E; ++e) {
     const PlanDesc& d = c.plans[e];
     if (d.count && g >= d.first && g < d.first + d.count) return e;
@@ -147,9 +166,11 @@ __device__ int tfind_plan(const Cfg& c, uint64_t g) {
 template <int B>
 __device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
   int rem = n;
+  #pragma unroll 1
   for (int j = 0; j < m - 1; ++j) {
     const int parts = m - j;
     int x = 1;
+    #pragma unroll 1
     for (; x <= rem - (parts - 1); ++x) {
       const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (B + 1) + (parts - 2)]);
       if (rank < cnt) break;
@@ -171,6 +192,7 @@ __device__ bool tnext(int m, TS& s) {
     return true;
   }
   int S = last, jj = m - 2;
+  #pragma unroll 1
   for (; jj >= 0; --jj) {  // largest jj whose suffix can still give one away
     if (S > m - 1 - jj) break;
     S += s.N[jj];
@@ -178,8 +200,11 @@ __device__ bool tnext(int m, TS& s) {
   if (jj < 0) return false;
   s.N[jj] += 1;
   int j = jj + 1;  // parts jj+1 .. m-2 become 1 (word stores where aligned; N is 4-byte aligned)
+  #pragma unroll 1
   for (; j < m - 1 && (j & 3); ++j) s.N[j] = 1;
-  for (; j + 4 <= m - 1; j += 4) *reinterpret_cast<uint32_t*>(s.N + j) = 0x01010101u;
+  #pragma unroll 1
+  for (; j + 4 <= m - 1; j += 4) s.N.w(j >> 2) = 0x01010101u;
+  #pragma unroll 1
   for (; j < m - 1; ++j) s.N[j] = 1;
   s.N[m - 1] = (uint8_t)(S - 1 - (m - 2 - jj));
   return true;
@@ -198,6 +223,7 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
   {
     int k = 0, q = 0;
     bool used = false;
+    #pragma unroll 1
     for (;;) {
       const int a = k < M ? s.thr[k] : n + 1, b = used ? n + 1 : bp;
       const int nb = min(a, b);
@@ -211,9 +237,11 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
   int64_t best = kNegInf;
   int i = 0, q = 0, k = 0;
   bool used = false;
+  #pragma unroll 1
   for (int t = 1, pos = 0; pos < maxneed; ++t) {
     const int start = pos + 1;
     i = max(i, start + q);
+    #pragma unroll 1
     for (;;) {  // thresholds up to slot i lower its need: move right
       const int a = k < M ? s.thr[k] : n + 1, b = used ? n + 1 : bp;
       if (min(a, b) > i) break;
@@ -227,12 +255,13 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
   return best;
 }
 
-__device__ __forceinline__ void assign_slot(const TPlan& p, const int64_t* D, TS& s, int j, int& slot, int64_t& dep_b) {
+__device__ __forceinline__ void assign_slot(const int64_t* preBEF, const int64_t* D, const TS& s, int j, int& slot,
+                                            int64_t& dep_b) {
   const int r = s.N[j] - s.kb[j];  // rank of this slot's deadline within pipeline j (R15)
   s.kb[j] += 1;
   s.own[slot] = (uint8_t)j;
   s.rk[slot] = (uint8_t)r;
-  dep_b = max(dep_b, __ldg(&p.preBEF[r]) - D[slot]);  // initial backward shift
+  dep_b = max(dep_b, __ldg(&preBEF[r]) - D[slot]);  // initial backward shift
   ++slot;
 }
 
@@ -246,9 +275,11 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
   auto mval = [&](int q) { return __ldg(&p.inbF[row_of(p, s.mvj[q]) * kmax + s.mvk[q]]); };
   auto mkey = [&](int q) { return ((int)s.mvj[q] << 8) | (s.c[s.mvj[q]] + s.mvk[q]); };
   int nm = 0;
+  #pragma unroll 1
   for (int j = 0, a = 0, r = 0; j < m; ++j) {
     const int cj = s.c[j], kfj = s.N[j] - cj;
     s.kb[j] = 0;
+    #pragma unroll 1
     for (int k = 0; k < kfj; ++k) {  // insertion sort of the moved entries
       const int64_t v = __ldg(&p.inbF[a * kmax + k]);
       const int key = (j << 8) | (cj + k);
@@ -266,52 +297,67 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
     }
     if (++r == rt) { r = 0; ++a; }
   }
-  uint8_t* act = s.seen;
+  const SB act = s.seen;
   int na = 0;
+  #pragma unroll 1
   for (int j = 0; j < m; ++j)
     if (s.c[j] > 0) act[na++] = (uint8_t)j;
   int slot = 0, mi = 0;
   int64_t dep_b = kNegInf;
   int64_t mv = nm > 0 ? mval(0) : INT64_MAX;  // value of the next moved entry
+  #pragma unroll 1
   for (int t = 1; na > 0; ++t) {
     const int64_t v = __ldg(&p.preEF[t]) - Df;
     while (mv < v) {  // moved entries below this level's value precede all of it
-      assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
+      assign_slot(p.preBEF, D, s, s.mvj[mi], slot, dep_b);
       ++mi;
       mv = mi < nm ? mval(mi) : INT64_MAX;
     }
     int nn = 0;
     if (mv == v) {  // equal values: merge by key
+      #pragma unroll 1
       for (int q = 0; q < na; ++q) {
         const int j = act[q];
         const int key = (j << 8) | (t - 1);
         while (mv == v && mkey(mi) < key) {
-          assign_slot(p, D, s, s.mvj[mi], slot, dep_b);
+          assign_slot(p.preBEF, D, s, s.mvj[mi], slot, dep_b);
           ++mi;
           mv = mi < nm ? mval(mi) : INT64_MAX;
         }
-        assign_slot(p, D, s, j, slot, dep_b);
+        assign_slot(p.preBEF, D, s, j, slot, dep_b);
         if (s.c[j] > t) act[nn++] = (uint8_t)j;
       }
     } else {
+      #pragma unroll 1
       for (int q = 0; q < na; ++q) {
         const int j = act[q];
-        assign_slot(p, D, s, j, slot, dep_b);
+        assign_slot(p.preBEF, D, s, j, slot, dep_b);
         if (s.c[j] > t) act[nn++] = (uint8_t)j;
       }
     }
     na = nn;
   }
-  while (mi < nm) assign_slot(p, D, s, s.mvj[mi++], slot, dep_b);
+  while (mi < nm) assign_slot(p.preBEF, D, s, s.mvj[mi++], slot, dep_b);
   return dep_b;
 }
 
 // Global ordering (R14) for any PRE_EF (levels of equal value grouped, so
 // ties order by (j, t-1)); moved entries extracted in key order by repeated
 // minimum search above the last key taken.
-__device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_t Df, bool moved, TS& s) {
-  const int rt = p.rt, kmax = p.kmax;
+// (rare: only plans whose coarse EFs tie; out of line, with plain arguments so
+// that the caller's plan and scratch views stay in registers)
+__device__ __noinline__ int64_t order_general(const int64_t* preEF, const int64_t* preBEF, const int64_t* inbF, int rt,
+                                              int kmax, const int64_t* D, int m, int64_t Df, bool moved, uint32_t oN,
+                                              uint32_t oc, uint32_t okb, uint32_t oown, uint32_t ork) {
+  TS s;
+  s.N = SB{oN};
+  s.c = SB{oc};
+  s.kb = SB{okb};
+  s.own = SB{oown};
+  s.rk = SB{ork};
+  struct { const int64_t *preEF, *preBEF, *inbF; } p{preEF, preBEF, inbF};
   int maxc = 0;
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) {
     maxc = max(maxc, (int)s.c[j]);
     s.kb[j] = 0;
@@ -323,8 +369,10 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_
     mv = kInf;
     mj = -1;
     if (!moved) return;
+    #pragma unroll 1
     for (int j = 0, a = 0, r = 0; j < m; ++j) {
       const int cj = s.c[j], kfj = s.N[j] - cj;
+      #pragma unroll 1
       for (int k = 0; k < kfj; ++k) {
         const int64_t v = __ldg(&p.inbF[a * kmax + k]);
         const int key = (j << 8) | (cj + k);
@@ -338,28 +386,31 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_
     }
   };
   next_moved();
+  #pragma unroll 1
   for (int t1 = 1; t1 <= maxc;) {
     int t2 = t1;
     const int64_t pv = __ldg(&p.preEF[t1]);
     while (t2 < maxc && __ldg(&p.preEF[t2 + 1]) == pv) ++t2;
     const int64_t v = pv - Df;
+    #pragma unroll 1
     for (int j = 0; j < m; ++j)
+      #pragma unroll 1
       for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
         const int key = (j << 8) | (t - 1);
         while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
-          assign_slot(p, D, s, mj, slot, dep_b);
+          assign_slot(p.preBEF, D, s, mj, slot, dep_b);
           lastv = mv;
           lastk = mk;
           next_moved();
         }
-        assign_slot(p, D, s, j, slot, dep_b);
+        assign_slot(p.preBEF, D, s, j, slot, dep_b);
         lastv = v;
         lastk = key;
       }
     t1 = t2 + 1;
   }
   while (mj >= 0) {
-    assign_slot(p, D, s, mj, slot, dep_b);
+    assign_slot(p.preBEF, D, s, mj, slot, dep_b);
     lastv = mv;
     lastk = mk;
     next_moved();
@@ -371,12 +422,15 @@ __device__ int64_t order_general(const TPlan& p, const int64_t* D, int m, int64_
 // the order is (t, j), slot of (t, j) gets rank N_j - t + 1; own/rk are not
 // materialised.
 __device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, int m, TS& s) {
-  uint8_t* actN = s.seen;  // N_j of the pipelines still active, in pipeline order
+  const SB actN = s.seen;  // N_j of the pipelines still active, in pipeline order
+  #pragma unroll 1
   for (int j = 0; j < m; ++j) actN[j] = s.N[j];
   int na = m, pos = 0;
   int64_t best = kNegInf;
+  #pragma unroll 1
   for (int t = 1; na > 0; ++t) {
     int nn = 0;
+    #pragma unroll 1
     for (int q = 0; q < na; ++q) {
       const int Nj = actN[q];
       best = max(best, __ldg(&p.preBEF[Nj - t + 1]) - D[pos++]);
@@ -391,6 +445,7 @@ __device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, 
 // (-1: none) with trial chain end efb.
 __device__ int64_t tdep_bwd(const TPlan& p, const int64_t* D, int n, int js, int64_t efb, const TS& s) {
   int64_t best = kNegInf;
+  #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int o = s.own[i];
     const int64_t d = D[i];
@@ -403,11 +458,11 @@ __device__ int64_t tdep_bwd(const TPlan& p, const int64_t* D, int n, int js, int
 }
 
 struct TStats {
-  unsigned v[8];
+  unsigned v[12];  // per-candidate loop counts (optimus_eval_stats); [8] fast path, [9] general path, [10] claims, [11] unranks
 };
 
 // decode a findCritical key: pipeline js and its DEV value (-inf, js = -1 if none)
-__device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev, const uint8_t* cnt8, uint32_t best,
+__device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev, const SB cnt8, uint32_t best,
                                               int& js) {
   if (best < 128u) { js = -1; return kNegInf; }
   js = 127 - (int)(best & 127u);
@@ -418,16 +473,13 @@ __device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev
 // ties -> lowest j.  cnt8 = the per-pipeline counts.  Compares the 32-bit
 // keys rank(DEV[row][count]) << 7 | (127 - j) (m <= 128): the max key is the
 // max DEV at the lowest j; rank 0 (count 0) never wins over a count > 0.
-__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, const uint32_t* key, const uint8_t* cnt8,
-                                            int m, int& js) {
-  const int rt = p.rt, np1 = p.np1;
+__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, int half, const SB cnt8, int m,
+                                            int& js) {
+  const uint32_t* key = reinterpret_cast<const uint32_t*>(p.kj) + half;  // KJ[j][c] word `half`
+  const int np1 = p.np1;
   uint32_t best = 0;
-  int base = 0, r = 0;
-#pragma unroll 4
-  for (int j = 0; j < m; ++j) {
-    best = max(best, (__ldg(&key[base + cnt8[j]]) << 7) | (uint32_t)(127 - j));
-    if (++r == rt) { r = 0; base += np1; }
-  }
+#pragma unroll 2
+  for (int j = 0; j < m; ++j) best = max(best, __ldg(&key[2 * (j * np1 + cnt8[j])]));
   return crit_value(p, dev, cnt8, best, js);
 }
 
@@ -438,41 +490,42 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, 
 template <bool EXPLAIN = false>
 __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
                          TStats& st, int64_t* xo = nullptr) {
-  const int n = c.n, m = p.m, rt = p.rt, kmax = p.kmax;
+  const int n = c.n, m = p.m, kmax = p.kmax;
   // ---------------- coarse init (R9) -------------------------------------
-  for (int t = 0; t < (n + 5) / 4; ++t) reinterpret_cast<uint32_t*>(s.cnt)[t] = 0u;  // cnt[0..n+1] (4-aligned)
+  #pragma unroll 1
+  for (int t = 0; t < (n + 5) / 4; ++t) s.cnt.w(t) = 0u;  // cnt[0..n+1] (4-aligned)
   // the first findCritical of both phases runs on N: one pass for both keys
   uint32_t kf0 = 0, kb0 = 0;
   int maxN = 0;
-  {
-    int base = 0, r = 0;
-    for (int j = 0; j < m; ++j) {
-      const int Nj = s.N[j];
-      s.c[j] = (uint8_t)Nj;
-      s.cnt[Nj] += 1;
-      maxN = max(maxN, Nj);
-      const uint32_t lo = (uint32_t)(127 - j);
-      kf0 = max(kf0, (__ldg(&p.keyF[base + Nj]) << 7) | lo);
-      kb0 = max(kb0, (__ldg(&p.keyB[base + Nj]) << 7) | lo);
-      if (++r == rt) { r = 0; base += p.np1; }
-    }
+  #pragma unroll 1
+  for (int j = 0, off = 0; j < m; ++j, off += p.np1) {
+    const int Nj = s.N[j];
+    s.c[j] = (uint8_t)Nj;
+    s.cnt[Nj] += 1;
+    maxN = max(maxN, Nj);
+    const uint64_t k = __ldg(&p.kj[off + Nj]);
+    kf0 = max(kf0, (uint32_t)k);
+    kb0 = max(kb0, (uint32_t)(k >> 32));
   }
+  #pragma unroll 1
   for (int t = maxN - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
   int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
   // initial forward shift (no thresholds, no trial): the first slot of each
   // level t sits at position sum_{t' < t} cnt[t'] (tdep_fwd with M = 0)
   int64_t dep = kNegInf;
+  #pragma unroll 1
   for (int t = 1, pos = 0; pos < n; ++t) {
     dep = max(dep, __ldg(&p.preEF[t]) - G[pos]);
     pos += s.cnt[t];
   }
   int64_t Delta;
+  #pragma unroll 1
   for (;;) {
     ++itf;
     int js;
     const int64_t dev = itf == 1 ? crit_value(p, p.devF, s.c, kf0, js)  // findCritical (R11)
-                                 : critical(p, p.devF, p.keyF, s.c, m, js);
+                                 : critical(p, p.devF, 0, s.c, m, js);
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
     const int as = row_of(p, js), cjs = s.c[js], kfj = s.N[js] - cjs;
@@ -503,14 +556,15 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   bool have_order = M > 0 || !p.strict;
   int64_t dep_b = !have_order ? order_fast(p, D, m, s)
                   : p.strict  ? order_strict(p, D, m, Df, s)
-                              : order_general(p, D, m, Df, M > 0, s);
+                              : order_general(p.preEF, p.preBEF, p.inbF, p.rt, p.kmax, D, m, Df, M > 0, s.N.o, s.c.o, s.kb.o, s.own.o, s.rk.o);
   // ---------------- backward OptimizeSchedule (R15) ------------------------
   int sumcb = n;
   bool init_b = false;
+  #pragma unroll 1
   for (;;) {
     ++itb;
     int js;
-    const int64_t dev = !init_b ? crit_value(p, p.devB, s.N, kb0, js) : critical(p, p.devB, p.keyB, s.cb, m, js);
+    const int64_t dev = !init_b ? crit_value(p, p.devB, s.N, kb0, js) : critical(p, p.devB, 1, s.cb, m, js);
     Delta = max((int64_t)0, max(dev, dep_b));
     if (Delta == 0 || sumcb == 0) break;
     const int as = row_of(p, js), kfj = s.N[js] - s.c[js];
@@ -524,12 +578,15 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
       have_order = true;
     }
     if (!init_b) {  // backward moves are rare: per-pipeline state on first use
+      #pragma unroll 1
       for (int j = 0; j < m; ++j) s.cb[j] = s.N[j];
+      #pragma unroll 1
       for (int i = 0; i < n; ++i) s.Qcb[i] = 0;
       init_b = true;
     }
     const int64_t dep2 = tdep_bwd(p, D, n, js, EFb, s);
     if (dep2 > Delta) break;
+    #pragma unroll 1
     for (int i = 0; i < n; ++i) s.Qcb[i] += (s.own[i] == js && EFb <= D[i]) ? 1 : 0;
     s.cb[js] -= 1;
     if (EXPLAIN) xo[8 + n + (n - sumcb)] = js;
@@ -541,6 +598,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     xo[2] = Delta;
     xo[3] = M;
     xo[4] = n - sumcb;
+    #pragma unroll 1
     for (int j = 0; j < m; ++j) {
       xo[8 + 2 * n + j] = s.N[j];
       xo[8 + 2 * n + m + j] = s.c[j];
@@ -555,7 +613,147 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   st.v[5] += m * itb;
   st.v[6] += itb;
   st.v[7] += atb;
+  st.v[9] += 1;
   return T_end + Df + Delta;  // R16
+}
+
+// ---------------------------------------------------------------------------
+// Fast path (plans with PRE_EF strictly increasing and m <= 32): the whole
+// candidate when neither phase commits a move, i.e. the first attempt of
+// each OptimizeSchedule phase fails (R11-R13) or is never made.  Returns
+// false as soon as a first move would commit; the candidate then goes to the
+// general path (teval), which evaluates it from the start.
+//
+// Pipeline sets are 32-bit masks.  E[x] = {j : N_j = x}; the walk over levels
+// t = 1..max N turns it into A_t = {j : N_j >= t} (stored back in E[t]), so
+// the slot of the pre entry (t, j) in the global ordering without moved
+// entries (R14: level-major, j within a level) is pos_t + |A_t below j|.
+//   * forward (R10): the first slot of level t is pos_t; a trial move of js
+//     (one threshold bp, R10's closed form) removes js from level N_js.
+//   * ordering + initial backward shift (R14, R15): slot (t, j) has rank
+//     N_j - t + 1 and D is non-increasing in the slot, so for each rank r the
+//     term PREB_EF(r) - D[slot] is largest at the largest slot of rank r:
+//     level N_max - r + 1 of jmax, the highest j with N_j = N_max.  One entry
+//     per level instead of one per slot.
+//   * backward trial of jb (no backward move yet, Qcb = 0): only jb's entries
+//     change (need = r - [EFb <= D]); the others' maximum is the shift above,
+//     or, when jb = jmax, the same walk over j2 (largest N among j != jmax).
+// Leaves E zeroed.  dep / depb / Delta are the quantities of teval.
+template <int B>
+__device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const int64_t* D, int n, const TS& s,
+                                      uint32_t* E, int64_t& Df, int64_t& Db, TStats& st) {
+  const int m = p.m, np1 = p.np1;
+  uint32_t kf0 = 0, kb0 = 0;
+  int Nmax = 0;
+#pragma unroll 2
+  for (int j = 0, off = 0; j < m; ++j, off += np1) {
+    const int Nj = s.N[j];
+    E[Nj] |= 1u << j;
+    const uint64_t k = __ldg(&p.kj[off + Nj]);  // first findCritical of both phases (R11)
+    kf0 = max(kf0, (uint32_t)k);
+    kb0 = max(kb0, (uint32_t)(k >> 32));
+    Nmax = max(Nmax, Nj);
+  }
+  const int jmax = 31 - __clz(E[Nmax]);  // highest j with N_j = N_max
+  const uint32_t all = m == 32 ? 0xffffffffu : (1u << m) - 1u;
+  const uint32_t below_max = (1u << jmax) - 1u;
+  int64_t dep = kNegInf, depb = kNegInf;
+  {
+    uint32_t A = all;
+    int pos = 0;
+    #pragma unroll 1
+    for (int t = 1; t <= Nmax; ++t) {
+      const uint32_t e = E[t];
+      E[t] = A;
+      dep = max(dep, __ldg(&p.preEF[t]) - G[pos]);
+      depb = max(depb, __ldg(&p.preBEF[Nmax - t + 1]) - D[pos + __popc(A & below_max)]);
+      pos += __popc(A);
+      A &= ~e;
+    }
+  }
+  bool general = false;
+  // ---- forward, first iteration
+  int js;
+  const int64_t dev = crit_value(p, p.devF, s.N, kf0, js);
+  int64_t Delta = max((int64_t)0, max(dev, dep));
+  int atf = 0;
+  if (Delta != 0) {
+    const int as = row_of(p, js);
+    if ((int)__ldg(&p.lenF[as]) > 0) {
+      ++atf;
+      const int bp = (int)__ldg(&p.bpF[as * p.kmax]);
+      if (bp <= n) {  // else need_n = n > n - 1 coarse entries: INF, the move fails
+        const int Njs = s.N[js];
+        const uint32_t jsbit = 1u << js;
+        int64_t dep2 = kNegInf;
+        #pragma unroll 1
+        for (int t = 1, pos = 0; pos < n - 1; ++t) {
+          uint32_t A = E[t];
+          if (t == Njs) A &= ~jsbit;
+          const int st1 = pos + 1;  // first position of level t (1-based): slot st1, or st1 + 1 past the threshold
+          dep2 = max(dep2, __ldg(&p.preEF[t]) - G[st1 < bp ? st1 - 1 : st1]);
+          pos += __popc(A);
+        }
+        general = dep2 <= Delta;  // checkEncLLMDep holds: the move commits
+      }
+    }
+  }
+  Df = Delta;
+  int atb = 0;
+  if (!general) {
+    // ---- backward, first iteration (initial shift depb)
+    int jb;
+    const int64_t devb = crit_value(p, p.devB, s.N, kb0, jb);
+    int64_t Delta_b = max((int64_t)0, max(devb, depb));
+    if (Delta_b != 0) {
+      const int as = row_of(p, jb);
+      const int64_t rowoff = (int64_t)as * (p.kmax + 1);  // kf = 0 forward chains
+      if ((int)__ldg(&p.lenB[rowoff]) > 0) {
+        ++atb;
+        const int64_t EFb = __ldg(&p.inbB[rowoff * p.kmax]);
+        if (EFb <= D[jb]) {  // else jb's rank-N slot (level 1, slot jb) loses its coarse entry: INF
+          const int Njb = s.N[jb];
+          const bool other2 = jb == jmax;
+          int N2 = 0, j2 = 0;  // jb = jmax: the others' largest N and its highest j (E[t] now holds A_t)
+          if (other2) {
+            for (N2 = Nmax; N2 > 0 && __popc(E[N2]) < 2; --N2) {}
+            if (N2 > 0) j2 = 31 - __clz(E[N2] & ~(1u << jmax));
+          }
+          const int tl = max(Njb, N2);
+          const uint32_t below_b = (1u << jb) - 1u, below_2 = (1u << j2) - 1u;
+          int64_t dep2 = other2 ? kNegInf : depb;
+          #pragma unroll 1
+          for (int t = 1, pos = 0; t <= tl; ++t) {
+            const uint32_t A = E[t];
+            if (t <= Njb) {
+              const int sl = pos + __popc(A & below_b);
+              const int64_t d = D[sl];
+              const int need = Njb - t + 1 - (EFb <= d ? 1 : 0);
+              if (need > 0) dep2 = max(dep2, __ldg(&p.preBEF[need]) - d);
+            }
+            if (other2 && t <= N2) dep2 = max(dep2, __ldg(&p.preBEF[N2 - t + 1]) - D[pos + __popc(A & below_2)]);
+            pos += __popc(A);
+          }
+          general = dep2 <= Delta_b;
+        }
+      }
+    }
+    Db = Delta_b;
+  }
+  #pragma unroll 1
+  for (int t = 1; t <= Nmax; ++t) E[t] = 0u;
+  if (!general) {
+    st.v[0] += 1;
+    st.v[1] += m;
+    st.v[2] += m;
+    st.v[3] += 1;
+    st.v[4] += atf;
+    st.v[5] += m;
+    st.v[6] += 1;
+    st.v[7] += atb;
+    st.v[8] += 1;
+  }
+  return !general;
 }
 
 // positions of this rank (block-cyclic over [begin, end)) below global index x >= begin
@@ -583,12 +781,12 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
 template <bool EXPLICIT, int B, int BM>
 __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
     k2_eval_thread(Cfg c, EvalArgs A) {
-  extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
   __shared__ long long bl_sm[kTThreads / 32];
   __shared__ unsigned long long bg_sm[kTThreads / 32];
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
   __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
+  __shared__ uint64_t psuf[EXPLICIT ? 1 : kMaxE + 1];  // this rank's positions of the plans at k2order[k..]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -605,6 +803,12 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
       pstate[e] = 0;
     }
   __syncthreads();
+  if (!EXPLICIT && threadIdx.x == 0) {
+    uint64_t acc = 0;
+    psuf[c.n_k2order] = 0;
+    for (int k = c.n_k2order - 1; k >= 0; --k) psuf[k] = acc += pn[c.k2order[k]];
+  }
+  __syncthreads();
 #ifdef PDL_PROBE
   if (!EXPLICIT && threadIdx.x == 0) {
     unsigned long long t;
@@ -612,12 +816,81 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     atomicMin(reinterpret_cast<unsigned long long*>(c.k1next) + 3, t);
   }
 #endif
-  TS s = ts_at<B, BM>(tsm + (size_t)threadIdx.x * tstride<B, BM>());
+  TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * tstride<B, BM>()));
+  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * tstride<B, BM>() + 2 * BM);  // tfast's masks (zero)
+  for (int t = 0; t < B + 2; ++t) E[t] = 0u;
   TPlan p;
   p.e = -1;
-  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
+  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   int64_t bl = INT64_MAX;
   uint64_t bg = UINT64_MAX;
+  // Per-warp queue of the candidates the fast path hands to the general path
+  // (teval): they are evaluated 32 at a time, one per lane, so the long
+  // general evaluation runs with full warps.  An entry is the composition
+  // (QB bytes at an odd word stride: lanes reading entry l hit distinct
+  // banks), its index g, lat_out position and plan.  Plans the fast path does
+  // not cover (m > 32 or PRE_EF not strictly increasing) run teval directly.
+  constexpr int QS = tqstride<BM>();
+  const uint32_t qoff = (uint32_t)(kTThreads * tstride<B, BM>() + warp * kQCap * QS);  // this warp's entries
+  __shared__ unsigned long long Qg[kTThreads / 32][kQCap], Qo[kTThreads / 32][kQCap];
+  __shared__ uint8_t Qe[kTThreads / 32][kQCap];
+  int qh = 0, qn = 0;  // warp-uniform ring head and length
+  const unsigned lt_mask = (1u << lane) - 1u;
+  // general-path evaluation of k queued entries (warp-uniform k <= 32)
+  auto run_queue = [&](int k) {
+    if (lane < k) {
+      const int sl = (qh + lane) & (kQCap - 1);
+      const uint64_t gq = Qg[warp][sl], oq = Qo[warp][sl];
+      const int eq = Qe[warp][sl];
+      if (eq != p.e) tplan(c, eq, p);
+      TS sq = s;
+      sq.N = SB{qoff + (uint32_t)(sl * QS)};  // teval only reads N; the lane's own composition stays in s.N
+      const int64_t lat = teval(c, p, G, D, T_end, sq, st);
+      if (A.lat_out) A.lat_out[oq] = lat;
+      tbetter(lat, gq, bl, bg);
+      for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval's scratch overlaps the fast path's masks
+    }
+    __syncwarp();
+    qh = (qh + k) & (kQCap - 1);
+    qn -= k;
+  };
+  // one candidate per lane (valid lanes): fast path, else queue (fast plans)
+  // or direct general evaluation (other plans); true if the queue ran
+  auto step = [&](bool valid, uint64_t g, uint64_t out, int e) -> bool {
+    bool pend = false;
+    if (valid) {
+      int64_t lat = 0;
+      bool done = true;
+      if (p.fast) {
+        int64_t Df, Db;
+        done = tfast<B>(p, G, D, n, s, E, Df, Db, st);
+        lat = T_end + Df + Db;  // R16
+      } else {
+        lat = teval(c, p, G, D, T_end, s, st);
+        for (int t = 0; t < B + 2; ++t) E[t] = 0u;
+      }
+      if (done) {
+        if (A.lat_out) A.lat_out[out] = lat;
+        tbetter(lat, g, bl, bg);
+      }
+      pend = !done;
+    }
+    const unsigned want = __ballot_sync(0xffffffffu, pend);
+    if (!want) return false;
+    if (pend) {
+      const int sl = (qh + qn + __popc(want & lt_mask)) & (kQCap - 1);
+      Qg[warp][sl] = g;
+      Qo[warp][sl] = out;
+      Qe[warp][sl] = (uint8_t)e;
+      const SB dst{qoff + (uint32_t)(sl * QS)};
+      for (int w = 0; w < (p.m + 3) / 4; ++w) dst.w(w) = s.N.w(w);
+    }
+    qn += __popc(want);
+    __syncwarp();
+    if (qn < 32) return false;
+    run_queue(32);
+    return true;
+  };
   if (EXPLICIT) {
     const uint64_t nchunks = (A.count + 31) / 32;
     for (;;) {
@@ -626,24 +899,26 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
       ch = __shfl_sync(0xffffffffu, ch, 0);
       if (ch >= nchunks) break;
       const uint64_t i = ch * 32 + lane;
+      bool valid = false;
+      uint64_t g = 0;
+      int e = -1;
       if (i < A.count) {
-        const uint64_t g = A.index[i];
-        const int e = tfind_plan(c, g);
+        g = A.index[i];
+        e = tfind_plan(c, g);
         if (e >= 0) {
           if (e != p.e) tplan(c, e, p);
           tunrank<B>(c, n, p.m, g - p.first, s);
-          const int64_t lat = teval(c, p, G, D, T_end, s, st);
-          if (A.lat_out) A.lat_out[i] = lat;
-          tbetter(lat, g, bl, bg);
+          valid = true;
         }
       }
+      step(valid, g, i, e);
     }
   } else {
     // Plan by plan in k2order, each plan once K1 has completed it (this
     // launch may overlap K1).  This rank's positions: block-cyclic over
     // [begin, end); plan e's are [plo[e], plo[e] + pn[e]).  A warp claims
     // 32 * r consecutive positions of one plan at a time (r consecutive
-    // candidates per lane), r from 8 down to 1 as the plan's remaining work
+    // candidates per lane), r from 16 down to 1 as the plan's remaining work
     // shrinks (guided self-scheduling: no long tail when work is scarce).
     const uint64_t nwarps = (uint64_t)gridDim.x * (kTThreads / 32);
     for (;;) {
@@ -664,7 +939,11 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
             }
             const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
             const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
-            const unsigned long long tk = min(32ull * kTRun, max(32ull * kTMinRun, rem * kTGss / (kTGssDen * nwarps) / 32 * 32));
+            // claim size from the work left in this and the later plans: the
+            // full kTRun-run claims while there is plenty (every run start costs
+            // an unranking), shrinking only near the end of the whole launch
+            const unsigned long long left = rem + psuf[k + 1];
+            const unsigned long long tk = min(32ull * kTRun, max(32ull * kTMinRun, left * kTGss / (kTGssDen * nwarps) / 32 * 32));
             const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
             if (st0 < pn[e2]) { e = e2; chunk = st0; take = tk; break; }
             pst[e2] = 2;
@@ -679,24 +958,29 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
       __syncwarp();  // the lanes' table reads follow lane 0's acquire
       if (e < 0) break;
       if (e != p.e) tplan(c, e, p);
-      const uint64_t r = take / 32;
+      const int r = (int)(take / 32);
+      st.v[10] += lane == 0;
       const uint64_t p0 = plo[e] + chunk + (uint64_t)lane * r, pend = plo[e] + pn[e];
       uint64_t g = 0;
-      for (uint64_t q = p0; q < min(p0 + r, pend); ++q) {
-        if (q == p0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
-          const uint64_t rb = q / A.block;
-          g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
-          tunrank<B>(c, n, p.m, g - p.first, s);
-        } else {
-          ++g;
-          tnext(p.m, s);
+      for (int it = 0; it < r; ++it) {  // the same trip count on every lane (warp-synchronous queue)
+        const uint64_t q = p0 + it;
+        const bool valid = q < pend;
+        if (valid) {
+          if (it == 0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
+            const uint64_t rb = q / A.block;
+            g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
+            tunrank<B>(c, n, p.m, g - p.first, s);
+            st.v[11] += 1;
+          } else {
+            ++g;
+            tnext(p.m, s);
+          }
         }
-        const int64_t lat = teval(c, p, G, D, T_end, s, st);
-        if (A.lat_out) A.lat_out[g - A.begin] = lat;
-        tbetter(lat, g, bl, bg);
+        if (step(valid, g, g - A.begin, e) && e != p.e) tplan(c, e, p);  // the queue ran: this lane's plan back
       }
     }
   }
+  if (qn > 0) run_queue(qn);  // the rest of the queue, part of a warp
   // warp + block argmin -> partials; counters
   for (int o = 16; o > 0; o >>= 1) {
     const int64_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
@@ -704,7 +988,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     tbetter(ol, og, bl, bg);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 12; ++i) {
     unsigned v = st.v[i];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0 && A.stats) atomicAdd(&A.stats[i], (unsigned long long)v);
@@ -726,7 +1010,6 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
 // backward ones, then N[m], c_final[m], cb_final[m].  One thread works.
 template <int B, int BM>
 __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64_t* out) {
-  extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ int64_t G[B], D[B];
   const int n = c.n;
   const int64_t T_end = c.scal[1];
@@ -741,9 +1024,9 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   if (e < 0) return;
   TPlan p;
   tplan(c, e, p);
-  TS s = ts_at<B, BM>(tsm);
+  TS s = ts_at<B, BM>(0u);
   tunrank<B>(c, n, p.m, g - p.first, s);
-  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0}};
+  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   out[5] = e;
   out[6] = p.m;
   out[7] = n;
@@ -754,7 +1037,7 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
 
 template <int B, int BM>
 static void k2t_attrs() {
-  constexpr int smem = kTThreads * tstride<B, BM>();
+  constexpr int smem = tsmem<B, BM>();
   cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
@@ -774,8 +1057,7 @@ __host__ __device__ constexpr int tinstance(int n, int mmax) {
 template <int B, int BM>
 static int grid_b(int sms) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B, BM>, kTThreads,
-                                                kTThreads * tstride<B, BM>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B, BM>, kTThreads, tsmem<B, BM>());
   return max(1, per) * sms;
 }
 
@@ -805,7 +1087,7 @@ int eval_thread_grid(int sms, int i) {
 
 template <int B, int BM>
 static void explain_b(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
-  k2_explain<B, BM><<<1, kTThreads, (size_t)kTThreads * tstride<B, BM>(), st>>>(c, g, d_out);
+  k2_explain<B, BM><<<1, kTThreads, (size_t)tsmem<B, BM>(), st>>>(c, g, d_out);
 }
 
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
@@ -822,7 +1104,7 @@ cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_
 
 template <int B, int BM>
 static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)kTThreads * tstride<B, BM>();
+  const size_t smem = (size_t)tsmem<B, BM>();
   if (a.index) {
     k2_eval_thread<true, B, BM><<<a.grid, kTThreads, smem, st>>>(c, a);
     return cudaGetLastError();

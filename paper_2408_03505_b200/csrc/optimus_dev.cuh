@@ -28,6 +28,9 @@ struct PlanDesc {
   int64_t bpF;        // [rp][kmax]: first LLM slot (1-based) whose F - L >= INB_F[a][k] (n+1: none)
   int64_t slot_base;  // first K1 scratch slot of this plan
   int64_t flag_base;  // first K1 flag of this plan: per row [kmax + 1] (0: forward done, v: stages that published version v)
+  int64_t pflags;     // 1 word written by K1: bit 0 = PRE_EF strictly increasing over t = 1..n
+  int64_t kj;         // [m][n+1] u64 findCritical keys per pipeline and count: low word forward, high word
+                      // backward, each rank(DEV[a_j][c]) << 7 | (127 - j) (R11: max key = max DEV, lowest j)
 };
 
 // K1 work items of a plan (forward rows, backward (row, kf), its tables):

@@ -329,9 +329,10 @@ class Ctx:
         return b.value, e.value
 
     def eval_stats(self, stream=None) -> dict:
-        a = (ctypes.c_uint64 * 6)()
+        a = (ctypes.c_uint64 * 10)()
         _check(lib().optimus_eval_stats(self.h, a, ctypes.c_void_p(_stream(stream))))
-        keys = ("candidates", "ops", "iters_f", "attempts_f", "iters_b", "attempts_b")
+        keys = ("candidates", "ops", "iters_f", "attempts_f", "iters_b", "attempts_b", "fast", "general", "claims",
+                "unranks")
         return dict(zip(keys, list(a)))
 
     def io_bytes(self):
