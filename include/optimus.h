@@ -207,6 +207,12 @@ int optimus_debug_plan_tables(const optimus_ctx* c, int32_t i, int64_t* h_out, s
 /* Kernel launches the last build / eval enqueued (for launch accounting). */
 int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t* eval_launches);
 
+/* K2 mode 1 instance this context launches (sized by n_mb and the largest m
+ * of a plan with candidates): 0 = (B, BM) (32, 32), 1 = (64, 64),
+ * 2 = (128, 64), 3 = (128, 128), 4 = (64, 16), 5 = (128, 16) slots and
+ * pipelines per thread; grid = its persistent grid (blocks).  Host only. */
+int optimus_eval_instance(const optimus_ctx* c, int32_t* instance, int32_t* grid);
+
 /* K2 variant used by the eval calls: 1 (default) = one candidate per thread
  * (eval_thread.cu), 0 = one candidate per warp (eval.cu).  Both compute the
  * same lat for every candidate (bit-exact); they differ only in speed.

@@ -826,6 +826,13 @@ int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t*
   return OPTIMUS_OK;
 }
 
+int optimus_eval_instance(const optimus_ctx* c, int32_t* instance, int32_t* grid) {
+  if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
+  if (instance) *instance = eval_thread_instance(c->X.n, plans_mmax(c->X));
+  if (grid) *grid = c->grid_thread;
+  return OPTIMUS_OK;
+}
+
 int optimus_set_eval_mode(optimus_ctx* c, int mode) {
   if (!c || (mode != 0 && mode != 1)) return fail(OPTIMUS_EINVAL, "mode must be 0 (warp per candidate) or 1 (thread per candidate)");
   c->mode = mode;

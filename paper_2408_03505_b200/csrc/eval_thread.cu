@@ -44,11 +44,14 @@ constexpr int kQCap = 64;                 // per-warp general-path queue (a powe
 #ifndef K2T_MINB
 #define K2T_MINB 4  // resident blocks per SM the register cap aims at (smem allows 4)
 #endif
-// per-thread scratch for n <= B slots and m <= BM pipelines: 4 BM + 4 B
-// bytes plus one odd word: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 772;
-// (128, 128) 1028; (64, 16) 324; (128, 16) 580
+// per-thread scratch for n <= B slots and m <= BM pipelines, an odd number of
+// words: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 780; (128, 128) 1028;
+// (64, 16) 364; (128, 16) 684 (at least N, c, the fast path's masks E[B + 2] and thresholds[B]; the
+// general path's byte arrays; an odd number of words)
 template <int B, int BM = B>
-__host__ __device__ constexpr int tstride() { return (4 * BM + 4 * B + 4) | 4; }
+__host__ __device__ constexpr int tstride() {
+  return ((4 * BM + 4 * B > 2 * BM + 5 * B + 8 ? 4 * BM + 4 * B : 2 * BM + 5 * B + 8) + 4) | 4;
+}
 // general-path queue entry: a composition of m <= 32 parts at an odd word stride
 template <int BM>
 __host__ __device__ constexpr int tqstride() { return (BM < 32 ? BM : 32) + 4; }
@@ -108,22 +111,26 @@ __device__ __forceinline__ TS ts_at(uint32_t b) {
   return s;
 }
 
+struct TV {
+  uint32_t o;  // element offset in Cfg::tables
+};
+
 struct TPlan {
   int e, P, rt, m, kmax, np1;
   unsigned rtm;            // row of pipeline j = (j * rtm) >> 16 (exact for j < 128, rt <= 128)
   bool strict;            // PRE_EF strictly increasing: pre entries order by (t, j)
   bool fast;              // strict and m <= 32: tfast (pipeline sets as 32-bit masks) applies
   uint64_t first, count;
-  const int64_t* preEF;   // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
-  const int64_t* preBEF;  // PREB_EF(t)
-  const int64_t* devF;
-  const int64_t* devB;
-  const uint64_t* kj;     // findCritical keys per pipeline and count (PlanDesc::kj)
-  const int64_t* inbF;
-  const int64_t* bpF;
-  const int64_t* lenF;
-  const int64_t* inbB;
-  const int64_t* lenB;
+  // the plan's tables as 32-bit element offsets from T (registers: one
+  // pointer instead of ten)
+  const int64_t* T;       // Cfg::tables
+  TV preEF;               // PRE_EF(t), t = 0..n (row P-1 of PRE_F)
+  TV preBEF;              // PREB_EF(t)
+  TV devF, devB;
+  TV kj;                  // findCritical keys per pipeline and count (PlanDesc::kj), u64
+  TV inbF, bpF, lenF, inbB, lenB;
+  __device__ __forceinline__ int64_t at(TV v, int i) const { return __ldg(&T[v.o + i]); }
+  __device__ __forceinline__ const int64_t* ptr(TV v) const { return T + v.o; }
 };
 
 __device__ __forceinline__ int row_of(const TPlan& p, int j) { return (int)(((unsigned)j * p.rtm) >> 16); }
@@ -139,16 +146,17 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.np1 = c.n + 1;
   p.first = d.first;
   p.count = d.count;
-  p.preEF = c.tables + d.preF + (int64_t)(d.P - 1) * (c.n + 1);
-  p.preBEF = c.tables + d.preB + (int64_t)(d.P - 1) * (c.n + 1);
-  p.devF = c.tables + d.devF;
-  p.devB = c.tables + d.devB;
-  p.kj = reinterpret_cast<const uint64_t*>(c.tables + d.kj);
-  p.inbF = c.tables + d.inbF;
-  p.bpF = c.tables + d.bpF;
-  p.lenF = c.tables + d.lenF;
-  p.inbB = c.tables + d.inbB;
-  p.lenB = c.tables + d.lenB;
+  p.T = c.tables;
+  p.preEF = TV{(uint32_t)(d.preF + (int64_t)(d.P - 1) * (c.n + 1))};
+  p.preBEF = TV{(uint32_t)(d.preB + (int64_t)(d.P - 1) * (c.n + 1))};
+  p.devF = TV{(uint32_t)d.devF};
+  p.devB = TV{(uint32_t)d.devB};
+  p.kj = TV{(uint32_t)d.kj};
+  p.inbF = TV{(uint32_t)d.inbF};
+  p.bpF = TV{(uint32_t)d.bpF};
+  p.lenF = TV{(uint32_t)d.lenF};
+  p.inbB = TV{(uint32_t)d.inbB};
+  p.lenB = TV{(uint32_t)d.lenB};
   p.strict = (__ldg(&c.tables[d.pflags]) & 1) != 0;
   p.fast = p.strict && d.m <= 32;
 }
@@ -249,7 +257,7 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
       ++q;
       i = start + q;
     }
-    best = max(best, __ldg(&p.preEF[t]) - G[i - 1]);
+    best = max(best, p.at(p.preEF, t) - G[i - 1]);
     pos += s.cnt[t];
   }
   return best;
@@ -272,7 +280,7 @@ __device__ __forceinline__ void assign_slot(const int64_t* preBEF, const int64_t
 // initial backward shift max_i PREB_EF(rk_i) - D_i.
 __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t Df, TS& s) {
   const int rt = p.rt, kmax = p.kmax;
-  auto mval = [&](int q) { return __ldg(&p.inbF[row_of(p, s.mvj[q]) * kmax + s.mvk[q]]); };
+  auto mval = [&](int q) { return p.at(p.inbF, row_of(p, s.mvj[q]) * kmax + s.mvk[q]); };
   auto mkey = [&](int q) { return ((int)s.mvj[q] << 8) | (s.c[s.mvj[q]] + s.mvk[q]); };
   int nm = 0;
   #pragma unroll 1
@@ -281,7 +289,7 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
     s.kb[j] = 0;
     #pragma unroll 1
     for (int k = 0; k < kfj; ++k) {  // insertion sort of the moved entries
-      const int64_t v = __ldg(&p.inbF[a * kmax + k]);
+      const int64_t v = p.at(p.inbF, a * kmax + k);
       const int key = (j << 8) | (cj + k);
       int q = nm;
       while (q > 0) {
@@ -307,9 +315,9 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
   int64_t mv = nm > 0 ? mval(0) : INT64_MAX;  // value of the next moved entry
   #pragma unroll 1
   for (int t = 1; na > 0; ++t) {
-    const int64_t v = __ldg(&p.preEF[t]) - Df;
+    const int64_t v = p.at(p.preEF, t) - Df;
     while (mv < v) {  // moved entries below this level's value precede all of it
-      assign_slot(p.preBEF, D, s, s.mvj[mi], slot, dep_b);
+      assign_slot(p.ptr(p.preBEF), D, s, s.mvj[mi], slot, dep_b);
       ++mi;
       mv = mi < nm ? mval(mi) : INT64_MAX;
     }
@@ -320,24 +328,24 @@ __device__ int64_t order_strict(const TPlan& p, const int64_t* D, int m, int64_t
         const int j = act[q];
         const int key = (j << 8) | (t - 1);
         while (mv == v && mkey(mi) < key) {
-          assign_slot(p.preBEF, D, s, s.mvj[mi], slot, dep_b);
+          assign_slot(p.ptr(p.preBEF), D, s, s.mvj[mi], slot, dep_b);
           ++mi;
           mv = mi < nm ? mval(mi) : INT64_MAX;
         }
-        assign_slot(p.preBEF, D, s, j, slot, dep_b);
+        assign_slot(p.ptr(p.preBEF), D, s, j, slot, dep_b);
         if (s.c[j] > t) act[nn++] = (uint8_t)j;
       }
     } else {
       #pragma unroll 1
       for (int q = 0; q < na; ++q) {
         const int j = act[q];
-        assign_slot(p.preBEF, D, s, j, slot, dep_b);
+        assign_slot(p.ptr(p.preBEF), D, s, j, slot, dep_b);
         if (s.c[j] > t) act[nn++] = (uint8_t)j;
       }
     }
     na = nn;
   }
-  while (mi < nm) assign_slot(p.preBEF, D, s, s.mvj[mi++], slot, dep_b);
+  while (mi < nm) assign_slot(p.ptr(p.preBEF), D, s, s.mvj[mi++], slot, dep_b);
   return dep_b;
 }
 
@@ -355,7 +363,11 @@ __device__ __noinline__ int64_t order_general(const int64_t* preEF, const int64_
   s.kb = SB{okb};
   s.own = SB{oown};
   s.rk = SB{ork};
-  struct { const int64_t *preEF, *preBEF, *inbF; } p{preEF, preBEF, inbF};
+  struct {
+    const int64_t *preEF, *preBEF, *inbF;
+    __device__ __forceinline__ int64_t at(const int64_t* v, int i) const { return __ldg(&v[i]); }
+    __device__ __forceinline__ const int64_t* ptr(const int64_t* v) const { return v; }
+  } p{preEF, preBEF, inbF};
   int maxc = 0;
   #pragma unroll 1
   for (int j = 0; j < m; ++j) {
@@ -374,7 +386,7 @@ __device__ __noinline__ int64_t order_general(const int64_t* preEF, const int64_
       const int cj = s.c[j], kfj = s.N[j] - cj;
       #pragma unroll 1
       for (int k = 0; k < kfj; ++k) {
-        const int64_t v = __ldg(&p.inbF[a * kmax + k]);
+        const int64_t v = p.at(p.inbF, a * kmax + k);
         const int key = (j << 8) | (cj + k);
         if ((v > lastv || (v == lastv && key > lastk)) && (v < mv || (v == mv && key < mk))) {
           mv = v;
@@ -389,8 +401,8 @@ __device__ __noinline__ int64_t order_general(const int64_t* preEF, const int64_
   #pragma unroll 1
   for (int t1 = 1; t1 <= maxc;) {
     int t2 = t1;
-    const int64_t pv = __ldg(&p.preEF[t1]);
-    while (t2 < maxc && __ldg(&p.preEF[t2 + 1]) == pv) ++t2;
+    const int64_t pv = p.at(p.preEF, t1);
+    while (t2 < maxc && p.at(p.preEF, t2 + 1) == pv) ++t2;
     const int64_t v = pv - Df;
     #pragma unroll 1
     for (int j = 0; j < m; ++j)
@@ -398,19 +410,19 @@ __device__ __noinline__ int64_t order_general(const int64_t* preEF, const int64_
       for (int t = t1; t <= min(t2, (int)s.c[j]); ++t) {
         const int key = (j << 8) | (t - 1);
         while (mj >= 0 && (mv < v || (mv == v && mk < key))) {
-          assign_slot(p.preBEF, D, s, mj, slot, dep_b);
+          assign_slot(p.ptr(p.preBEF), D, s, mj, slot, dep_b);
           lastv = mv;
           lastk = mk;
           next_moved();
         }
-        assign_slot(p.preBEF, D, s, j, slot, dep_b);
+        assign_slot(p.ptr(p.preBEF), D, s, j, slot, dep_b);
         lastv = v;
         lastk = key;
       }
     t1 = t2 + 1;
   }
   while (mj >= 0) {
-    assign_slot(p.preBEF, D, s, mj, slot, dep_b);
+    assign_slot(p.ptr(p.preBEF), D, s, mj, slot, dep_b);
     lastv = mv;
     lastk = mk;
     next_moved();
@@ -433,7 +445,7 @@ __device__ __forceinline__ int64_t order_fast(const TPlan& p, const int64_t* D, 
     #pragma unroll 1
     for (int q = 0; q < na; ++q) {
       const int Nj = actN[q];
-      best = max(best, __ldg(&p.preBEF[Nj - t + 1]) - D[pos++]);
+      best = max(best, p.at(p.preBEF, Nj - t + 1) - D[pos++]);
       if (Nj > t) actN[nn++] = (uint8_t)Nj;
     }
     na = nn;
@@ -452,7 +464,7 @@ __device__ int64_t tdep_bwd(const TPlan& p, const int64_t* D, int n, int js, int
     const int cbo = s.cb[o] - (o == js ? 1 : 0);
     const int need = s.rk[i] - s.Qcb[i] - (o == js && efb <= d ? 1 : 0);
     if (need > cbo) return kInf;
-    if (need > 0) best = max(best, __ldg(&p.preBEF[need]) - d);
+    if (need > 0) best = max(best, p.at(p.preBEF, need) - d);
   }
   return best;
 }
@@ -462,20 +474,20 @@ struct TStats {
 };
 
 // decode a findCritical key: pipeline js and its DEV value (-inf, js = -1 if none)
-__device__ __forceinline__ int64_t crit_value(const TPlan& p, const int64_t* dev, const SB cnt8, uint32_t best,
+__device__ __forceinline__ int64_t crit_value(const TPlan& p, TV dev, const SB cnt8, uint32_t best,
                                               int& js) {
   if (best < 128u) { js = -1; return kNegInf; }
   js = 127 - (int)(best & 127u);
-  return __ldg(&dev[row_of(p, js) * p.np1 + cnt8[js]]);
+  return p.at(dev, row_of(p, js) * p.np1 + cnt8[js]);
 }
 
 // findCritical (R11): argmax over pipelines with count > 0 of DEV[row][count],
 // ties -> lowest j.  cnt8 = the per-pipeline counts.  Compares the 32-bit
 // keys rank(DEV[row][count]) << 7 | (127 - j) (m <= 128): the max key is the
 // max DEV at the lowest j; rank 0 (count 0) never wins over a count > 0.
-__device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, int half, const SB cnt8, int m,
+__device__ __forceinline__ int64_t critical(const TPlan& p, TV dev, int half, const SB cnt8, int m,
                                             int& js) {
-  const uint32_t* key = reinterpret_cast<const uint32_t*>(p.kj) + half;  // KJ[j][c] word `half`
+  const uint32_t* key = reinterpret_cast<const uint32_t*>(p.ptr(p.kj)) + half;  // KJ[j][c] word `half`
   const int np1 = p.np1;
   uint32_t best = 0;
 #pragma unroll 2
@@ -487,40 +499,160 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, const int64_t* dev, 
 // EXPLAIN (NEXT-1, one candidate): xo[8 + t] = pipeline of the t-th committed
 // forward move, xo[8 + n + t] = of the t-th backward move; xo[1..4] = Df, Db,
 // forward / backward move counts.
-template <bool EXPLAIN = false>
+// Forward dependency shift (R10) on 32-bit level masks (B = 32 instance):
+// thresholds T_1 <= .. <= T_K (sorted bytes, n + 1 = never), levels from
+// E[x] = {j : c_j = x} (E[0]: c_j = 0).  max_i need_i = max over k of
+// T_k - k with T_{K+1} = n + 1; INF if that exceeds the coarse entries;
+// else the level walk of tdep_fwd (first slot of a level: start + thresholds
+// passed).
+__device__ __forceinline__ int64_t tdep_mask(const TPlan& p, const int64_t* G, int n, int sumc, const uint32_t* E,
+                                             uint32_t all, const SB thr, int K) {
+  int maxneed = n - K;
+#pragma unroll 1
+  for (int k = 0; k < K; ++k) maxneed = max(maxneed, (int)thr[k] - (k + 1));
+  if (maxneed > sumc) return kInf;
+  int64_t best = kNegInf;
+  uint32_t A = all & ~E[0];
+  int k = 0;
+#pragma unroll 1
+  for (int t = 1, pos = 0; pos < maxneed; ++t) {
+    int i = pos + 1 + k;
+    while (k < K && (int)thr[k] <= i) { ++k; ++i; }
+    best = max(best, p.at(p.preEF, t) - G[i - 1]);
+    pos += __popc(A);
+    A &= ~E[t];
+  }
+  return best;
+}
+
+// Global ordering (R14) and the initial backward shift for strict plans on
+// level masks, when every moved entry sorts after every coarse one.  Coarse
+// values PRE_EF(t) - Df rise with t, a pipeline's moved ones INB_F[a][k] with
+// k: compare the largest coarse value with the smallest moved one; false if
+// they may interleave.  Otherwise pipeline j's entries are its c_j coarse ones
+// (level t: slot pos_t + |A_t below j|, rank N_j - t + 1) followed by its
+// moved ones (slot sum c + place among the moved, rank kf_j - k).  D is
+// non-increasing in the slot, so for a rank r > max kf the largest term is at
+// the coarse entry of jmax (largest N, highest j) at level N_max - r + 1, and
+// ranks r <= max kf are dominated by a moved entry of that rank.  E[x] =
+// {j : c_j = x} on entry (clobbered by the moved-entry sort; the caller
+// zeroes it).
+__device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS& s, uint32_t* E, uint32_t all,
+                                     uint32_t MV, int maxN, int jmax, int sumc, int64_t Df, int64_t& dep_b) {
+  const int kmax = p.kmax;
+  int maxc = maxN;
+#pragma unroll 1
+  while (maxc > 0 && E[maxc] == 0u) --maxc;
+  if (MV != 0u && maxc > 0) {
+    const int64_t vpre = p.at(p.preEF, maxc) - Df;
+#pragma unroll 1
+    for (uint32_t b = MV; b; b &= b - 1)
+      if (p.at(p.inbF, row_of(p, __ffs(b) - 1) * kmax) <= vpre) return false;
+  }
+  int maxkf = 0;
+#pragma unroll 1
+  for (uint32_t b = MV; b; b &= b - 1) {
+    const int j = __ffs(b) - 1;
+    maxkf = max(maxkf, (int)s.N[j] - (int)s.c[j]);
+  }
+  const uint32_t below = (1u << jmax) - 1u;
+  uint32_t A = all & ~E[0];
+  int64_t best = kNegInf;
+#pragma unroll 1
+  for (int u = 1, pos = 0; u <= maxN - maxkf; ++u) {
+    best = max(best, p.at(p.preBEF, maxN - u + 1) - D[pos + __popc(A & below)]);
+    pos += __popc(A);
+    A &= ~E[u];
+  }
+  // moved entries sorted by (value, key): inserted in (j, k) order, so a
+  // stable insertion by value keeps key order among equal values
+  int nm = 0;
+#pragma unroll 1
+  for (uint32_t b = MV; b; b &= b - 1) {
+    const int j = __ffs(b) - 1, a = row_of(p, j), kfj = (int)s.N[j] - (int)s.c[j];
+#pragma unroll 1
+    for (int k = 0; k < kfj; ++k) {
+      const int64_t v = p.at(p.inbF, a * kmax + k);
+      int q = nm++;
+#pragma unroll 1
+      for (; q > 0 && p.at(p.inbF, row_of(p, s.mvj[q - 1]) * kmax + s.mvk[q - 1]) > v; --q) {
+        s.mvj[q] = s.mvj[q - 1];
+        s.mvk[q] = s.mvk[q - 1];
+      }
+      s.mvj[q] = (uint8_t)j;
+      s.mvk[q] = (uint8_t)k;
+    }
+  }
+#pragma unroll 1
+  for (int q = 0; q < nm; ++q) {
+    const int j = s.mvj[q];
+    best = max(best, p.at(p.preBEF, (int)s.N[j] - (int)s.c[j] - (int)s.mvk[q]) - D[sumc + q]);
+  }
+  dep_b = best;
+  return true;
+}
+
+// One candidate, sequentially in this thread (the general path).
+// B = 32 (kMask): the forward loop runs on level masks E (uint32 words at
+// E, zero on entry; left dirty, the caller zeroes them) with the thresholds
+// after them, and for strict plans the ordering's initial backward shift is
+// taken level by level when every moved EF sorts after every coarse one
+// (then owners and ranks are materialised only if a backward move is tried).
+// EXPLAIN (NEXT-1, one candidate): xo[8 + t] = pipeline of the t-th committed
+// forward move, xo[8 + n + t] = of the t-th backward move; xo[1..4] = Df, Db,
+// forward / backward move counts.
+template <int B, bool EXPLAIN = false>
 __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
-                         TStats& st, int64_t* xo = nullptr) {
+                         uint32_t* E, TStats& st, int64_t* xo = nullptr) {
+  constexpr bool kMask = B == 32;
   const int n = c.n, m = p.m, kmax = p.kmax;
+  const uint32_t all = m >= 32 ? 0xffffffffu : (1u << m) - 1u;
+  const SB thr = kMask ? SB{(uint32_t)((reinterpret_cast<unsigned char*>(E) - k2sm) + 4 * (B + 2))} : s.thr;
   // ---------------- coarse init (R9) -------------------------------------
-  #pragma unroll 1
-  for (int t = 0; t < (n + 5) / 4; ++t) s.cnt.w(t) = 0u;  // cnt[0..n+1] (4-aligned)
+  if (!kMask) {
+#pragma unroll 1
+    for (int t = 0; t < (n + 5) / 4; ++t) s.cnt.w(t) = 0u;  // cnt[0..n+1] (4-aligned)
+  }
   // the first findCritical of both phases runs on N: one pass for both keys
   uint32_t kf0 = 0, kb0 = 0;
   int maxN = 0;
-  #pragma unroll 1
+#pragma unroll 1
   for (int j = 0, off = 0; j < m; ++j, off += p.np1) {
     const int Nj = s.N[j];
     s.c[j] = (uint8_t)Nj;
-    s.cnt[Nj] += 1;
+    if (kMask) E[Nj] |= 1u << j;
+    else s.cnt[Nj] += 1;
     maxN = max(maxN, Nj);
-    const uint64_t k = __ldg(&p.kj[off + Nj]);
+    const uint64_t k = __ldg(reinterpret_cast<const uint64_t*>(p.ptr(p.kj)) + off + Nj);
     kf0 = max(kf0, (uint32_t)k);
     kb0 = max(kb0, (uint32_t)(k >> 32));
   }
-  #pragma unroll 1
-  for (int t = maxN - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
+  const int jmax = kMask ? 31 - __clz(E[maxN]) : 0;  // highest j with N_j = max N
+  if (!kMask) {
+#pragma unroll 1
+    for (int t = maxN - 1; t >= 1; --t) s.cnt[t] += s.cnt[t + 1];  // histogram -> #{j : c_j >= t}
+  }
   int sumc = n, M = 0, itf = 0, atf = 0, itb = 0, atb = 0;
+  uint32_t MV = 0;  // pipelines with a committed forward move (kMask)
   // ---------------- forward OptimizeSchedule (R10-R13) --------------------
   // initial forward shift (no thresholds, no trial): the first slot of each
   // level t sits at position sum_{t' < t} cnt[t'] (tdep_fwd with M = 0)
   int64_t dep = kNegInf;
-  #pragma unroll 1
-  for (int t = 1, pos = 0; pos < n; ++t) {
-    dep = max(dep, __ldg(&p.preEF[t]) - G[pos]);
-    pos += s.cnt[t];
+  {
+    uint32_t A = all;
+#pragma unroll 1
+    for (int t = 1, pos = 0; pos < n; ++t) {
+      dep = max(dep, p.at(p.preEF, t) - G[pos]);
+      if (kMask) {
+        pos += __popc(A);
+        A &= ~E[t];
+      } else {
+        pos += s.cnt[t];
+      }
+    }
   }
   int64_t Delta;
-  #pragma unroll 1
+#pragma unroll 1
   for (;;) {
     ++itf;
     int js;
@@ -529,34 +661,62 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
     const int as = row_of(p, js), cjs = s.c[js], kfj = s.N[js] - cjs;
-    if (kfj >= (int)__ldg(&p.lenF[as])) break;  // ScheduleKernels fails (R12)
-    const int64_t EF = __ldg(&p.inbF[as * kmax + kfj]);
+    if (kfj >= (int)p.at(p.lenF, as)) break;  // ScheduleKernels fails (R12)
     ++atf;
-    const int bp = (int)__ldg(&p.bpF[as * kmax + kfj]);  // EF_i + L <= F_i holds for slots >= bp
-    s.c[js] = (uint8_t)(cjs - 1);       // trial move
-    s.cnt[cjs] -= 1;
-    const int64_t dep2 = tdep_fwd(p, G, n, sumc - 1, bp, s, M);
-    if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
-      s.c[js] = (uint8_t)cjs;
-      s.cnt[cjs] += 1;
-      break;
+    const int bp = (int)p.at(p.bpF, as * kmax + kfj);  // EF_i + L <= F_i holds for slots >= bp
+    int64_t dep2;
+    int q = M;
+    if (kMask) {  // trial move: js one level down, threshold bp inserted in order
+      const uint32_t bit = 1u << js;
+      E[cjs] &= ~bit;
+      E[cjs - 1] |= bit;
+#pragma unroll 1
+      for (; q > 0 && (int)thr[q - 1] > bp; --q) thr[q] = thr[q - 1];
+      thr[q] = (uint8_t)bp;
+      dep2 = tdep_mask(p, G, n, sumc - 1, E, all, thr, M + 1);
+      if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
+        E[cjs - 1] &= ~bit;
+        E[cjs] |= bit;
+#pragma unroll 1
+        for (; q < M; ++q) thr[q] = thr[q + 1];
+        break;
+      }
+      s.c[js] = (uint8_t)(cjs - 1);
+      MV |= bit;
+      ++M;
+    } else {
+      s.c[js] = (uint8_t)(cjs - 1);  // trial move
+      s.cnt[cjs] -= 1;
+      dep2 = tdep_fwd(p, G, n, sumc - 1, bp, s, M);
+      if (dep2 > Delta) {  // checkEncLLMDep fails (R13): undo, phase ends
+        s.c[js] = (uint8_t)cjs;
+        s.cnt[cjs] += 1;
+        break;
+      }
+      ++M;  // commit: insert the threshold
+#pragma unroll 1
+      for (; q > 0 && s.thr[q - 1] > bp; --q) s.thr[q] = s.thr[q - 1];
+      s.thr[q] = (uint8_t)bp;
     }
-    if (EXPLAIN) xo[8 + M] = js;
-    int q = M++;  // commit: insert the threshold
-    while (q > 0 && s.thr[q - 1] > bp) {
-      s.thr[q] = s.thr[q - 1];
-      --q;
-    }
-    s.thr[q] = (uint8_t)bp;
+    if (EXPLAIN) xo[8 + M - 1] = js;
     dep = dep2;
     --sumc;
   }
   const int64_t Df = Delta;
   // ---------------- global ordering (R14) -------------------------------
-  bool have_order = M > 0 || !p.strict;
-  int64_t dep_b = !have_order ? order_fast(p, D, m, s)
-                  : p.strict  ? order_strict(p, D, m, Df, s)
-                              : order_general(p.preEF, p.preBEF, p.inbF, p.rt, p.kmax, D, m, Df, M > 0, s.N.o, s.c.o, s.kb.o, s.own.o, s.rk.o);
+  bool have_order = true;
+  int64_t dep_b = kNegInf;
+  bool done_b = false;
+  if (kMask && p.strict && tsep(p, D, s, E, all, MV, maxN, jmax, sumc, Df, dep_b)) {
+    have_order = false;  // owners and ranks materialised if a backward move is tried
+    done_b = true;
+  }
+  if (!done_b) {
+    have_order = M > 0 || !p.strict;
+    dep_b = !have_order ? order_fast(p, D, m, s)
+            : p.strict  ? order_strict(p, D, m, Df, s)
+                        : order_general(p.ptr(p.preEF), p.ptr(p.preBEF), p.ptr(p.inbF), p.rt, p.kmax, D, m, Df, M > 0, s.N.o, s.c.o, s.kb.o, s.own.o, s.rk.o);
+  }
   // ---------------- backward OptimizeSchedule (R15) ------------------------
   int sumcb = n;
   bool init_b = false;
@@ -570,8 +730,8 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     const int as = row_of(p, js), kfj = s.N[js] - s.c[js];
     const int kbj = init_b ? s.N[js] - s.cb[js] : 0;
     const int64_t rowoff = (int64_t)as * (kmax + 1) + kfj;
-    if (kbj >= (int)__ldg(&p.lenB[rowoff])) break;
-    const int64_t EFb = __ldg(&p.inbB[rowoff * kmax + kbj]);
+    if (kbj >= (int)p.at(p.lenB, rowoff)) break;
+    const int64_t EFb = p.at(p.inbB, rowoff * kmax + kbj);
     ++atb;
     if (!have_order) {  // materialise owners and ranks (same order, same initial shift)
       order_strict(p, D, m, Df, s);
@@ -622,11 +782,13 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
 // candidate when neither phase commits a move, i.e. the first attempt of
 // each OptimizeSchedule phase fails (R11-R13) or is never made.  Returns
 // false as soon as a first move would commit; the candidate then goes to the
-// general path (teval), which evaluates it from the start.
+// general path (teval), which evaluates it from the start.  (Letting the
+// fast path run the forward loop further measured slower: the warp waits for
+// its longest loop, which the general path's full batches absorb better.)
 //
 // Pipeline sets are 32-bit masks.  E[x] = {j : N_j = x}; the walk over levels
 // t = 1..max N turns it into A_t = {j : N_j >= t} (stored back in E[t]), so
-// the slot of the pre entry (t, j) in the global ordering without moved
+// the slot of the coarse entry (t, j) in the global ordering without moved
 // entries (R14: level-major, j within a level) is pos_t + |A_t below j|.
 //   * forward (R10): the first slot of level t is pos_t; a trial move of js
 //     (one threshold bp, R10's closed form) removes js from level N_js.
@@ -638,18 +800,19 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
 //   * backward trial of jb (no backward move yet, Qcb = 0): only jb's entries
 //     change (need = r - [EFb <= D]); the others' maximum is the shift above,
 //     or, when jb = jmax, the same walk over j2 (largest N among j != jmax).
-// Leaves E zeroed.  dep / depb / Delta are the quantities of teval.
+// Leaves E zeroed.
 template <int B>
 __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const int64_t* D, int n, const TS& s,
                                       uint32_t* E, int64_t& Df, int64_t& Db, TStats& st) {
   const int m = p.m, np1 = p.np1;
   uint32_t kf0 = 0, kb0 = 0;
   int Nmax = 0;
+  const uint64_t* kj = reinterpret_cast<const uint64_t*>(p.ptr(p.kj));
 #pragma unroll 2
   for (int j = 0, off = 0; j < m; ++j, off += np1) {
     const int Nj = s.N[j];
     E[Nj] |= 1u << j;
-    const uint64_t k = __ldg(&p.kj[off + Nj]);  // first findCritical of both phases (R11)
+    const uint64_t k = __ldg(kj + off + Nj);  // first findCritical of both phases (R11)
     kf0 = max(kf0, (uint32_t)k);
     kb0 = max(kb0, (uint32_t)(k >> 32));
     Nmax = max(Nmax, Nj);
@@ -660,13 +823,12 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
   int64_t dep = kNegInf, depb = kNegInf;
   {
     uint32_t A = all;
-    int pos = 0;
-    #pragma unroll 1
-    for (int t = 1; t <= Nmax; ++t) {
+#pragma unroll 1
+    for (int t = 1, pos = 0; t <= Nmax; ++t) {
       const uint32_t e = E[t];
       E[t] = A;
-      dep = max(dep, __ldg(&p.preEF[t]) - G[pos]);
-      depb = max(depb, __ldg(&p.preBEF[Nmax - t + 1]) - D[pos + __popc(A & below_max)]);
+      dep = max(dep, p.at(p.preEF, t) - G[pos]);
+      depb = max(depb, p.at(p.preBEF, Nmax - t + 1) - D[pos + __popc(A & below_max)]);
       pos += __popc(A);
       A &= ~e;
     }
@@ -675,23 +837,23 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
   // ---- forward, first iteration
   int js;
   const int64_t dev = crit_value(p, p.devF, s.N, kf0, js);
-  int64_t Delta = max((int64_t)0, max(dev, dep));
+  const int64_t Delta = max((int64_t)0, max(dev, dep));
   int atf = 0;
   if (Delta != 0) {
     const int as = row_of(p, js);
-    if ((int)__ldg(&p.lenF[as]) > 0) {
+    if ((int)p.at(p.lenF, as) > 0) {
       ++atf;
-      const int bp = (int)__ldg(&p.bpF[as * p.kmax]);
+      const int bp = (int)p.at(p.bpF, as * p.kmax);
       if (bp <= n) {  // else need_n = n > n - 1 coarse entries: INF, the move fails
         const int Njs = s.N[js];
         const uint32_t jsbit = 1u << js;
         int64_t dep2 = kNegInf;
-        #pragma unroll 1
+#pragma unroll 1
         for (int t = 1, pos = 0; pos < n - 1; ++t) {
           uint32_t A = E[t];
           if (t == Njs) A &= ~jsbit;
           const int st1 = pos + 1;  // first position of level t (1-based): slot st1, or st1 + 1 past the threshold
-          dep2 = max(dep2, __ldg(&p.preEF[t]) - G[st1 < bp ? st1 - 1 : st1]);
+          dep2 = max(dep2, p.at(p.preEF, t) - G[st1 < bp ? st1 - 1 : st1]);
           pos += __popc(A);
         }
         general = dep2 <= Delta;  // checkEncLLMDep holds: the move commits
@@ -704,43 +866,44 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
     // ---- backward, first iteration (initial shift depb)
     int jb;
     const int64_t devb = crit_value(p, p.devB, s.N, kb0, jb);
-    int64_t Delta_b = max((int64_t)0, max(devb, depb));
+    const int64_t Delta_b = max((int64_t)0, max(devb, depb));
     if (Delta_b != 0) {
       const int as = row_of(p, jb);
       const int64_t rowoff = (int64_t)as * (p.kmax + 1);  // kf = 0 forward chains
-      if ((int)__ldg(&p.lenB[rowoff]) > 0) {
+      if ((int)p.at(p.lenB, rowoff) > 0) {
         ++atb;
-        const int64_t EFb = __ldg(&p.inbB[rowoff * p.kmax]);
+        const int64_t EFb = p.at(p.inbB, rowoff * p.kmax);
         if (EFb <= D[jb]) {  // else jb's rank-N slot (level 1, slot jb) loses its coarse entry: INF
           const int Njb = s.N[jb];
           const bool other2 = jb == jmax;
-          int N2 = 0, j2 = 0;  // jb = jmax: the others' largest N and its highest j (E[t] now holds A_t)
+          int N2 = 0, j2 = 0;  // jb = jmax: the others' largest N and its highest j (E[t] holds A_t)
           if (other2) {
+#pragma unroll 1
             for (N2 = Nmax; N2 > 0 && __popc(E[N2]) < 2; --N2) {}
             if (N2 > 0) j2 = 31 - __clz(E[N2] & ~(1u << jmax));
           }
           const int tl = max(Njb, N2);
           const uint32_t below_b = (1u << jb) - 1u, below_2 = (1u << j2) - 1u;
           int64_t dep2 = other2 ? kNegInf : depb;
-          #pragma unroll 1
+#pragma unroll 1
           for (int t = 1, pos = 0; t <= tl; ++t) {
             const uint32_t A = E[t];
             if (t <= Njb) {
               const int sl = pos + __popc(A & below_b);
               const int64_t d = D[sl];
               const int need = Njb - t + 1 - (EFb <= d ? 1 : 0);
-              if (need > 0) dep2 = max(dep2, __ldg(&p.preBEF[need]) - d);
+              if (need > 0) dep2 = max(dep2, p.at(p.preBEF, need) - d);
             }
-            if (other2 && t <= N2) dep2 = max(dep2, __ldg(&p.preBEF[N2 - t + 1]) - D[pos + __popc(A & below_2)]);
+            if (other2 && t <= N2) dep2 = max(dep2, p.at(p.preBEF, N2 - t + 1) - D[pos + __popc(A & below_2)]);
             pos += __popc(A);
           }
-          general = dep2 <= Delta_b;
+          general = dep2 <= Delta_b;  // a backward move commits: the general path
         }
       }
     }
     Db = Delta_b;
   }
-  #pragma unroll 1
+#pragma unroll 1
   for (int t = 1; t <= Nmax; ++t) E[t] = 0u;
   if (!general) {
     st.v[0] += 1;
@@ -845,7 +1008,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
       if (eq != p.e) tplan(c, eq, p);
       TS sq = s;
       sq.N = SB{qoff + (uint32_t)(sl * QS)};  // teval only reads N; the lane's own composition stays in s.N
-      const int64_t lat = teval(c, p, G, D, T_end, sq, st);
+      const int64_t lat = teval<B>(c, p, G, D, T_end, sq, E, st);
       if (A.lat_out) A.lat_out[oq] = lat;
       tbetter(lat, gq, bl, bg);
       for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval's scratch overlaps the fast path's masks
@@ -866,7 +1029,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
         done = tfast<B>(p, G, D, n, s, E, Df, Db, st);
         lat = T_end + Df + Db;  // R16
       } else {
-        lat = teval(c, p, G, D, T_end, s, st);
+        lat = teval<B>(c, p, G, D, T_end, s, E, st);
         for (int t = 0; t < B + 2; ++t) E[t] = 0u;
       }
       if (done) {
@@ -1025,12 +1188,14 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   TPlan p;
   tplan(c, e, p);
   TS s = ts_at<B, BM>(0u);
+  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + 2 * BM);
+  for (int t = 0; t < B + 2; ++t) E[t] = 0u;
   tunrank<B>(c, n, p.m, g - p.first, s);
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   out[5] = e;
   out[6] = p.m;
   out[7] = n;
-  out[0] = teval<true>(c, p, G, D, T_end, s, st, out);
+  out[0] = teval<B, true>(c, p, G, D, T_end, s, E, st, out);
 }
 
 }  // namespace

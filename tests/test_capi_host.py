@@ -144,3 +144,16 @@ def test_n_mb_limit(L):
     p["n_mb"] = 136
     code, msg = _err(L, p)
     assert code == -5 and "exceeds the supported 128" in msg
+
+
+def test_eval_instance_selection(L):
+    """K2 mode 1 instance by (n_mb, largest m with candidates), host only."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_parity import kmax128_problem, mid_m_problem, wide_m_problem
+    from workload import config_problem
+    cases = [(config_problem(4), 0), (config_problem(3), 0), (config_problem(3, 64), 1), (mid_m_problem(), 2),
+             (wide_m_problem(), 3), (config_problem(5, 64), 4), (config_problem(5, 128), 5), (kmax128_problem(), 5)]
+    for prob, inst in cases:
+        ctx = L.optimus_plan_only(prob)
+        assert ctx.eval_instance()[0] == inst, prob["name"]

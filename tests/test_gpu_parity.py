@@ -139,26 +139,45 @@ def test_full_space_parity_config4(dev, config4_oracle_lat, mode):
     assert (int(b[0]), int(b[1])) == (int(ref.min()), int(np.argmin(ref)))
 
 
-@MODES
-@pytest.mark.parametrize("prob", BIG, ids=lambda p: p["name"])
-def test_sampled_parity_full_size(dev, oracle_mod, prob, mode):
-    """BASELINE sizes: 4096 seeded indices per config through eval_indices."""
+SAMPLED = 1 << 17  # the first 2^17 indices of the seeded stream for configs 3 and 5
+_ORACLE_SAMPLES = {}
+
+
+def _oracle_sample(oracle_mod, prob, count):
+    """(indices, oracle lats) of the seeded stream, computed once per problem."""
+    key = (prob["name"], count)
+    if key not in _ORACLE_SAMPLES:
+        o = oracle_mod.Oracle(prob)
+        idx = np.array(sample_indices(20241018, count, o.total), dtype=np.uint64)
+        _ORACLE_SAMPLES[key] = (idx, o.eval(idx, threads=THREADS))
+        o.close()
+    return _ORACLE_SAMPLES[key]
+
+
+def _sampled_parity(dev, oracle_mod, prob, mode, count):
     torch = dev
     ctx = _load(prob, mode)
-    total, _ = ctx.num_candidates()
-    idx = np.array(sample_indices(20241018, 4096, total), dtype=np.uint64)
+    idx, ref = _oracle_sample(oracle_mod, prob, count)
     di = torch.from_numpy(idx.astype(np.int64)).cuda()
     lat = torch.empty(len(idx), dtype=torch.int64, device="cuda")
     best2 = torch.empty(2, dtype=torch.int64, device="cuda")
     ctx.eval_indices(di, best2, lat_out=lat)
     torch.cuda.synchronize()
-    ref = oracle_mod.Oracle(prob).eval(idx, threads=THREADS)
     got = lat.cpu().numpy()
     bad = np.nonzero(got != ref)[0]
     assert bad.size == 0, f"{bad.size} mismatches, first idx={idx[bad[:5]].tolist()}"
     b = best2.cpu().numpy()
     j = min(range(len(idx)), key=lambda i: (ref[i], idx[i]))
     assert (int(b[0]), int(b[1])) == (int(ref[j]), int(idx[j]))
+    return ctx
+
+
+@MODES
+@pytest.mark.parametrize("prob", BIG, ids=lambda p: p["name"])
+def test_sampled_parity_full_size(dev, oracle_mod, prob, mode):
+    """BASELINE sizes: 2^17 seeded indices per config through eval_indices
+    (the first 2^17 of the seeded stream for configs 3 and 5)."""
+    _sampled_parity(dev, oracle_mod, prob, mode, SAMPLED)
 
 
 @MODES
@@ -464,22 +483,22 @@ def test_efficiency_trend_table7(dev):
 
 
 # ---------------------------------------------------------------------------
-# N_mb 64 / 128 (config 5's sweep): K2 mode 1's wide instance (n, m <= 128)
-WIDE = [config_problem(5, 64), config_problem(5, 128)]
+# N_mb 64 / 128 (config 5's sweep): K2 mode 1's instances for n > 32
+WIDE_NMB = [config_problem(5, 64), config_problem(5, 128)]
 
 
-@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+@pytest.mark.parametrize("prob", WIDE_NMB, ids=lambda p: p["name"])
 def test_wide_template_parity(dev, oracle_mod, prob):
     test_template_parity(dev, oracle_mod, prob)
 
 
-@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+@pytest.mark.parametrize("prob", WIDE_NMB, ids=lambda p: p["name"])
 def test_wide_sampled_parity(dev, oracle_mod, prob):
-    """4096 seeded indices of the 2.2e9 / 3.6e11 spaces through eval_indices."""
-    test_sampled_parity_full_size(dev, oracle_mod, prob, 1)
+    """2^17 seeded indices of the 2.2e9 / 3.6e11 spaces through eval_indices."""
+    _sampled_parity(dev, oracle_mod, prob, 1, SAMPLED)
 
 
-@pytest.mark.parametrize("prob", WIDE, ids=lambda p: p["name"])
+@pytest.mark.parametrize("prob", WIDE_NMB, ids=lambda p: p["name"])
 def test_wide_contiguous_ranges(dev, oracle_mod, prob):
     """The range path (overlapped with K1, claims per plan) on windows that
     straddle plan boundaries, plus the very first and last candidates."""
@@ -509,3 +528,119 @@ def test_wide_mode0_refused(dev):
     with pytest.raises(OptimusError) as ei:
         ctx.eval_candidates(0, 100, best2)
     assert ei.value.code == -5
+
+
+# ---------------------------------------------------------------------------
+# K2 mode 1 instances for n > 32 with plans of m > 16 pipelines: (64, 64),
+# (128, 64) and (128, 128) slots x pipelines per thread
+def wide_m_problem():
+    """LLM PP 22 x TP 3 with N_mb = 66: the (P = 1, T = 1) plan has m = 66 > 64
+    pipelines (instance (128, 128)).  A plan with m > 64 always comes with one
+    of m / 2, and C(n - 1, m / 2 - 1) fits in 64 bits only for n up to ~67, so
+    this is about the largest such space the index type allows (3.7e18).  Small
+    random kernels, memory never binding."""
+    from workload.gen import _Rng, _rand_layer
+    q = random_problem(7, max_p=4, max_t=2, max_n=8)
+    pp, tp = 22, 3
+    q["name"] = "wide_m66_pp22_tp3_n66"
+    q["llm"] = {"dp": 1, "pp": pp, "tp": tp, "v": 1}
+    q["llm_layers"] = pp
+    q["n_mb"] = 66
+    q["n_gpu"] = pp * tp
+    q["tp_opts"] = [1, 3]
+    rng = _Rng(77)
+    q["llm_fwd_layer"] = _rand_layer(rng, tp, 400, 3)
+    q["llm_bwd_layer"] = _rand_layer(rng, tp, 800, 3)
+    q["branches"] = [{"layers": 4, "params": 1000,
+                      "fwd": [_rand_layer(rng, T, max(2, 60 // T), 2) for T in q["tp_opts"]],
+                      "bwd": [_rand_layer(rng, T, max(2, 120 // T), 2) for T in q["tp_opts"]]}]
+    return q
+
+
+def mid_m_problem():
+    """LLM PP 20, TP 1 with N_mb = 80: plans with m = 20 pipelines and n > 64
+    (instance (128, 64)); config 3 at N_mb > 66 would overflow the 64-bit
+    candidate index (C(n - 1, 31) for its m = 32 plans)."""
+    from workload.gen import _Rng, _rand_layer
+    q = random_problem(8, max_p=4, max_t=1, max_n=8)
+    pp = 20
+    q["name"] = "mid_m20_pp20_tp1_n80"
+    q["llm"] = {"dp": 1, "pp": pp, "tp": 1, "v": 1}
+    q["llm_layers"] = pp
+    q["n_mb"] = 80
+    q["n_gpu"] = pp
+    q["tp_opts"] = [1]
+    rng = _Rng(88)
+    q["llm_fwd_layer"] = _rand_layer(rng, 1, 400, 3)
+    q["llm_bwd_layer"] = _rand_layer(rng, 1, 800, 3)
+    q["branches"] = [{"layers": 5, "params": 1000, "fwd": [_rand_layer(rng, 1, 90, 2)],
+                      "bwd": [_rand_layer(rng, 1, 180, 2)]}]
+    return q
+
+
+INSTANCE_PROBS = [(config_problem(3, 64), 1), (mid_m_problem(), 2), (wide_m_problem(), 3)]
+
+
+@pytest.mark.parametrize("prob,inst", INSTANCE_PROBS, ids=lambda x: x["name"] if isinstance(x, dict) else str(x))
+def test_instance_sampled_parity(dev, oracle_mod, prob, inst):
+    """2^17 seeded indices through eval_indices on the (64, 64), (128, 64)
+    and (128, 128) instances (verdict r1: never compared with the oracle)."""
+    ctx = _sampled_parity(dev, oracle_mod, prob, 1, SAMPLED)
+    assert ctx.eval_instance()[0] == inst
+
+
+@pytest.mark.parametrize("prob,inst", INSTANCE_PROBS, ids=lambda x: x["name"] if isinstance(x, dict) else str(x))
+def test_instance_ranges(dev, oracle_mod, prob, inst):
+    """The range path (overlapped with K1, claims per plan) on the same
+    instances: windows straddling every plan boundary, the first and the last
+    candidates, and the whole of every plan with m > 16 that is small."""
+    torch = dev
+    ctx = _load(prob, 1)
+    assert ctx.eval_instance()[0] == inst
+    total, n_plans = ctx.num_candidates()
+    plans = [ctx.get_plan(i) for i in range(n_plans)]
+    firsts = [q["first"] for q in plans if q["count"]]
+    wins = [(max(0, f - 500), min(total, f + 701)) for f in firsts[1:]] + [(0, 1200), (total - 1100, total)]
+    wins += [(q["first"], q["first"] + q["count"]) for q in plans if q["m"] > 16 and 0 < q["count"] <= 4000]
+    o = oracle_mod.Oracle(prob)
+    for begin, end in wins:
+        lat = torch.empty(end - begin, dtype=torch.int64, device="cuda")
+        best2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(begin, end, best2, lat_out=lat)
+        torch.cuda.synchronize()
+        ref = o.eval_range(begin, end, threads=THREADS)
+        got = lat.cpu().numpy()
+        assert np.array_equal(got, ref), (begin, end, int((got != ref).sum()))
+        b = best2.cpu().numpy()
+        assert (int(b[0]), int(b[1])) == (int(ref.min()), begin + int(np.argmin(ref)))
+
+
+def kmax128_problem():
+    """Config 1 at N_mb = 128 with the encoder's kernels 10x shorter: its m = 1
+    plan (P = 2, T = 2) fits all kmax = n - m + 1 = 128 forward chains, so K1
+    publishes snapshot versions up to 128 (advisor r1: int8 owner versions)."""
+    p = config_problem(1, n_mb=128)
+    p["name"] = "c1_n128_enc_div10"
+    for b in p["branches"]:
+        b["fwd"] = [[(k, max(1, ns // 10)) for k, ns in lst] for lst in b["fwd"]]
+        b["bwd"] = [[(k, max(1, ns // 10)) for k, ns in lst] for lst in b["bwd"]]
+    return p
+
+
+def test_kmax128_chain_tables(dev, oracle_mod):
+    prob = kmax128_problem()
+    ctx = _load(prob)
+    o = oracle_mod.Oracle(prob)
+    _, n_plans = ctx.num_candidates()
+    full = 0
+    for e in range(n_plans):
+        t = ctx.debug_plan_tables(e)
+        if t is None:
+            continue
+        for a in range(t["rp"]):
+            assert t["INB_F"][a] == o.row_chains(e, a, -1, t["kmax"]), (e, a)
+            for kf in range(t["lenF"][a] + 1):
+                assert t["INB_B"][a][kf] == o.row_chains(e, a, kf, t["kmax"]), (e, a, kf)
+            full += t["lenF"][a] == 128
+    assert full > 0  # the m = 1 plan placed all 128 forward chains
+    _sampled_parity(dev, oracle_mod, prob, 1, 4096)

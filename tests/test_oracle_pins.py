@@ -380,3 +380,116 @@ def test_appendix_c_golden_toy(oracle_mod):
         if "db" in row:
             assert aux[row["g"]][1] == row["db"]
     assert list(o.best()) == gold["best"]
+
+
+# ------------------------------------------------- R11 findCritical order
+def _moves(trace, key):
+    """Moving pipeline of each committed move, in move order (trace records
+    are [pipeline, stage, comm, start, end, move])."""
+    seq = {}
+    for r in trace[key]:
+        seq.setdefault(r[5], r[0])
+    return [seq[k] for k in sorted(seq)]
+
+
+def test_findcritical_order_p389(oracle_mod):
+    """P:387-389 (Fig. 'move_enc', partition [3, 5] of N_mb = 8 over two
+    encoder pipelines): "encoder pipeline 2's forward computation
+    (microbatch 8 forward) is initially on the critical path ... After
+    successfully scheduling that microbatch forward to later bubbles, encoder
+    pipeline 1 assumes the critical path position."  Pipeline 1 runs on the
+    first LLM stages and pipeline 2 on the later ones (R7).  On this
+    fixture the oracle's first two committed forward moves are pipeline 2 then
+    pipeline 1, which R11 (critical = largest end(s, c_j) - w of the stage's
+    own LLM stage) produces; the reading "largest absolute end time" cannot:
+    after the first move pipeline 2 still holds 4 coarse microbatches against
+    pipeline 1's 3, so its absolute GPipe end is later and it would stay
+    critical."""
+    prob = random_problem(2606, max_p=4, max_t=2, max_n=8, p2p=False, jitter=False)
+    assert prob["llm"]["pp"] == 4 and prob["n_mb"] == 8
+    pl = oracle_mod.plans(prob)["plans"]
+    e = next(i for i, q in enumerate(pl) if q["m"] == 2 and q["P"] == 2 and q["count"])
+    g = pl[e]["first"] + 2  # lexicographic: [1,7], [2,6], [3,5]
+    o = oracle_mod.Oracle(prob)
+    t = o.trace(g)
+    assert t["N"] == [3, 5]
+    mv = _moves(t, "fwd_place")
+    assert mv[:2] == [1, 0], mv  # 0-based: encoder pipeline 2, then encoder pipeline 1
+    # the absolute-end reading: GPipe end of the last stage, counts [3, 4]
+    ends = oracle_mod.gpipe(t["tau_f"], prob["enc_p2p_ns"], 8)[-1]
+    assert ends[4] > ends[3]
+
+
+# ------------------------------------------------- R8 stage split (P:400, P:478)
+def _chain_stage_kernels(trace, key):
+    """{(move, stage): [(comm, duration, start, end), ...]} from the trace."""
+    out = {}
+    for pj, st, comm, s, e, mv in trace[key]:
+        out.setdefault((mv, st), []).append((comm, e - s, s, e))
+    return out
+
+
+def test_stage_split_and_order_p400(oracle_mod):
+    """P:400 (Fig. 'schedule_kernel'): "device 1 holds the first two layers of
+    the encoder, while device 2 holds the next two layers ... device 2 can only
+    utilize bubbles that occur after device 1 completes its forward pass ...
+    for backward computation ... in the reverse order."  Four encoder layers
+    over two encoder stages: every moved chain places exactly two layers'
+    kernels on each stage, stage 2's forward kernels all start after stage 1's
+    last forward kernel ends, and a backward chain finishes on stage 2 before
+    it starts on stage 1."""
+    prob = toy_problem()  # encoder of 4 identical layers; plan (P=2, T=2) has m = 2
+    o = oracle_mod.Oracle(prob)
+    pl = oracle_mod.plans(prob)["plans"]
+    e = next(i for i, q in enumerate(pl) if q["P"] == 2 and q["T"] == 2)
+    per_layer_f = len(prob["branches"][0]["fwd"][1])
+    per_layer_b = len(prob["branches"][0]["bwd"][1])
+    seen_f = seen_b = 0
+    for g in range(pl[e]["first"], pl[e]["first"] + pl[e]["count"]):
+        t = o.trace(g)
+        for key, per in (("fwd_place", per_layer_f), ("bwd_place", per_layer_b)):
+            ch = _chain_stage_kernels(t, key)
+            for mvi in {k[0] for k in ch}:
+                s0, s1 = ch[(mvi, 0)], ch[(mvi, 1)]
+                assert len(s0) == len(s1) == 2 * per  # two layers per device
+                if key == "fwd_place":
+                    assert min(x[2] for x in s1) >= max(x[3] for x in s0)
+                    seen_f += 1
+                else:
+                    assert min(x[2] for x in s0) >= max(x[3] for x in s1)
+                    seen_b += 1
+    assert seen_f > 0 and seen_b > 0
+
+
+def test_multibranch_per_encoder_split_p478(oracle_mod):
+    """P:474-478 (Fig. 'multi_enc_design'): "layers within each encoder are
+    divided into PP_enc stages ... The bubble scheduler breaks down the layers
+    of distinct encoders into kernel-level granularity and arranges their
+    scheduling as if these kernels were part of a single encoder."  Branch A
+    (4 layers) and branch B (2 layers) with distinct kernel durations over two
+    stages: every stage of every moved chain carries two A layers and one B
+    layer (per-encoder split; splitting the concatenated 6 layers instead would
+    put A0-A2 on stage 1 and A3, B0, B1 on stage 2), both branches within one
+    chain."""
+    prob = toy_problem()
+    C = 0
+    a_f = [(C, 17), (C, 29)]
+    a_b = [(C, 31), (C, 37)]
+    b_f = [(C, 41), (C, 43)]
+    b_b = [(C, 47), (C, 53)]
+    prob["branches"] = [{"layers": 4, "params": 100, "fwd": [a_f, a_f], "bwd": [a_b, a_b]},
+                        {"layers": 2, "params": 100, "fwd": [b_f, b_f], "bwd": [b_b, b_b]}]
+    o = oracle_mod.Oracle(prob)
+    pl = oracle_mod.plans(prob)["plans"]
+    e = next(i for i, q in enumerate(pl) if q["P"] == 2 and q["count"])
+    want_f = sorted([d for _, d in a_f] * 2 + [d for _, d in b_f])
+    want_b = sorted([d for _, d in a_b] * 2 + [d for _, d in b_b])
+    seen = 0
+    for g in range(pl[e]["first"], pl[e]["first"] + pl[e]["count"]):
+        t = o.trace(g)
+        assert t["tau_f"] == [sum(want_f)] * 2 and t["tau_b"] == [sum(want_b)] * 2
+        for key, want in (("fwd_place", want_f), ("bwd_place", want_b)):
+            for (mvi, st), ks in _chain_stage_kernels(t, key).items():
+                assert sorted(d for _, d, _, _ in ks) == want, (g, key, mvi, st)
+                seen += 1
+    assert seen > 0
