@@ -111,9 +111,21 @@ __device__ __forceinline__ TS ts_at(uint32_t b) {
   return s;
 }
 
+#ifndef K2T_TV_OFF
+struct TV {
+  const int64_t* o;  // the table's address (32-bit offsets from Cfg::tables measured 1-2% slower)
+};
+#else
 struct TV {
   uint32_t o;  // element offset in Cfg::tables
 };
+#endif
+
+#ifndef K2T_TV_OFF
+#define TVOF(x) TV{c.tables + (x)}
+#else
+#define TVOF(x) TV{(uint32_t)(x)}
+#endif
 
 struct TPlan {
   int e, P, rt, m, kmax, np1;
@@ -129,8 +141,13 @@ struct TPlan {
   TV devF, devB;
   TV kj;                  // findCritical keys per pipeline and count (PlanDesc::kj), u64
   TV inbF, bpF, lenF, inbB, lenB;
+#ifndef K2T_TV_OFF
+  __device__ __forceinline__ int64_t at(TV v, int i) const { return __ldg(&v.o[i]); }
+  __device__ __forceinline__ const int64_t* ptr(TV v) const { return v.o; }
+#else
   __device__ __forceinline__ int64_t at(TV v, int i) const { return __ldg(&T[v.o + i]); }
   __device__ __forceinline__ const int64_t* ptr(TV v) const { return T + v.o; }
+#endif
 };
 
 __device__ __forceinline__ int row_of(const TPlan& p, int j) { return (int)(((unsigned)j * p.rtm) >> 16); }
@@ -147,16 +164,16 @@ __device__ void tplan(const Cfg& c, int e, TPlan& p) {
   p.first = d.first;
   p.count = d.count;
   p.T = c.tables;
-  p.preEF = TV{(uint32_t)(d.preF + (int64_t)(d.P - 1) * (c.n + 1))};
-  p.preBEF = TV{(uint32_t)(d.preB + (int64_t)(d.P - 1) * (c.n + 1))};
-  p.devF = TV{(uint32_t)d.devF};
-  p.devB = TV{(uint32_t)d.devB};
-  p.kj = TV{(uint32_t)d.kj};
-  p.inbF = TV{(uint32_t)d.inbF};
-  p.bpF = TV{(uint32_t)d.bpF};
-  p.lenF = TV{(uint32_t)d.lenF};
-  p.inbB = TV{(uint32_t)d.inbB};
-  p.lenB = TV{(uint32_t)d.lenB};
+  p.preEF = TVOF((d.preF + (int64_t)(d.P - 1) * (c.n + 1)));
+  p.preBEF = TVOF((d.preB + (int64_t)(d.P - 1) * (c.n + 1)));
+  p.devF = TVOF(d.devF);
+  p.devB = TVOF(d.devB);
+  p.kj = TVOF(d.kj);
+  p.inbF = TVOF(d.inbF);
+  p.bpF = TVOF(d.bpF);
+  p.lenF = TVOF(d.lenF);
+  p.inbB = TVOF(d.inbB);
+  p.lenB = TVOF(d.lenB);
   p.strict = (__ldg(&c.tables[d.pflags]) & 1) != 0;
   p.fast = p.strict && d.m <= 32;
 }
