@@ -149,7 +149,8 @@ def run_reference(args, rank: int, world: int, prob: dict, name: str):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": workload_config(prob, name, world, args, orc.total),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }), flush=True)
@@ -168,6 +169,16 @@ def workload_config(prob, name, world, args, total):
 
 
 # ---------------------------------------------------------------- cpu leg
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(ctx, prob, torch):
     """Oracle on this box's host cores over a bounded sample of the same space
     (~10-20 s), plus a GPU-vs-oracle parity spot check on that sample."""
@@ -196,7 +207,8 @@ def cpu_baseline(ctx, prob, torch):
     t0 = time.perf_counter()
     orc.eval(one, threads=1)
     rate1 = len(one) / (time.perf_counter() - t0)
-    return ({"value": count / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "value_1thread": rate1,
+    return ({"value": count / dt, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(), "kind": "oracle",
+             "value_1thread": rate1,
              "sample": f"{count} seeded splitmix64 indices of the {orc.total}-candidate space, oracle C++ -O2, "
                        f"{cores} threads, {dt:.1f} s"},
             {"sample": count, "mismatches": mism})
@@ -303,10 +315,25 @@ def main():
     # library around the build and around K2 on the launch stream (the event
     # between K1 and K2 serialises them, so this pass is not the timed one)
     ctx.set_timing(True)
-    k2_ms, build_ms = [], []
+    k2_ms, build_ms, gather_ms = [], [], []
     for _ in range(max(3, args.steps // 2)):
         flush.zero_()
-        step()
+        if dist:  # ranks in phase, so that the gather's events time the collective alone
+            torch.cuda.synchronize()
+            dist.barrier()
+        ctx.rebuild(stream)
+        if didx is not None:
+            ctx.eval_indices(didx, best2, stream=stream)
+        else:
+            ctx.eval_candidates(0, total, best2, rank=rank, world=world, block=args.block, stream=stream)
+        if world > 1:  # the 16-byte gather, timed on the stream it runs on
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            gather_best(best2)
+            g1.record(stream)
+            g1.synchronize()
+            gather_ms.append(g0.elapsed_time(g1))
         b, k = ctx.last_timing()
         build_ms.append(b)
         k2_ms.append(k)
@@ -320,6 +347,15 @@ def main():
         dist.all_reduce(sum_ms, op=dist.ReduceOp.MAX)
     ms_per_step = float(sum_ms.item()) / args.steps
     value = units / (ms_per_step / 1000.0)
+    # SURVEY §8(e)'s scaling measure: evaluation alone (K2 + K3 + gather), the
+    # build (K0 + K1, replicated on every rank) excluded; max over ranks
+    ev_ms = torch.tensor([sum(k2_ms) / len(k2_ms) + (sum(gather_ms) / len(gather_ms) if gather_ms else 0.0)],
+                         dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(ev_ms, op=dist.ReduceOp.MAX)
+    eval_only = {"value": units / (float(ev_ms.item()) / 1000.0), "unit": UNIT, "ms": float(ev_ms.item()),
+                 "what": "K2 (library events around its launch) + the 16 B all_gather (N > 1), max over ranks; build excluded",
+                 "gather_ms": (sum(gather_ms) / len(gather_ms)) if gather_ms else 0.0}
 
     # ---- e2e through the public API from host inputs, every step
     e2e = None
@@ -365,17 +401,23 @@ def main():
     ops_per_launch = (stats1["ops"] - stats0["ops"]) / args.steps
     k2_avg = sum(k2_ms) / len(k2_ms)
     achieved = ops_per_launch / (k2_avg / 1000.0) / 1e9
-    traffic = None
+    # traffic and issue-slot share are ncu metrics: read from the round's
+    # committed capture (never measured under a profiler inside this run)
+    traffic = issue = None
+    tsrc = None
     tfile = os.path.join(ROOT, "profiles", "k2_traffic.json")
     if os.path.exists(tfile):
         try:
             tj = json.load(open(tfile))
             if tj.get("workload") == name:
                 traffic = tj.get("dram_bytes_per_launch")
+                issue = tj.get("issue_active_pct")
+                tsrc = tj.get("source")
         except Exception:
             pass
     roofline = {"bound": "alu", "kernel": "k2_eval", "achieved": achieved, "peak": peak_gops,
                 "unit": "Gop/s (32-bit integer lane-ops)", "frac": achieved / peak_gops, "traffic": traffic,
+                "traffic_source": tsrc, "issue_slot_pct_ncu": issue,
                 "peak_basis": f"{sms} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
                 "k2_ms": k2_avg, "k2_share_of_step": k2_avg / (sum(step_ms) / len(step_ms)),
                 "build_ms": sum(build_ms) / len(build_ms),
@@ -391,7 +433,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": workload_config(prob, name, world, args, total),
-            "e2e": e2e, "gpu_launches": (nb + ne) * args.steps, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "eval_only": eval_only, "gpu_launches": (nb + ne) * args.steps, "roofline": roofline,
+            "cpu_baseline": cpu,
             "clocks": clocks,
             "best": {"lat_ns": best["lat_ns"], "index": best["index"], "enc_plan": best["enc"], "m": best["m"],
                      "partition": best["counts"]},

@@ -254,6 +254,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   // can finish them first
   for (size_t e = 0; e < X.plans.size(); ++e)
     if (X.plans[e].d.count) X.k2order.push_back((int32_t)e);
+  // (fewer stages first measured 1.7x slower K2 on config 4)
   std::stable_sort(X.k2order.begin(), X.k2order.end(),
                    [&](int32_t x, int32_t y) { return X.plans[x].d.P > X.plans[y].d.P; });
   // K1 work list: every forward unit first (all start at once; a backward
