@@ -334,6 +334,150 @@ Template build_template(const Problem& P) {
   return T;
 }
 
+// ------------------------------------- Megatron-LM baselines (NEXT-2)
+// The paper's comparison systems for its headline speedups (Table 5
+// P:598-600), as iteration times under the same cost model:
+//   naive "we place multimodal encoders to the preprocess in the
+//            first pipeline stage": every encoder layer (all branches, at the
+//            LLM's TP) joins virtual stage 0 (stage 0, chunk 0) in front of
+//            its LLM layers; every virtual stage holds llm_layers / (p v) LLM
+//            layers.
+//   balanced (App. B) the layer sequence (encoder layers,
+//            then LLM layers) is cut into V x PP contiguous virtual stages by
+//            F(l, 1) = sum_{i<=l} t_i,
+//            F(l, m) = min_{j<l} max(F(j, m-1), sum_{i=j+1..l} t_i),
+//            t_i = the layer's forward + backward kernel time (the paper's
+//            "estimated based on FLOPs"; reading R-DP: the profiled time),
+//            every virtual stage non-empty, ties to the smallest j (R-DP);
+//            single encoder only.
+// Virtual stage k = chunk k div p of stage k mod p (Megatron interleaving).
+// Both run Megatron's default warm-up (R2, policy 0), ops back to back with
+// the stage's summed layer times, from T_ag, plus T_rs (R3).
+
+// ASAP list schedule (R2, R3) with per-(stage, chunk) op durations
+// opF/opB[s * v + c] (the template's simulate() has one duration per direction).
+Sim simulate_ops(const Problem& P, const std::vector<int>& W, const std::vector<i64>& opF,
+                 const std::vector<i64>& opB) {
+  int p = (int)P.pp, v = (int)P.v, n = (int)P.n_mb;
+  Sim S;
+  S.order.resize(p);
+  S.start.resize(p);
+  S.end.resize(p);
+  for (int s = 0; s < p; ++s) {
+    S.order[s] = stage_order(P, W[s]);
+    S.start[s].assign(S.order[s].size(), -1);
+    S.end[s].assign(S.order[s].size(), -1);
+  }
+  std::vector<i64> done((size_t)p * 2 * v * n, -1);
+  auto D = [&](int s, int f, int c, int i) -> i64& { return done[(((size_t)s * 2 + f) * v + c) * n + i]; };
+  std::vector<size_t> pos(p, 0);
+  std::vector<i64> free_at(p, 0);
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (int s = 0; s < p; ++s) {
+      while (pos[s] < S.order[s].size()) {
+        OpId op = S.order[s][pos[s]];
+        int ds = -1, df = 0, dc = 0;
+        if (op.fwd) {
+          if (s > 0) { ds = s - 1; df = 1; dc = op.chunk; }
+          else if (op.chunk > 0) { ds = p - 1; df = 1; dc = op.chunk - 1; }
+        } else {
+          if (s < p - 1) { ds = s + 1; df = 0; dc = op.chunk; }
+          else if (op.chunk < v - 1) { ds = 0; df = 0; dc = op.chunk + 1; }
+          else { ds = p - 1; df = 1; dc = v - 1; }
+        }
+        i64 t = std::max(free_at[s], P.T_ag);
+        if (ds >= 0) {
+          i64 e = D(ds, df, dc, op.mb);
+          if (e < 0) break;
+          t = std::max(t, e + (ds != s ? P.pp_p2p : 0));
+        }
+        i64 d = op.fwd ? opF[(size_t)s * v + op.chunk] : opB[(size_t)s * v + op.chunk];
+        S.start[s][pos[s]] = t;
+        S.end[s][pos[s]] = t + d;
+        D(s, op.fwd, op.chunk, op.mb) = t + d;
+        free_at[s] = t + d;
+        ++pos[s];
+        changed = true;
+      }
+    }
+  }
+  S.ok = true;
+  for (int s = 0; s < p; ++s)
+    if (pos[s] != S.order[s].size()) S.ok = false;
+  S.last_end = free_at;
+  S.span = 0;
+  for (int s = 0; s < p; ++s) S.span = std::max(S.span, free_at[s]);
+  return S;
+}
+
+// App. B's DP over t[0..L): the minimal largest group sum over VP contiguous
+// non-empty groups, and the group sizes (ties: the smallest j).  -1 if L < VP.
+i64 partition_dp(const std::vector<i64>& t, int VP, std::vector<int>& sizes) {
+  const int L = (int)t.size();
+  sizes.clear();
+  if (VP < 1 || L < VP) return -1;
+  std::vector<i64> S(L + 1, 0);
+  for (int i = 0; i < L; ++i) S[i + 1] = S[i] + t[i];
+  // F[m][l]: first l layers over m virtual stages; arg[m][l]: the chosen j
+  std::vector<std::vector<i64>> F(VP + 1, std::vector<i64>(L + 1, INF));
+  std::vector<std::vector<int>> arg(VP + 1, std::vector<int>(L + 1, -1));
+  for (int l = 1; l <= L; ++l) F[1][l] = S[l];
+  for (int m = 2; m <= VP; ++m)
+    for (int l = m; l <= L; ++l)
+      for (int j = m - 1; j < l; ++j) {
+        i64 c = std::max(F[m - 1][j], S[l] - S[j]);
+        if (c < F[m][l]) { F[m][l] = c; arg[m][l] = j; }
+      }
+  int l = L;
+  std::vector<int> rev;
+  for (int m = VP; m >= 2; --m) {
+    int j = arg[m][l];
+    rev.push_back(l - j);
+    l = j;
+  }
+  rev.push_back(l);
+  sizes.assign(rev.rbegin(), rev.rend());
+  return F[VP][L];
+}
+
+// kind 0 naive, 1 balanced: iteration time; sizes = layers per virtual
+// stage (naive: the encoder layers counted in stage 0); -1 if not defined.
+i64 baseline(const Problem& P, int kind, std::vector<int>& sizes, std::vector<i64>& opF, std::vector<i64>& opB) {
+  const int p = (int)P.pp, v = (int)P.v, VP = p * v;
+  const size_t ti = P.tp_opts.size() - 1;  // the encoder at the LLM's TP (inside its stage)
+  std::vector<i64> tf, tb;                 // per layer, encoder first
+  for (const Branch& b : P.branches)
+    for (i64 l = 0; l < b.layers; ++l) { tf.push_back(list_sum(b.fwd[ti])); tb.push_back(list_sum(b.bwd[ti])); }
+  const int Le = (int)tf.size();
+  for (i64 l = 0; l < P.llm_layers; ++l) { tf.push_back(list_sum(P.llm_fwd)); tb.push_back(list_sum(P.llm_bwd)); }
+  const int L = (int)tf.size();
+  const int lc = (int)(P.llm_layers / VP);
+  sizes.clear();
+  if (kind == 0) {
+    for (int k = 0; k < VP; ++k) sizes.push_back(lc + (k == 0 ? Le : 0));
+  } else {
+    if (P.branches.size() != 1) return -1;
+    std::vector<i64> t(L);
+    for (int i = 0; i < L; ++i) t[i] = tf[i] + tb[i];
+    if (partition_dp(t, VP, sizes) < 0) return -1;
+  }
+  opF.assign((size_t)VP, 0);
+  opB.assign((size_t)VP, 0);
+  int i = 0;
+  for (int k = 0; k < VP; ++k) {
+    const int s = k % p, c = k / p;
+    for (int q = 0; q < sizes[k]; ++q, ++i) {
+      opF[(size_t)s * v + c] += tf[i];
+      opB[(size_t)s * v + c] += tb[i];
+    }
+  }
+  Sim S = simulate_ops(P, default_warmup(P), opF, opB);
+  if (!S.ok) return -1;
+  return S.span + P.T_rs;
+}
+
 // ------------------------------------------------------ model planner (a1)
 struct Plan {
   i64 P, T, dp_enc, m, r_p, r_t;
@@ -928,6 +1072,34 @@ long long oracle_simulate(const int64_t* blob, long long len, const int32_t* W, 
   if ((long long)o.size() > cap) return -1;
   std::memcpy(out, o.data(), o.size() * sizeof(i64));
   return (long long)o.size();
+}
+
+// Megatron-LM baseline (kind 0 naive, 1 balanced): out = [iteration ns, VP,
+// layers per virtual stage [VP], forward op ns per (stage, chunk) [VP],
+// backward [VP]]; -1 if undefined (balanced with several encoders).
+long long oracle_baseline(const int64_t* blob, long long len, int kind, int64_t* out, long long cap) {
+  Problem P;
+  if (!parse(blob, len, P)) return -1;
+  std::vector<int> sizes;
+  std::vector<i64> opF, opB;
+  i64 it = baseline(P, kind, sizes, opF, opB);
+  if (it < 0) return -1;
+  std::vector<i64> o{it, (i64)sizes.size()};
+  for (int x : sizes) o.push_back(x);
+  for (i64 x : opF) o.push_back(x);
+  for (i64 x : opB) o.push_back(x);
+  if ((long long)o.size() > cap) return -1;
+  std::memcpy(out, o.data(), o.size() * sizeof(i64));
+  return (long long)o.size();
+}
+
+// App. B's DP alone: returns F(L, VP) (-1 if L < VP), sizes[VP] = group sizes.
+long long oracle_partition_dp(const int64_t* t, int L, int VP, int32_t* sizes) {
+  std::vector<i64> tv(t, t + L);
+  std::vector<int> sz;
+  i64 r = partition_dp(tv, VP, sz);
+  for (size_t q = 0; q < sz.size(); ++q) sizes[q] = sz[q];
+  return r;
 }
 
 // Plans: out = [nplans, total, then per plan (P, T, dp_enc, m, kept, count, first)]

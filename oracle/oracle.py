@@ -44,6 +44,10 @@ def lib():
         L.oracle_llm_kernels.argtypes = [P64, ctypes.c_longlong, ctypes.c_int, P64, ctypes.c_longlong]
         L.oracle_simulate.restype = ctypes.c_longlong
         L.oracle_simulate.argtypes = [P64, ctypes.c_longlong, ctypes.POINTER(ctypes.c_int32), P64, ctypes.c_longlong]
+        L.oracle_baseline.restype = ctypes.c_longlong
+        L.oracle_baseline.argtypes = [P64, ctypes.c_longlong, ctypes.c_int, P64, ctypes.c_longlong]
+        L.oracle_partition_dp.restype = ctypes.c_longlong
+        L.oracle_partition_dp.argtypes = [P64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int32)]
         L.oracle_plans.restype = ctypes.c_longlong
         L.oracle_plans.argtypes = [P64, ctypes.c_longlong, P64, ctypes.c_longlong]
         L.oracle_unrank.restype = ctypes.c_int
@@ -175,6 +179,26 @@ def plans(prob: dict) -> dict:
         P, T, dpe, m, kept, cnt, first = o[2 + 7 * q:9 + 7 * q]
         pl.append({"P": P, "T": T, "dp_enc": dpe, "m": m, "kept": bool(kept), "count": cnt, "first": first})
     return {"total": o[1], "plans": pl}
+
+
+def baseline(prob: dict, kind: int) -> dict | None:
+    """Megatron-LM baseline iteration time (kind 0 naive P:519, 1 balanced P:521 / App. B)."""
+    blob = encode(prob)
+    out = np.zeros(16 + 3 * 4096, dtype=np.int64)
+    k = lib().oracle_baseline(_p64(blob), len(blob), kind, _p64(out), len(out))
+    if k < 0:
+        return None
+    VP = int(out[1])
+    return {"iter_ns": int(out[0]), "sizes": out[2:2 + VP].tolist(), "opF": out[2 + VP:2 + 2 * VP].tolist(),
+            "opB": out[2 + 2 * VP:2 + 3 * VP].tolist()}
+
+
+def partition_dp(t, VP: int):
+    """App. B's DP: (F(L, VP), group sizes) or (-1, [])."""
+    a = np.array(t, dtype=np.int64)
+    sz = (ctypes.c_int32 * max(1, VP))()
+    r = lib().oracle_partition_dp(_p64(a), len(a), VP, sz)
+    return int(r), (list(sz)[:VP] if r >= 0 else [])
 
 
 def unrank(n: int, m: int, rank: int) -> list[int]:

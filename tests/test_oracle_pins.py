@@ -493,3 +493,82 @@ def test_multibranch_per_encoder_split_p478(oracle_mod):
                 assert sorted(d for _, d, _, _ in ks) == want, (g, key, mvi, st)
                 seen += 1
     assert seen > 0
+
+
+# ------------------------------------------------- NEXT-2 Megatron-LM baselines
+def test_partition_dp_hand_solved(oracle_mod):
+    """App. B: F(l, m) = min_{j<l} max(F(j, m-1), sum t_(j+1..l)).
+    Hand-solved: t = 1..5 over 2 virtual stages -> [1,2,3 | 4,5], largest 9
+    (the other splits give 10, 12, 14)."""
+    assert oracle_mod.partition_dp([1, 2, 3, 4, 5], 2) == (9, [3, 2])
+    assert oracle_mod.partition_dp([5, 1, 1, 1, 1, 1], 3)[0] == 5  # the 5-layer stands alone
+    assert oracle_mod.partition_dp([1, 1], 3) == (-1, [])  # fewer layers than virtual stages
+
+
+def test_partition_dp_bruteforce(oracle_mod):
+    """The DP's value is the minimum over every split of L layers into VP
+    non-empty contiguous groups of the largest group sum (exhaustive), and
+    its returned split attains it."""
+    rng = random.Random(7)
+    for _ in range(300):
+        L = rng.randint(1, 9)
+        VP = rng.randint(1, min(L, 4))
+        t = [rng.randint(1, 20) for _ in range(L)]
+        best = None
+        for cuts in itertools.combinations(range(1, L), VP - 1):
+            b = (0,) + cuts + (L,)
+            mx = max(sum(t[b[i]:b[i + 1]]) for i in range(VP))
+            best = mx if best is None else min(best, mx)
+        val, sizes = oracle_mod.partition_dp(t, VP)
+        assert val == best, (t, VP)
+        assert len(sizes) == VP and min(sizes) >= 1 and sum(sizes) == L
+        acc, mx = 0, 0
+        for sz in sizes:
+            mx = max(mx, sum(t[acc:acc + sz]))
+            acc += sz
+        assert mx == val
+
+
+def _baseline_problem(p, v, n, t_llm, t_enc, enc_layers, llm_layers, T_ag=0, T_rs=0):
+    """Uniform single-kernel layers: LLM layer (t_llm fwd, 2 t_llm bwd), encoder
+    layer (t_enc, 2 t_enc); TP 1."""
+    enc = {"layers": enc_layers, "params": 1, "fwd": [[(0, t_enc)]], "bwd": [[(0, 2 * t_enc)]]}
+    pb = uniform_problem(p, v, n, t_llm, 2 * t_llm, T_ag=T_ag, T_rs=T_rs, enc=enc)
+    pb["llm_layers"] = llm_layers
+    return pb
+
+
+def test_baseline_balanced_uniform_closed_form(oracle_mod):
+    """Balanced: identical layers split evenly over V x PP virtual
+    stages, then Megatron's interleaved 1F1B with uniform ops: iteration =
+    T_ag + (n v + p - 1)(t_f + t_b) + T_rs (the closed form the template pin
+    uses, per virtual stage of k layers)."""
+    for p, v, n in [(2, 2, 4), (4, 2, 8), (3, 1, 6), (4, 3, 8)]:
+        VP = p * v
+        enc_layers, llm_layers = VP, VP * 2  # 3 identical layers per virtual stage
+        pb = _baseline_problem(p, v, n, 10, 10, enc_layers, llm_layers, T_ag=7, T_rs=11)
+        b = oracle_mod.baseline(pb, 1)
+        assert b["sizes"] == [3] * VP
+        assert b["iter_ns"] == 7 + (n * v + p - 1) * (30 + 60) + 11
+
+
+def test_baseline_naive_sequential_closed_form(oracle_mod):
+    """Naive (encoder in the first pipeline stage): with p = v = 1 the
+    schedule is sequential, iteration = T_ag + n (encoder + LLM, forward +
+    backward) + T_rs; with p = 2 the encoder lengthens only virtual stage 0."""
+    pb = _baseline_problem(1, 1, 3, 10, 7, 4, 5, T_ag=5, T_rs=9)
+    b = oracle_mod.baseline(pb, 0)
+    assert b["sizes"] == [4 + 5]
+    assert b["iter_ns"] == 5 + 3 * (4 * 7 + 4 * 14 + 5 * 10 + 5 * 20) + 9
+    pb = _baseline_problem(2, 1, 2, 10, 7, 4, 6)
+    b = oracle_mod.baseline(pb, 0)
+    assert b["sizes"] == [4 + 3, 3]
+    assert b["opF"] == [4 * 7 + 3 * 10, 3 * 10] and b["opB"] == [4 * 14 + 3 * 20, 3 * 20]
+
+
+def test_baseline_balanced_single_encoder_only(oracle_mod):
+    """"this DP algorithm does not apply to MLLM models that feature
+    multiple encoders"; the naive placement does."""
+    prob = config_problem(5, 16)
+    assert oracle_mod.baseline(prob, 1) is None
+    assert oracle_mod.baseline(prob, 0)["iter_ns"] > 0
