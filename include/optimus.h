@@ -207,6 +207,23 @@ int optimus_debug_plan_tables(const optimus_ctx* c, int32_t i, int64_t* h_out, s
 /* Kernel launches the last build / eval enqueued (for launch accounting). */
 int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t* eval_launches);
 
+/* Megatron-LM baselines: the iteration time of the
+ * systems the paper's headline speedups are measured against (Table 5
+ * P:598-600), under the same cost model, simulated on the GPU:
+ *   kind 0, naive: every encoder layer (all branches, at the LLM's
+ *          TP) runs in the first pipeline stage, in front of virtual stage
+ *          0's LLM layers;
+ *   kind 1, balanced (App. B): the layer sequence (encoder,
+ *          then LLM) cut into V x PP contiguous virtual stages by App. B's DP
+ *          (max virtual-stage time minimised; ties to the smallest cut);
+ *          single encoder only (EINVAL otherwise); ERANGE if there are
+ *          fewer layers than virtual stages.
+ * Both run Megatron's default interleaved 1F1B warm-up from T_ag, + T_rs.
+ * h_out (cap >= 2 + 3 V PP): [iteration ns, V PP, layers per virtual stage
+ * [V PP], forward op ns per (stage, chunk) [PP][V], backward [PP][V]].
+ * Synchronises the stream. */
+int optimus_baseline(optimus_ctx* c, int32_t kind, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream);
+
 /* K2 mode 1 instance this context launches (sized by n_mb and the largest m
  * of a plan with candidates): 0 = (B, BM) (32, 32), 1 = (64, 64),
  * 2 = (128, 64), 3 = (128, 128), 4 = (64, 16), 5 = (128, 16) slots and

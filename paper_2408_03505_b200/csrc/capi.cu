@@ -63,7 +63,8 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_rec, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_rec, o_base, total_bytes;
+  int base_L = 0, base_Le = 0;  // Megatron baselines: layers in the sequence, encoder layers among them
   int grid;
 };
 
@@ -315,6 +316,9 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_stats = take(16 * 8);
   X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN + 4) * 8);  // + the efficiency sums
   X.o_rec = take((size_t)std::max(1, X.kmax_all) * std::max(1, X.nk_max) * 4 * 8);
+  for (int b = 0; b < X.nb; ++b) X.base_Le += X.blayers[b];
+  X.base_L = X.base_Le + pb->llm_layers;
+  X.o_base = take(baseline_ws_bytes(X.base_L, X.p * X.v, X.p, X.v, X.n));
   X.total_bytes = o;
   return OPTIMUS_OK;
 }
@@ -824,6 +828,28 @@ int optimus_launch_count(const optimus_ctx* c, int32_t* build_launches, int32_t*
   if (!c) return fail(OPTIMUS_EINVAL, "ctx is NULL");
   if (build_launches) *build_launches = c->build_launches;
   if (eval_launches) *eval_launches = c->eval_launches;
+  return OPTIMUS_OK;
+}
+
+int optimus_baseline(optimus_ctx* c, int32_t kind, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream) {
+  if (!c || !h_out || !len) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  if (kind != 0 && kind != 1) return fail(OPTIMUS_EINVAL, "kind must be 0 (naive) or 1 (balanced)");
+  const Prep& X = c->X;
+  if (kind == 1 && X.nb != 1)
+    return fail(OPTIMUS_EINVAL, "the balanced partitioner is defined for a single encoder (P:778); %d branches", X.nb);
+  const int VP = X.p * X.v;
+  if (kind == 1 && X.base_L < VP)
+    return fail(OPTIMUS_ERANGE, "%d layers cannot fill %d virtual stages", X.base_L, VP);
+  const size_t need = 2 + 3 * (size_t)VP;
+  if (cap < need) return fail(OPTIMUS_ERANGE, "cap %zu < %zu", cap, need);
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int64_t* d_out = nullptr;
+  CK(launch_baseline(c->cfg, kind, X.base_L, X.base_Le, c->ws + X.o_base, &d_out, st));
+  CK(cudaMemcpyAsync(h_out, d_out, need * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_out[0] < 0) return fail(OPTIMUS_ECUDA, "baseline schedule deadlocked");
+  *len = need;
   return OPTIMUS_OK;
 }
 

@@ -126,6 +126,8 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches);
 cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches);
 size_t k1_smem_for(int nk, int p, int ci, int kmax_all);
 int k1_grid(const Cfg& c);
+size_t baseline_ws_bytes(int L, int VP, int p, int v, int n);
+cudaError_t launch_baseline(const Cfg& c, int kind, int L, int Le, void* ws, int64_t** d_out, cudaStream_t st);
 void template_attrs();
 void chains_attrs();
 void eval_thread_attrs();

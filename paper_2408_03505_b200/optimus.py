@@ -21,7 +21,7 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance",
+    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance", "optimus_baseline",
     "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
@@ -92,6 +92,7 @@ def lib():
             "optimus_debug_plan_tables": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_eval_instance": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
+            "optimus_baseline": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_set_timing": [vp, ctypes.c_int],
             "optimus_set_eval_mode": [vp, ctypes.c_int],
             "optimus_last_timing": [vp, P(ctypes.c_float), P(ctypes.c_float)],
@@ -315,6 +316,16 @@ class Ctx:
         b, e = ctypes.c_int32(), ctypes.c_int32()
         _check(lib().optimus_launch_count(self.h, ctypes.byref(b), ctypes.byref(e)))
         return b.value, e.value
+
+    def baseline(self, kind: int, stream=None) -> dict:
+        """Megatron-LM baseline iteration time: kind 0 naive, 1 balanced (App. B)."""
+        n = ctypes.c_size_t()
+        cap = 2 + 3 * 4096
+        buf = (ctypes.c_int64 * cap)()
+        _check(lib().optimus_baseline(self.h, kind, buf, cap, ctypes.byref(n), ctypes.c_void_p(_stream(stream))))
+        VP = buf[1]
+        o = list(buf)[:n.value]
+        return {"iter_ns": o[0], "sizes": o[2:2 + VP], "opF": o[2 + VP:2 + 2 * VP], "opB": o[2 + 2 * VP:2 + 3 * VP]}
 
     def eval_instance(self):
         """(K2 mode 1 instance 0-5, its persistent grid)."""
