@@ -213,6 +213,7 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   if (!w.dirty) return;
   const int lane = threadIdx.x & 31;
   const int i = w.base + lane;
+  OPT_CHECK(M || (V.ver >= 0 && V.ver <= 32767));
   if (i < V.count) (M ? V.fill : V.snap0 + V.ver * V.vstride)[i] = w.lo;  // forward: the whole block
   const int64_t cap = warp_max64(i < V.count ? w.hi - w.lo : kNegInf);
   if (lane == 0) {
@@ -554,6 +555,7 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   const PlanDesc pd = c.plans[e];
   const int P = pd.P, icap = c.icapc + c.icapm;
   int* flags = c.k1flags + pd.flag_base + (int64_t)a * (pd.kmax + 1);
+  OPT_CHECK(pd.flag_base + (int64_t)(a + 1) * (pd.kmax + 1) <= c.nflags && kf <= pd.kmax);
   if (M && kf > 0) {  // wait for forward version kf of this row
     if (threadIdx.x == 0) {
       // poll relaxed (an acquire load invalidates the SM's L1, which the
@@ -576,7 +578,10 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   volatile int* status = (volatile int*)(dsm + ub);  // [P][KM]: 0 pending, 1 done, 2 failed
   volatile int64_t* endv = (volatile int64_t*)(dsm + ub + (((size_t)L.Pmax * L.KM * 4 + 15) & ~size_t(15)));
   volatile int* stop = &stop_at;
-  auto slot = [&](int k, int st) { return pd.slot_base + ((int64_t)k * pd.rp + a) * P + st; };
+  auto slot = [&](int k, int st) {
+    OPT_CHECK(k >= 0 && k <= pd.kmax && st >= 0 && st < P);
+    return pd.slot_base + ((int64_t)k * pd.rp + a) * P + st;
+  };
 #ifdef K1_STATS
   const long long tk0 = clock64();
   if (threadIdx.x < 32 * 8) k1st[threadIdx.x >> 3][threadIdx.x & 7] = 0;

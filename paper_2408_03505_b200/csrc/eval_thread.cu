@@ -283,6 +283,7 @@ __device__ __forceinline__ int64_t tdep_fwd(const TPlan& p, const int64_t* G, in
 __device__ __forceinline__ void assign_slot(const int64_t* preBEF, const int64_t* D, const TS& s, int j, int& slot,
                                             int64_t& dep_b) {
   const int r = s.N[j] - s.kb[j];  // rank of this slot's deadline within pipeline j (R15)
+  OPT_CHECK(slot < 128 && r >= 1 && r <= 128);
   s.kb[j] += 1;
   s.own[slot] = (uint8_t)j;
   s.rk[slot] = (uint8_t)r;
@@ -535,6 +536,7 @@ __device__ __forceinline__ int64_t tdep_mask(const TPlan& p, const int64_t* G, i
   for (int t = 1, pos = 0; pos < maxneed; ++t) {
     int i = pos + 1 + k;
     while (k < K && (int)thr[k] <= i) { ++k; ++i; }
+    OPT_CHECK(i >= 1 && i <= n && t <= n);
     best = max(best, p.at(p.preEF, t) - G[i - 1]);
     pos += __popc(A);
     A &= ~E[t];
@@ -577,6 +579,7 @@ __device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS&
   int64_t best = kNegInf;
 #pragma unroll 1
   for (int u = 1, pos = 0; u <= maxN - maxkf; ++u) {
+    OPT_CHECK(pos + __popc(A & below) < kMaxN && maxN - u + 1 >= 1);
     best = max(best, p.at(p.preBEF, maxN - u + 1) - D[pos + __popc(A & below)]);
     pos += __popc(A);
     A &= ~E[u];
@@ -603,6 +606,7 @@ __device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS&
 #pragma unroll 1
   for (int q = 0; q < nm; ++q) {
     const int j = s.mvj[q];
+    OPT_CHECK(sumc + q < kMaxN && (int)s.N[j] - (int)s.c[j] - (int)s.mvk[q] >= 1);
     best = max(best, p.at(p.preBEF, (int)s.N[j] - (int)s.c[j] - (int)s.mvk[q]) - D[sumc + q]);
   }
   dep_b = best;
@@ -685,6 +689,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     int q = M;
     if (kMask) {  // trial move: js one level down, threshold bp inserted in order
       const uint32_t bit = 1u << js;
+      OPT_CHECK(cjs >= 1 && cjs <= B && M < B);
       E[cjs] &= ~bit;
       E[cjs - 1] |= bit;
 #pragma unroll 1
@@ -828,6 +833,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
 #pragma unroll 2
   for (int j = 0, off = 0; j < m; ++j, off += np1) {
     const int Nj = s.N[j];
+    OPT_CHECK(Nj >= 1 && Nj <= n && Nj <= B);
     E[Nj] |= 1u << j;
     const uint64_t k = __ldg(kj + off + Nj);  // first findCritical of both phases (R11)
     kf0 = max(kf0, (uint32_t)k);
@@ -844,6 +850,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
     for (int t = 1, pos = 0; t <= Nmax; ++t) {
       const uint32_t e = E[t];
       E[t] = A;
+      OPT_CHECK(t <= n && pos < n && pos + __popc(A & below_max) < n);
       dep = max(dep, p.at(p.preEF, t) - G[pos]);
       depb = max(depb, p.at(p.preBEF, Nmax - t + 1) - D[pos + __popc(A & below_max)]);
       pos += __popc(A);
@@ -870,6 +877,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
           uint32_t A = E[t];
           if (t == Njs) A &= ~jsbit;
           const int st1 = pos + 1;  // first position of level t (1-based): slot st1, or st1 + 1 past the threshold
+          OPT_CHECK(t <= n && (st1 < bp ? st1 - 1 : st1) < n);
           dep2 = max(dep2, p.at(p.preEF, t) - G[st1 < bp ? st1 - 1 : st1]);
           pos += __popc(A);
         }
@@ -1058,6 +1066,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     const unsigned want = __ballot_sync(0xffffffffu, pend);
     if (!want) return false;
     if (pend) {
+      OPT_CHECK(qn + __popc(want) <= kQCap);
       const int sl = (qh + qn + __popc(want & lt_mask)) & (kQCap - 1);
       Qg[warp][sl] = g;
       Qo[warp][sl] = out;

@@ -2,9 +2,26 @@
 // (Product code.  Nothing here is shared with oracle/.)
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace optimus {
+
+// Debug builds (OPTIMUS_NVCC_EXTRA=-DOPTIMUS_DEVICE_CHECKS): bounds and
+// protocol checks in the kernels; a failed check prints its site and traps.
+// (compute-sanitizer is not available on the GPU pool.)
+#ifdef OPTIMUS_DEVICE_CHECKS
+#define OPT_CHECK(cond)                                                                              \
+  do {                                                                                               \
+    if (!(cond)) {                                                                                   \
+      printf("OPT_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,          \
+             (int)blockIdx.x, (int)threadIdx.x);                                                     \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define OPT_CHECK(cond) do { } while (0)
+#endif
 
 constexpr int64_t kInf = INT64_MAX / 4;   // "no finite shift" / +infinity
 constexpr int64_t kNegInf = -(INT64_MAX / 4);
