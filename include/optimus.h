@@ -198,6 +198,21 @@ int optimus_emit_schedule(const optimus_ctx* c, uint64_t g, int64_t* h_out, size
  * (lo,hi)...]; *len = number of int64 written (ERANGE if cap too small). */
 int optimus_debug_template(const optimus_ctx* c, int64_t* h_out, size_t cap, size_t* len, void* cuda_stream);
 
+/* NEXT-4: the encoder-LLM P2P pairs of candidate g's schedule: for
+ * every LLM microbatch i (the global ordering, R14, designates its encoder
+ * pipeline j) a forward pair, activations from the last stage of pipeline j
+ * to the first LLM stage, sent at j's forward finish EF_i and arriving at
+ * EF_i + L <= F_i, and a backward pair, gradients from the first LLM stage
+ * at B_i (end of its backward) to pipeline j's last stage, arriving at
+ * B_i + L.  Reading R-P2P: endpoints are (LLM stage, TP slot b of pipeline
+ * j = a r_t + b); pipeline j's last stage sits on LLM stage a P + P - 1
+ * (R7).  Times are LLM-relative (template) ns: the executed schedule adds
+ * Df.  h_out (cap >= 18 n): per record [dir 0 fwd / 1 bwd, microbatch i,
+ * pipeline j, src stage, src slot, dst stage, dst slot, send ns, arrive ns],
+ * 2 n records in slot order (forward, backward).  Synchronises the stream. */
+int optimus_emit_p2p(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* n_records,
+                     void* cuda_stream);
+
 /* Chain tables of plan i: h_out = [r_p, kmax, lenF[r_p], INB_F[r_p][kmax],
  * lenB[r_p][kmax+1], INB_B[r_p][kmax+1][kmax], PRE_F[P][n+1], PRE_B[P][n+1]].
  * Entries past a length are unspecified. */

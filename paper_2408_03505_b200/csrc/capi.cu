@@ -63,7 +63,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_rec, o_base, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_order, o_rec, o_base, total_bytes;
   int base_L = 0, base_Le = 0;  // Megatron baselines: layers in the sequence, encoder layers among them
   int grid;
 };
@@ -315,6 +315,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_counter = take(8);
   X.o_stats = take(16 * 8);
   X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN + 4) * 8);  // + the efficiency sums
+  X.o_order = take((size_t)2 * kMaxN * 8);
   X.o_rec = take((size_t)std::max(1, X.kmax_all) * std::max(1, X.nk_max) * 4 * 8);
   for (int b = 0; b < X.nb; ++b) X.base_Le += X.blayers[b];
   X.base_L = X.base_Le + pb->llm_layers;
@@ -751,6 +752,40 @@ int optimus_emit_schedule(const optimus_ctx* c, uint64_t g, int64_t* h_out, size
   if ((rc = emit(true, mb)) != OPTIMUS_OK) return rc;
   n_records[0] = nfwd;
   n_records[1] = out / 6 - nfwd;
+  return OPTIMUS_OK;
+}
+
+int optimus_emit_p2p(const optimus_ctx* c, uint64_t g, int64_t* h_out, size_t cap, size_t* n_records,
+                     void* cuda_stream) {
+  if (!c || !h_out || !n_records) return fail(OPTIMUS_EINVAL, "NULL argument");
+  if (!c->ws) return fail(OPTIMUS_EINVAL, "host-only context (optimus_plan_only) has no device state");
+  const Prep& X = c->X;
+  const int n = X.n;
+  if (cap < (size_t)n * 2 * 9) return fail(OPTIMUS_ERANGE, "cap %zu < %d", cap, n * 2 * 9);
+  std::vector<int64_t> x(8 + 2 * kMaxN + 3 * kMaxN);
+  size_t xl = 0;
+  int rc = optimus_explain(c, g, x.data(), x.size(), &xl, cuda_stream);  // leaves its device output in place
+  if (rc != OPTIMUS_OK) return rc;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  int64_t* d_ord = (int64_t*)(c->ws + X.o_order);
+  CK(launch_order_dump(c->cfg, (const int64_t*)(c->ws + X.o_explain), d_ord, st));
+  std::vector<int64_t> ord(2 * (size_t)n), F(n), B(n);
+  CK(cudaMemcpyAsync(ord.data(), d_ord, ord.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(F.data(), c->cfg.F, n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(B.data(), c->cfg.B, n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const PlanDesc& d = X.plans[(int)x[5]].d;
+  const int64_t L = c->cfg.L;
+  size_t o = 0;
+  for (int i = 0; i < n; ++i) {  // a pair per microbatch and direction
+    const int j = (int)ord[2 * i], a = j / d.rt, b = j % d.rt;
+    const int64_t last = (int64_t)a * d.P + d.P - 1;  // LLM stage hosting pipeline j's last encoder stage (R7)
+    const int64_t rf[9] = {0, i, j, last, b, 0, b, ord[2 * i + 1], ord[2 * i + 1] + L};
+    const int64_t rb[9] = {1, i, j, 0, b, last, b, B[i], B[i] + L};
+    for (int q = 0; q < 9; ++q) h_out[o++] = rf[q];
+    for (int q = 0; q < 9; ++q) h_out[o++] = rb[q];
+  }
+  *n_records = 2 * (size_t)n;
   return OPTIMUS_OK;
 }
 

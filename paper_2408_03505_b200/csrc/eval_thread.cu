@@ -1224,6 +1224,38 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   out[0] = teval<B, true>(c, p, G, D, T_end, s, E, st, out);
 }
 
+// NEXT-4: the global ordering (R14) of an explained candidate, slot by slot:
+// out[2 i] = the pipeline whose forward finish is LLM microbatch i, out[2 i +
+// 1] = that finish (LLM-relative: coarse PRE_EF(t) - Df, moved INB_F).  One
+// thread, the plain definition: every entry, sorted by (value, pipeline,
+// local index).  xo = optimus_explain's device output.
+__global__ void k_order_dump(Cfg c, const int64_t* xo, int64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = c.n, e = (int)xo[5], m = (int)xo[6];
+  const int64_t Df = xo[1];
+  const int64_t* N = xo + 8 + 2 * n;
+  const int64_t* cf = N + m;
+  const PlanDesc& d = c.plans[e];
+  const int64_t* preEF = c.tables + d.preF + (int64_t)(d.P - 1) * (n + 1);
+  const int64_t* inbF = c.tables + d.inbF;
+  int q = 0;
+  for (int j = 0; j < m; ++j) {
+    const int a = j / d.rt;
+    for (int u = 0; u < (int)N[j]; ++u) {  // j's entries in local order: coarse t = 1..c_j, then moved
+      const int64_t v = u < cf[j] ? preEF[u + 1] - Df : inbF[(int64_t)a * d.kmax + (u - cf[j])];
+      int x = q++;
+      // insertion by (value, pipeline, local): later (j, u) keys are larger
+      while (x > 0 && out[2 * (x - 1) + 1] > v) {
+        out[2 * x] = out[2 * (x - 1)];
+        out[2 * x + 1] = out[2 * (x - 1) + 1];
+        --x;
+      }
+      out[2 * x] = j;
+      out[2 * x + 1] = v;
+    }
+  }
+}
+
 }  // namespace
 
 template <int B, int BM>
@@ -1279,6 +1311,11 @@ int eval_thread_grid(int sms, int i) {
 template <int B, int BM>
 static void explain_b(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {
   k2_explain<B, BM><<<1, kTThreads, (size_t)tsmem<B, BM>(), st>>>(c, g, d_out);
+}
+
+cudaError_t launch_order_dump(const Cfg& c, const int64_t* d_explain, int64_t* d_out, cudaStream_t st) {
+  k_order_dump<<<1, 32, 0, st>>>(c, d_explain, d_out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st) {

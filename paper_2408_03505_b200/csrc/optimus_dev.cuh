@@ -170,6 +170,7 @@ struct EvalArgs {
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
+cudaError_t launch_order_dump(const Cfg& c, const int64_t* d_explain, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
 int eval_thread_grid(int sms, int instance);
 int eval_thread_instance(int n, int mmax);

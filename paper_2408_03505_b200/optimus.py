@@ -21,7 +21,7 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance", "optimus_baseline",
+    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance", "optimus_baseline", "optimus_emit_p2p",
     "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
@@ -93,6 +93,7 @@ def lib():
             "optimus_launch_count": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_eval_instance": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_baseline": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
+            "optimus_emit_p2p": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_set_timing": [vp, ctypes.c_int],
             "optimus_set_eval_mode": [vp, ctypes.c_int],
             "optimus_last_timing": [vp, P(ctypes.c_float), P(ctypes.c_float)],
@@ -237,7 +238,7 @@ class Ctx:
 
     def explain(self, g: int, stream=None) -> dict:
         """The committed moves of candidate g (optimus_explain; NEXT-1)."""
-        buf = (ctypes.c_int64 * (8 + 2 * 32 + 3 * 32))()
+        buf = (ctypes.c_int64 * (8 + 2 * 128 + 3 * 128))()
         n = ctypes.c_size_t()
         _check(lib().optimus_explain(self.h, ctypes.c_uint64(g), buf, len(buf), ctypes.byref(n),
                                      ctypes.c_void_p(_stream(stream))))
@@ -247,6 +248,17 @@ class Ctx:
                 "moves_f": v[8:8 + nf], "moves_b": v[8 + nmb:8 + nmb + nb],
                 "N": v[8 + 2 * nmb:8 + 2 * nmb + m], "c_final": v[8 + 2 * nmb + m:8 + 2 * nmb + 2 * m],
                 "cb_final": v[8 + 2 * nmb + 2 * m:8 + 2 * nmb + 3 * m]}
+
+    def emit_p2p(self, g: int, stream=None) -> list:
+        """Encoder-LLM P2P send/recv pairs of candidate g (optimus_emit_p2p; NEXT-4): records
+        [dir, microbatch, pipeline, src stage, src slot, dst stage, dst slot, send ns, arrive ns]."""
+        cap = 18 * 128
+        buf = (ctypes.c_int64 * cap)()
+        n = ctypes.c_size_t()
+        _check(lib().optimus_emit_p2p(self.h, ctypes.c_uint64(g), buf, cap, ctypes.byref(n),
+                                      ctypes.c_void_p(_stream(stream))))
+        v = list(buf)[:9 * n.value]
+        return [v[9 * k:9 * k + 9] for k in range(n.value)]
 
     def efficiency(self, g: int, stream=None) -> dict:
         """Eff_fine / Eff_coarse of candidate g as exact work sums (optimus_efficiency; NEXT-1)."""

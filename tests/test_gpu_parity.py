@@ -698,3 +698,56 @@ def test_megatron_speedup_config4(dev, oracle_mod):
     print(f"config 4: Optimus {lat} ns, Megatron naive {naive} ns ({naive / lat - 1:.1%} slower), "
           f"balanced {bal} ns ({bal / lat - 1:.1%} slower)")
     assert lat < bal < naive
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: encoder-LLM P2P insertion and schedule export
+@pytest.mark.parametrize("prob", [toy_problem(), config_problem(2), config_problem(4)] +
+                         [random_problem(s) for s in range(12)], ids=lambda p: p["name"])
+def test_emit_p2p_matches_oracle(dev, oracle_mod, prob):
+    """optimus_emit_p2p record for record against the pairs assembled from the
+    oracle's global ordering (its trace) and its template's B_i."""
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    o = oracle_mod.Oracle(prob)
+    tpl = oracle_mod.template(prob)
+    L = prob["enc_llm_p2p_ns"]
+    plans = oracle_mod.plans(prob)["plans"]
+    for g in sample_indices(31, min(total, 24), total):
+        t = o.trace(int(g))
+        P, rt = t["P"], t["r_t"]
+        want = []
+        for i, (val, j) in enumerate(t["order"]):
+            a, b = j // rt, j % rt
+            last = a * P + P - 1
+            want.append([0, i, j, last, b, 0, b, val, val + L])
+            want.append([1, i, j, 0, b, last, b, tpl["B"][i], tpl["B"][i] + L])
+        got = ctx.emit_p2p(int(g))
+        assert got == want, g
+        for r in got:  # the dependencies the pairs serve (R20)
+            if r[0] == 0:
+                assert r[8] <= tpl["F"][r[1]] + t["df"]
+
+
+def test_schedule_export(dev, tmp_path):
+    """The winner of config 4 as JSON and Chrome trace: every emitted kernel and
+    P2P pair appears, events are well formed."""
+    torch = dev
+    from paper_2408_03505_b200 import export
+    prob = config_problem(4)
+    ctx = _load(prob)
+    total, _ = ctx.num_candidates()
+    b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+    ctx.eval_candidates(0, total, b2)
+    torch.cuda.synchronize()
+    g = int(b2[1].item())
+    sch = export.schedule(ctx, g)
+    assert sch["lat_ns"] == int(b2[0].item()) and len(sch["p2p"]["records"]) == 2 * prob["n_mb"]
+    tr = export.chrome_trace(ctx, g)
+    nk = len(sch["encoder_kernels"]["forward"]) + len(sch["encoder_kernels"]["backward"])
+    assert sum(1 for e in tr["traceEvents"] if e["name"].startswith("enc ")) == nk
+    assert sum(1 for e in tr["traceEvents"] if e["name"].startswith("p2p ")) == 4 * prob["n_mb"]
+    assert all(e["ph"] == "X" and e["dur"] >= 0 for e in tr["traceEvents"])
+    export.write(ctx, g, str(tmp_path / "c4.trace.json"))
+    import json
+    assert json.load(open(tmp_path / "c4.trace.json"))["otherData"]["candidate"] == g
