@@ -52,6 +52,9 @@ def parse_args():
     ap.add_argument("--sample", type=int, default=0,
                     help="evaluate K seeded splitmix64 indices (resident in HBM) instead of the whole space, "
                          "e.g. config 5 at N_mb 128 (3.6e11 candidates)")
+    ap.add_argument("--sweep", type=str, default="",
+                    help="NEXT-3: comma-separated N_mb values of --config searched as one sweep (one call), "
+                         "e.g. --config 5 --sweep 16,32,64")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no clocks/cpu/e2e legs")
@@ -214,6 +217,95 @@ def cpu_baseline(ctx, prob, torch):
             {"sample": count, "mismatches": mism})
 
 
+def run_sweep(args, rank, world, local):
+    """NEXT-3 bench line: several LLM templates (config --config at each N_mb
+    of --sweep) searched in one call per step (optimus_sweep_eval: every
+    template's build + evaluation of this rank's shard, one stream), then the
+    [count, 2] gather.  value = candidates of all the templates / step time."""
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if dist:
+        dist.barrier()
+    from paper_2408_03505_b200 import optimus as OP
+    from workload import config_problem
+    ns = [int(x) for x in args.sweep.split(",")]
+    probs = [config_problem(args.config, n) for n in ns]
+    stream = torch.cuda.current_stream()
+    sw = OP.Sweep(probs, stream)
+    totals = [c.num_candidates()[0] for c in sw.ctxs]
+    units = sum(totals)
+    best = torch.empty((len(probs), 2), dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        sw.eval(best, rank=rank, world=world, stream=stream)
+        if world > 1:
+            out = torch.empty((world, len(probs), 2), dtype=torch.int64, device="cuda")
+            dist.all_gather_into_tensor(out.view(-1), best.view(-1))
+            return out
+        return best.view(1, len(probs), 2)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    os.dup2(saved, 1)
+    os.close(saved)
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    ms = []
+    g = None
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g = step()
+        e1.record(stream)
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_per_step = float(tot.item()) / args.steps
+    gg = g.cpu().numpy()
+    winners = []
+    for i, c in enumerate(sw.ctxs):
+        r = c.best_plan(gg[:, i, :])
+        winners.append({"n_mb": ns[i], "candidates": int(totals[i]), "lat_ns": r["lat_ns"], "index": r["index"],
+                        "enc_plan": r["enc"], "partition": r["counts"]})
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": units / (ms_per_step / 1000.0), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": f"c{args.config}_sweep_nmb_" + "_".join(map(str, ns)), "candidates": int(units),
+                       "templates": len(ns), "l2": "flushed before every timed step (256 MiB memset)",
+                       "parallelism": f"candidates-dp{world}", "api": "optimus_sweep_eval (one call per step)"},
+            "winners": winners, "clocks": clocks, "roofline": None, "e2e": None, "cpu_baseline": None,
+        }), flush=True)
+    sw.free()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     rank = int(os.environ.get("RANK", "0"))
@@ -225,6 +317,9 @@ def main():
         sys.exit(subprocess.call(cmd))
 
     from workload import config_problem
+    if args.sweep:
+        run_sweep(args, rank, world, local)
+        return
     prob = config_problem(args.config, args.n_mb)
     name = prob["name"]
     if args.impl == "reference":

@@ -274,6 +274,25 @@ int optimus_io_bytes(const optimus_ctx* c, uint64_t* h2d, uint64_t* d2h);
 
 void optimus_free(optimus_ctx* c);
 
+/* NEXT-3: a sweep over LLM templates.  The planner fixes the LLM plan (P:254,
+ * P:303); a sweep makes (LLM plan, V, N_mb, warm-up policy) an outer axis of
+ * one search: count problems (one per template, each validated as by
+ * optimus_load_costs) loaded back to back into one caller workspace
+ * (optimus_sweep_workspace_bytes).  optimus_sweep_eval enqueues, on one
+ * stream, every template's build and the evaluation of this rank's shard of
+ * its whole space, and writes template i's (lat, index) to d_best[2 i ..]
+ * (asynchronous; decode with optimus_best_plan on optimus_sweep_ctx(i), a
+ * borrowed context valid until optimus_sweep_free).  Comparing lats across
+ * templates is the caller's choice: templates with different N_mb train
+ * different global batches. */
+typedef struct optimus_sweep optimus_sweep;
+int optimus_sweep_workspace_bytes(const optimus_problem* pbs, int32_t count, size_t* bytes);
+int optimus_sweep_load(const optimus_problem* pbs, int32_t count, void* d_workspace, size_t bytes, void* cuda_stream,
+                       optimus_sweep** out);
+int optimus_sweep_eval(optimus_sweep* sw, uint32_t rank, uint32_t world, int64_t* d_best, void* cuda_stream);
+int optimus_sweep_ctx(optimus_sweep* sw, int32_t i, optimus_ctx** ctx);
+void optimus_sweep_free(optimus_sweep* sw);
+
 const char* optimus_last_error(void);
 
 #ifdef __cplusplus

@@ -955,4 +955,75 @@ int optimus_io_bytes(const optimus_ctx* c, uint64_t* h2d, uint64_t* d2h) {
 
 void optimus_free(optimus_ctx* c) { delete c; }
 
+// ---------------------------------------------------------------- NEXT-3
+// A sweep over LLM templates (LLM plan, V, N_mb, warm-up policy): the
+// planner fixes the LLM plan; the sweep makes it an outer axis
+// of one search.  One context per template, laid out back to back in one
+// workspace; eval enqueues every template's build and evaluation on one
+// stream (each K2 overlapping its own K1) and writes each template's best.
+struct optimus_sweep {
+  std::vector<optimus_ctx*> ctx;
+  ~optimus_sweep() {
+    for (auto* c : ctx) delete c;
+  }
+};
+
+int optimus_sweep_workspace_bytes(const optimus_problem* pbs, int32_t count, size_t* bytes) {
+  if (!pbs || count < 1 || !bytes) return fail(OPTIMUS_EINVAL, "NULL argument or count < 1");
+  size_t t = 0;
+  for (int i = 0; i < count; ++i) {
+    size_t b = 0;
+    const int rc = optimus_workspace_bytes(&pbs[i], &b);
+    if (rc) return rc;
+    t += align256(b);
+  }
+  *bytes = t;
+  return OPTIMUS_OK;
+}
+
+int optimus_sweep_load(const optimus_problem* pbs, int32_t count, void* d_workspace, size_t bytes, void* cuda_stream,
+                       optimus_sweep** out) {
+  if (!out) return fail(OPTIMUS_EINVAL, "out is NULL");
+  *out = nullptr;
+  size_t need = 0;
+  int rc = optimus_sweep_workspace_bytes(pbs, count, &need);
+  if (rc) return rc;
+  if (bytes < need) return fail(OPTIMUS_ENOSPACE, "workspace has %zu bytes, the sweep needs %zu", bytes, need);
+  optimus_sweep* sw = new optimus_sweep;
+  size_t off = 0;
+  for (int i = 0; i < count; ++i) {
+    size_t b = 0;
+    optimus_workspace_bytes(&pbs[i], &b);
+    optimus_ctx* c = nullptr;
+    rc = optimus_load_costs(&pbs[i], (char*)d_workspace + off, b, cuda_stream, &c);
+    if (rc) {
+      delete sw;
+      return rc;
+    }
+    sw->ctx.push_back(c);
+    off += align256(b);
+  }
+  *out = sw;
+  return OPTIMUS_OK;
+}
+
+int optimus_sweep_eval(optimus_sweep* sw, uint32_t rank, uint32_t world, int64_t* d_best, void* cuda_stream) {
+  if (!sw || !d_best) return fail(OPTIMUS_EINVAL, "NULL argument");
+  for (size_t i = 0; i < sw->ctx.size(); ++i) {
+    optimus_ctx* c = sw->ctx[i];
+    int rc = optimus_rebuild(c, cuda_stream);
+    if (!rc) rc = optimus_eval_candidates(c, 0, c->X.total, rank, world, 4096, nullptr, d_best + 2 * i, cuda_stream);
+    if (rc) return rc;
+  }
+  return OPTIMUS_OK;
+}
+
+int optimus_sweep_ctx(optimus_sweep* sw, int32_t i, optimus_ctx** ctx) {
+  if (!sw || !ctx || i < 0 || i >= (int)sw->ctx.size()) return fail(OPTIMUS_EINVAL, "bad sweep index");
+  *ctx = sw->ctx[i];
+  return OPTIMUS_OK;
+}
+
+void optimus_sweep_free(optimus_sweep* sw) { delete sw; }
+
 }  // extern "C"

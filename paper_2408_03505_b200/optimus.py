@@ -21,7 +21,8 @@ ERRORS = {-1: "EINVAL", -2: "EINFEASIBLE", -3: "ECUDA", -4: "ENOSPACE", -5: "ERA
 HEADER_SYMBOLS = [
     "optimus_workspace_bytes", "optimus_plan_only", "optimus_load_costs", "optimus_rebuild", "optimus_num_candidates",
     "optimus_get_plan", "optimus_eval_candidates", "optimus_eval_indices", "optimus_best_plan",
-    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance", "optimus_baseline", "optimus_emit_p2p",
+    "optimus_explain", "optimus_emit_schedule", "optimus_efficiency", "optimus_debug_template", "optimus_debug_plan_tables", "optimus_launch_count", "optimus_eval_instance", "optimus_baseline", "optimus_emit_p2p", "optimus_sweep_workspace_bytes", "optimus_sweep_load",
+    "optimus_sweep_eval", "optimus_sweep_ctx", "optimus_sweep_free",
     "optimus_set_eval_mode",
     "optimus_set_timing",
     "optimus_last_timing", "optimus_eval_stats", "optimus_io_bytes", "optimus_free", "optimus_last_error",
@@ -94,6 +95,10 @@ def lib():
             "optimus_eval_instance": [vp, P(ctypes.c_int32), P(ctypes.c_int32)],
             "optimus_baseline": [vp, ctypes.c_int32, P(ctypes.c_int64), sz, P(sz), vp],
             "optimus_emit_p2p": [vp, ctypes.c_uint64, P(ctypes.c_int64), sz, P(sz), vp],
+            "optimus_sweep_workspace_bytes": [P(optimus_problem), ctypes.c_int32, P(sz)],
+            "optimus_sweep_load": [P(optimus_problem), ctypes.c_int32, vp, sz, vp, P(vp)],
+            "optimus_sweep_eval": [vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp],
+            "optimus_sweep_ctx": [vp, ctypes.c_int32, P(vp)],
             "optimus_set_timing": [vp, ctypes.c_int],
             "optimus_set_eval_mode": [vp, ctypes.c_int],
             "optimus_last_timing": [vp, P(ctypes.c_float), P(ctypes.c_float)],
@@ -204,6 +209,14 @@ class Ctx:
                                             ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
         self.h = h
         self.n_mb = problem.n_mb
+        self._owned = True
+
+    @classmethod
+    def borrowed(cls, problem: Problem, workspace, h):
+        """A context owned elsewhere (a Sweep's): never freed by this object."""
+        c = cls.__new__(cls)
+        c.problem, c.workspace, c.h, c.n_mb, c._owned = problem, workspace, h, problem.n_mb, False
+        return c
 
     def rebuild(self, stream=None):
         _check(lib().optimus_rebuild(self.h, ctypes.c_void_p(_stream(stream))))
@@ -372,7 +385,8 @@ class Ctx:
 
     def free(self):
         if getattr(self, "h", None):
-            lib().optimus_free(self.h)
+            if getattr(self, "_owned", True):
+                lib().optimus_free(self.h)
             self.h = None
 
     def __del__(self):
@@ -389,6 +403,46 @@ def optimus_load_costs(prob: dict, stream=None, device="cuda") -> Ctx:
     nbytes = optimus_workspace_bytes(P)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
     return Ctx(P, ws, stream)
+
+
+class Sweep:
+    """NEXT-3: several LLM templates searched in one call (optimus_sweep_*)."""
+
+    def __init__(self, probs: list, stream=None, device="cuda"):
+        import torch
+        self.problems = [Problem(p) for p in probs]
+        arr = (optimus_problem * len(probs))(*[p.s for p in self.problems])
+        self._arr = arr
+        nb = ctypes.c_size_t()
+        _check(lib().optimus_sweep_workspace_bytes(arr, len(probs), ctypes.byref(nb)))
+        self.workspace = torch.empty(nb.value, dtype=torch.uint8, device=device)
+        h = ctypes.c_void_p()
+        _check(lib().optimus_sweep_load(arr, len(probs), ctypes.c_void_p(self.workspace.data_ptr()), nb.value,
+                                        ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
+        self.h = h
+        self.ctxs = []
+        for i in range(len(probs)):
+            c = ctypes.c_void_p()
+            _check(lib().optimus_sweep_ctx(self.h, i, ctypes.byref(c)))
+            self.ctxs.append(Ctx.borrowed(self.problems[i], self.workspace, c))
+
+    def eval(self, best, rank: int = 0, world: int = 1, stream=None):
+        """best: int64 device tensor [count, 2] <- each template's (lat, index) over this rank's shard."""
+        _check(lib().optimus_sweep_eval(self.h, rank, world, ctypes.c_void_p(best.data_ptr()),
+                                        ctypes.c_void_p(_stream(stream))))
+
+    def free(self):
+        if self.h:
+            for c in self.ctxs:
+                c.h = None
+            lib().optimus_sweep_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def optimus_plan_only(prob: dict) -> Ctx:

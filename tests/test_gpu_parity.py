@@ -751,3 +751,35 @@ def test_schedule_export(dev, tmp_path):
     export.write(ctx, g, str(tmp_path / "c4.trace.json"))
     import json
     assert json.load(open(tmp_path / "c4.trace.json"))["otherData"]["candidate"] == g
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: a sweep over LLM templates in one call
+def test_sweep_matches_single_templates(dev, oracle_mod):
+    """optimus_sweep_*: config 5's N_mb 16 / 32 templates plus three other
+    LLM templates in one workspace and one call; every template's best equals
+    its own single search, and the oracle's where the space is small."""
+    torch = dev
+    from paper_2408_03505_b200.optimus import Sweep
+    probs = [config_problem(5, 16), config_problem(5, 32), toy_problem(), random_problem(4), config_problem(2)]
+    sw = Sweep(probs)
+    best = torch.empty((len(probs), 2), dtype=torch.int64, device="cuda")
+    sw.eval(best)
+    torch.cuda.synchronize()
+    got = best.cpu().numpy()
+    for i, prob in enumerate(probs):
+        ctx = _load(prob)
+        total, _ = ctx.num_candidates()
+        b2 = torch.empty(2, dtype=torch.int64, device="cuda")
+        ctx.eval_candidates(0, total, b2)
+        torch.cuda.synchronize()
+        assert (int(got[i][0]), int(got[i][1])) == tuple(int(x) for x in b2.cpu().numpy()), prob["name"]
+        if total <= 30000:
+            assert (int(got[i][0]), int(got[i][1])) == oracle_mod.Oracle(prob).best(threads=THREADS), prob["name"]
+        res = sw.ctxs[i].best_plan(got[i:i + 1])
+        assert res["lat_ns"] == int(got[i][0])
+    # a second sweep evaluation (rebuild + eval) is identical
+    sw.eval(best)
+    torch.cuda.synchronize()
+    assert (best.cpu().numpy() == got).all()
+    sw.free()
