@@ -19,6 +19,10 @@
 
 using namespace optimus;
 
+#ifndef K2_QUEUE_LOG2
+#define K2_QUEUE_LOG2 26
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -63,8 +67,9 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_explain, o_order, o_rec, o_base, total_bytes;
-  int base_L = 0, base_Le = 0;  // Megatron baselines: layers in the sequence, encoder layers among them
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_gq, o_gqo, o_gqn, o_partials2, o_explain, o_order, o_rec, o_base, total_bytes;
+  int base_L = 0, base_Le = 0;
+  uint64_t gqcap = 0;  // Megatron baselines: layers in the sequence, encoder layers among them
   int grid;
 };
 
@@ -312,6 +317,14 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_snap_own = take((size_t)X.n_slots * 2 * ((std::max(X.icapc, X.icapm) + 31) / 32) * 2);
   X.grid = 148 * 8;  // upper bound for partials; actual grid set at load
   X.o_partials = take((size_t)4096 * 2 * 8);
+  // K2 mode 1's queue from the fast to the general kernel: a chunk of up to
+  // 2^K2_QUEUE_LOG2 candidates + the batches the fast warps (<= 4096 blocks
+  // of 4) may leave partly used (16 B per slot)
+  X.gqcap = std::min<uint64_t>(X.total, (uint64_t)1 << K2_QUEUE_LOG2) + (uint64_t)kGqBatch * 4096 * 4;
+  X.o_gq = take((size_t)X.gqcap * 8);
+  X.o_gqo = take((size_t)X.gqcap * 8);
+  X.o_gqn = take(64);  // [0] u32 reserved slots, [8] u64 general kernel's work counter
+  X.o_partials2 = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
   X.o_stats = take(16 * 8);
   X.o_explain = take((size_t)(8 + 2 * kMaxN + 3 * kMaxN + 4) * 8);  // + the efficiency sums
@@ -331,7 +344,7 @@ struct optimus_ctx {
   Cfg cfg;
   char* ws = nullptr;
   int sms = 0;
-  int grid = 0, grid_thread = 0;
+  int grid = 0, grid_thread = 0, grid_general = 0;
   int mode = 1;  // K2 variant: 1 = one candidate per thread (default), 0 = one per warp
   int build_launches = 0, eval_launches = 0;
   bool timing = false;
@@ -351,6 +364,7 @@ namespace {
 struct DeviceInfo {
   int grid = 0;
   int grid_thread[6] = {0, 0, 0, 0, 0, 0};
+  int grid_general[6] = {0, 0, 0, 0, 0, 0};
 };
 
 DeviceInfo device_info(int dev, int sms) {
@@ -365,6 +379,7 @@ DeviceInfo device_info(int dev, int sms) {
   DeviceInfo d;
   d.grid = std::min(4096, eval_grid(sms));
   for (int i = 0; i < 6; ++i) d.grid_thread[i] = std::min(4096, eval_thread_grid(sms, i));
+  for (int i = 0; i < 6; ++i) d.grid_general[i] = std::min(4096, eval_general_grid(sms, i));
   cache[dev] = d;
   return d;
 }
@@ -476,6 +491,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   const DeviceInfo di = device_info(dev, sms);  // function attributes + occupancy, once per device
   c->grid = di.grid;
   c->grid_thread = di.grid_thread[eval_thread_instance(X.n, plans_mmax(X))];  // K2 mode 1 instance
+  c->grid_general = di.grid_general[eval_thread_instance(X.n, plans_mmax(X))];
   c->ws = (char*)d_workspace;
   c->cfg = make_cfg(X, pb, c->ws);
   c->cfg.sms = sms;
@@ -548,6 +564,13 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
     return fail(OPTIMUS_ERANGE, "eval mode 0 (one lane per slot) takes n_mb <= %d; n_mb = %d needs mode 1", kMaxNWarp, c->X.n);
   a.grid = c->mode == 1 ? c->grid_thread : c->grid;
   a.stats = (unsigned long long*)(c->ws + c->X.o_stats);
+  a.gq = (unsigned long long*)(c->ws + c->X.o_gq);
+  a.gqo = (unsigned long long*)(c->ws + c->X.o_gqo);
+  a.gqn = (unsigned int*)(c->ws + c->X.o_gqn);
+  a.counter2 = (unsigned long long*)(c->ws + c->X.o_gqn + 8);
+  a.gqcap = c->X.gqcap;
+  a.partials2 = (int64_t*)(c->ws + c->X.o_partials2);
+  a.grid2 = c->mode == 1 ? c->grid_general : 0;
   a.pclaim = c->cfg.pclaim;
   a.nplans = c->cfg.E;
   a.ev0 = c->timing ? c->ev[2] : nullptr;

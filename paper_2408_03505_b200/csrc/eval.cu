@@ -452,6 +452,8 @@ __global__ void k3_reduce(EvalArgs A) {
   int64_t l = INT64_MAX;
   uint64_t g = UINT64_MAX;
   for (int i = threadIdx.x; i < A.grid; i += blockDim.x) better(A.partials[2 * i], (uint64_t)A.partials[2 * i + 1], l, g);
+  for (int i = threadIdx.x; i < A.grid2; i += blockDim.x)  // K2 mode 1's general kernel
+    better(A.partials2[2 * i], (uint64_t)A.partials2[2 * i + 1], l, g);
   l_sm[threadIdx.x] = l;
   g_sm[threadIdx.x] = g;
   __syncthreads();
@@ -493,7 +495,7 @@ cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* l
   }
   if (a.ev1) cudaEventRecord(a.ev1, st);
   k3_reduce<<<1, 256, 0, st>>>(a);
-  if (launches) *launches += 2;
+  if (launches) *launches += a.mode == 1 ? 1 + 2 * eval_thread_chunks(a) : 2;
   return cudaGetLastError();
 }
 

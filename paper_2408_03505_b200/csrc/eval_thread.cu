@@ -40,9 +40,11 @@ constexpr int kTMinRun = K2T_MINRUN;      // fewest consecutive candidates per t
 #define K2T_GSS_DEN 1
 #endif
 constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remaining * GSS / (GSS_DEN * warps), capped
-constexpr int kQCap = 64;                 // per-warp general-path queue (a power of 2 >= 63)
 #ifndef K2T_MINB
-#define K2T_MINB 4  // resident blocks per SM the register cap aims at (smem allows 4)
+#define K2T_MINB 6  // fast kernel: resident blocks per SM the register cap aims at (smem allows 6)
+#endif
+#ifndef K2T_GMINB
+#define K2T_GMINB 5  // general kernel
 #endif
 // per-thread scratch for n <= B slots and m <= BM pipelines, an odd number of
 // words: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 780; (128, 128) 1028;
@@ -52,12 +54,9 @@ template <int B, int BM = B>
 __host__ __device__ constexpr int tstride() {
   return ((4 * BM + 4 * B > 2 * BM + 5 * B + 8 ? 4 * BM + 4 * B : 2 * BM + 5 * B + 8) + 4) | 4;
 }
-// general-path queue entry: a composition of m <= 32 parts at an odd word stride
-template <int BM>
-__host__ __device__ constexpr int tqstride() { return (BM < 32 ? BM : 32) + 4; }
-// dynamic shared memory of a K2 mode 1 block: per-thread scratch + the warps' queues
+// dynamic shared memory of a K2 mode 1 block: the per-thread scratch
 template <int B, int BM>
-__host__ __device__ constexpr int tsmem() { return kTThreads * tstride<B, BM>() + (kTThreads / 32) * kQCap * tqstride<BM>(); }
+__host__ __device__ constexpr int tsmem() { return kTThreads * tstride<B, BM>(); }
 
 // Per-thread scratch (bytes 0..8B-1, B = 32 shown).  The three phases of one
 // candidate use disjoint live sets, so bytes 2B..8B-1 are shared between them:
@@ -966,16 +965,52 @@ __device__ __forceinline__ void tbetter(int64_t lat, uint64_t g, int64_t& bl, ui
   if (lat < bl || (lat == bl && g < bg)) { bl = lat; bg = g; }
 }
 
-template <bool EXPLICIT, int B, int BM>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
-    k2_eval_thread(Cfg c, EvalArgs A) {
-  __shared__ int64_t G[B], D[B];
+// block argmin of the warps' bests into this block's partial (written on a
+// range's first chunk, merged into on the later ones)
+__device__ __forceinline__ void block_best(int64_t bl, uint64_t bg, int64_t* partials, int first) {
   __shared__ long long bl_sm[kTThreads / 32];
   __shared__ unsigned long long bg_sm[kTThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+    const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+    tbetter(ol, og, bl, bg);
+  }
+  if (lane == 0) { bl_sm[warp] = bl; bg_sm[warp] = bg; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t l = INT64_MAX;
+    uint64_t gg = UINT64_MAX;
+    if (!first) { l = partials[2 * blockIdx.x]; gg = (uint64_t)partials[2 * blockIdx.x + 1]; }
+    for (int w = 0; w < kTThreads / 32; ++w) tbetter(bl_sm[w], bg_sm[w], l, gg);
+    partials[2 * blockIdx.x] = l;
+    partials[2 * blockIdx.x + 1] = (int64_t)gg;
+  }
+}
+
+__device__ __forceinline__ void flush_stats(const TStats& st, unsigned long long* stats) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 12; ++i) {
+    unsigned v = st.v[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && stats && v) atomicAdd(&stats[i], (unsigned long long)v);
+  }
+}
+
+// K2 mode 1, fast kernel: every candidate of this rank's shard (range) or of
+// the index list (EXPLICIT) through tfast; the candidates it hands over (and
+// every candidate of a plan it does not cover: m > 32 or PRE_EF not strictly
+// increasing) go to the global queue for k2_general, one warp-reserved batch
+// of kGqBatch slots at a time (unused slots marked ~0).
+template <bool EXPLICIT, int B, int BM>
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
+    k2_fast(Cfg c, EvalArgs A) {
+  __shared__ int64_t G[B], D[B];
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
   __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
   __shared__ uint64_t psuf[EXPLICIT ? 1 : kMaxE + 1];  // this rank's positions of the plans at k2order[k..]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, n = c.n;
+  const int lane = threadIdx.x & 31, n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     G[i] = c.F[i] - c.L;          // EF_i + L <= F_i
@@ -997,13 +1032,6 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     for (int k = c.n_k2order - 1; k >= 0; --k) psuf[k] = acc += pn[c.k2order[k]];
   }
   __syncthreads();
-#ifdef PDL_PROBE
-  if (!EXPLICIT && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicMin(reinterpret_cast<unsigned long long*>(c.k1next) + 3, t);
-  }
-#endif
   TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * tstride<B, BM>()));
   uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * tstride<B, BM>() + 2 * BM);  // tfast's masks (zero)
   for (int t = 0; t < B + 2; ++t) E[t] = 0u;
@@ -1012,73 +1040,39 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   int64_t bl = INT64_MAX;
   uint64_t bg = UINT64_MAX;
-  // Per-warp queue of the candidates the fast path hands to the general path
-  // (teval): they are evaluated 32 at a time, one per lane, so the long
-  // general evaluation runs with full warps.  An entry is the composition
-  // (QB bytes at an odd word stride: lanes reading entry l hit distinct
-  // banks), its index g, lat_out position and plan.  Plans the fast path does
-  // not cover (m > 32 or PRE_EF not strictly increasing) run teval directly.
-  constexpr int QS = tqstride<BM>();
-  const uint32_t qoff = (uint32_t)(kTThreads * tstride<B, BM>() + warp * kQCap * QS);  // this warp's entries
-  __shared__ unsigned long long Qg[kTThreads / 32][kQCap], Qo[kTThreads / 32][kQCap];
-  __shared__ uint8_t Qe[kTThreads / 32][kQCap];
-  int qh = 0, qn = 0;  // warp-uniform ring head and length
   const unsigned lt_mask = (1u << lane) - 1u;
-  // general-path evaluation of k queued entries (warp-uniform k <= 32)
-  auto run_queue = [&](int k) {
-    if (lane < k) {
-      const int sl = (qh + lane) & (kQCap - 1);
-      const uint64_t gq = Qg[warp][sl], oq = Qo[warp][sl];
-      const int eq = Qe[warp][sl];
-      if (eq != p.e) tplan(c, eq, p);
-      TS sq = s;
-      sq.N = SB{qoff + (uint32_t)(sl * QS)};  // teval only reads N; the lane's own composition stays in s.N
-      const int64_t lat = teval<B>(c, p, G, D, T_end, sq, E, st);
-      if (A.lat_out) A.lat_out[oq] = lat;
-      tbetter(lat, gq, bl, bg);
-      for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval's scratch overlaps the fast path's masks
-    }
-    __syncwarp();
-    qh = (qh + k) & (kQCap - 1);
-    qn -= k;
-  };
-  // one candidate per lane (valid lanes): fast path, else queue (fast plans)
-  // or direct general evaluation (other plans); true if the queue ran
-  auto step = [&](bool valid, uint64_t g, uint64_t out, int e) -> bool {
+  unsigned qb = 0, qe = 0;  // this warp's reserved queue slots [qb, qe) (warp-uniform)
+  // one candidate per lane (valid lanes): fast path, else into the queue
+  auto step = [&](bool valid, uint64_t g, uint64_t out, int e) {
     bool pend = false;
     if (valid) {
-      int64_t lat = 0;
-      bool done = true;
-      if (p.fast) {
-        int64_t Df, Db;
-        done = tfast<B>(p, G, D, n, s, E, Df, Db, st);
-        lat = T_end + Df + Db;  // R16
-      } else {
-        lat = teval<B>(c, p, G, D, T_end, s, E, st);
-        for (int t = 0; t < B + 2; ++t) E[t] = 0u;
-      }
-      if (done) {
+      int64_t Df, Db;
+      if (p.fast && tfast<B>(p, G, D, n, s, E, Df, Db, st)) {
+        const int64_t lat = T_end + Df + Db;  // R16
         if (A.lat_out) A.lat_out[out] = lat;
         tbetter(lat, g, bl, bg);
+      } else {
+        pend = true;
       }
-      pend = !done;
     }
     const unsigned want = __ballot_sync(0xffffffffu, pend);
-    if (!want) return false;
-    if (pend) {
-      OPT_CHECK(qn + __popc(want) <= kQCap);
-      const int sl = (qh + qn + __popc(want & lt_mask)) & (kQCap - 1);
-      Qg[warp][sl] = g;
-      Qo[warp][sl] = out;
-      Qe[warp][sl] = (uint8_t)e;
-      const SB dst{qoff + (uint32_t)(sl * QS)};
-      for (int w = 0; w < (p.m + 3) / 4; ++w) dst.w(w) = s.N.w(w);
+    if (!want) return;
+    const unsigned k = __popc(want);
+    if (qb + k > qe) {  // a new batch; the rest of the old one stays unused
+      for (unsigned x = qb + lane; x < qe; x += 32) A.gq[x] = ~0ull;
+      unsigned r = 0;
+      if (lane == 0) r = atomicAdd(A.gqn, (unsigned)kGqBatch);
+      r = __shfl_sync(0xffffffffu, r, 0);
+      OPT_CHECK(r + kGqBatch <= A.gqcap);
+      qb = r;
+      qe = r + kGqBatch;
     }
-    qn += __popc(want);
-    __syncwarp();
-    if (qn < 32) return false;
-    run_queue(32);
-    return true;
+    if (pend) {  // (the index g may use 64 bits; lat_out positions stay below 2^56)
+      const unsigned x = qb + __popc(want & lt_mask);
+      A.gq[x] = g;
+      A.gqo[x] = out | (uint64_t)e << 56;
+    }
+    qb += k;
   };
   if (EXPLICIT) {
     const uint64_t nchunks = (A.count + 31) / 32;
@@ -1107,8 +1101,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     // launch may overlap K1).  This rank's positions: block-cyclic over
     // [begin, end); plan e's are [plo[e], plo[e] + pn[e]).  A warp claims
     // 32 * r consecutive positions of one plan at a time (r consecutive
-    // candidates per lane), r from 16 down to 1 as the plan's remaining work
-    // shrinks (guided self-scheduling: no long tail when work is scarce).
+    // candidates per lane), r from kTRun down to 1 as the launch's remaining
+    // work shrinks (guided self-scheduling: no long tail when work is scarce).
     const uint64_t nwarps = (uint64_t)gridDim.x * (kTThreads / 32);
     for (;;) {
       int e = -1;
@@ -1128,9 +1122,6 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
             }
             const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
             const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
-            // claim size from the work left in this and the later plans: the
-            // full kTRun-run claims while there is plenty (every run start costs
-            // an unranking), shrinking only near the end of the whole launch
             const unsigned long long left = rem + psuf[k + 1];
             const unsigned long long tk = min(32ull * kTRun, max(32ull * kTMinRun, left * kTGss / (kTGssDen * nwarps) / 32 * 32));
             const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
@@ -1148,7 +1139,9 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
       if (e < 0) break;
       if (e != p.e) tplan(c, e, p);
       const int r = (int)(take / 32);
+#ifndef K2T_GSTATS
       st.v[10] += lane == 0;
+#endif
       const uint64_t p0 = plo[e] + chunk + (uint64_t)lane * r, pend = plo[e] + pn[e];
       uint64_t g = 0;
       for (int it = 0; it < r; ++it) {  // the same trip count on every lane (warp-synchronous queue)
@@ -1159,38 +1152,65 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
             const uint64_t rb = q / A.block;
             g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
             tunrank<B>(c, n, p.m, g - p.first, s);
+#ifndef K2T_GSTATS
             st.v[11] += 1;
+#endif
           } else {
             ++g;
             tnext(p.m, s);
           }
         }
-        if (step(valid, g, g - A.begin, e) && e != p.e) tplan(c, e, p);  // the queue ran: this lane's plan back
+        step(valid, g, g - A.begin, e);
       }
     }
   }
-  if (qn > 0) run_queue(qn);  // the rest of the queue, part of a warp
-  // warp + block argmin -> partials; counters
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
-    const uint64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
-    tbetter(ol, og, bl, bg);
+  for (unsigned x = qb + lane; x < qe; x += 32) A.gq[x] = ~0ull;  // the tail of this warp's last batch
+  flush_stats(st, A.stats);
+  block_best(bl, bg, A.partials, A.first_chunk);
+}
+
+// K2 mode 1, general kernel: the queued candidates through teval (the whole
+// algorithm), warps taking 32 queue slots at a time.
+template <int B, int BM>
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
+    k2_general(Cfg c, EvalArgs A) {
+  __shared__ int64_t G[B], D[B];
+  const int lane = threadIdx.x & 31, n = c.n;
+  const int64_t T_end = c.scal[1];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    G[i] = c.F[i] - c.L;
+    D[i] = T_end - c.B[i] - c.L;
   }
-#pragma unroll
-  for (int i = 0; i < 12; ++i) {
-    unsigned v = st.v[i];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0 && A.stats) atomicAdd(&A.stats[i], (unsigned long long)v);
-  }
-  if (lane == 0) { bl_sm[warp] = bl; bg_sm[warp] = bg; }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t l = INT64_MAX;
-    uint64_t gg = UINT64_MAX;
-    for (int w = 0; w < kTThreads / 32; ++w) tbetter(bl_sm[w], bg_sm[w], l, gg);
-    A.partials[2 * blockIdx.x] = l;
-    A.partials[2 * blockIdx.x + 1] = (int64_t)gg;
+  TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * tstride<B, BM>()));
+  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * tstride<B, BM>() + 2 * BM);
+  for (int t = 0; t < B + 2; ++t) E[t] = 0u;
+  TPlan p;
+  p.e = -1;
+  TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
+  int64_t bl = INT64_MAX;
+  uint64_t bg = UINT64_MAX;
+  const uint64_t total = *reinterpret_cast<volatile unsigned*>(A.gqn);  // written by the fast kernel before
+  for (;;) {
+    unsigned long long ch = 0;
+    if (lane == 0) ch = atomicAdd(A.counter2, 32ull);
+    ch = __shfl_sync(0xffffffffu, ch, 0);
+    if (ch >= total) break;
+    const uint64_t i = ch + lane;
+    const uint64_t g = i < total ? A.gq[i] : ~0ull;
+    if (g != ~0ull) {
+      const uint64_t qo = A.gqo[i];
+      const int e = (int)(qo >> 56);
+      if (e != p.e) tplan(c, e, p);
+      tunrank<B>(c, n, p.m, g - p.first, s);
+      const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st);
+      if (A.lat_out) A.lat_out[qo & ((1ull << 56) - 1)] = lat;
+      tbetter(lat, g, bl, bg);
+      for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval leaves its masks and scratch dirty
+    }
   }
+  flush_stats(st, A.stats);
+  block_best(bl, bg, A.partials2, A.first_chunk);
 }
 
 // NEXT-1: one candidate's decisions (the schedule's moves), for emission.
@@ -1261,11 +1281,14 @@ __global__ void k_order_dump(Cfg c, const int64_t* xo, int64_t* out) {
 template <int B, int BM>
 static void k2t_attrs() {
   constexpr int smem = tsmem<B, BM>();
-  cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k2_eval_thread<false, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaFuncSetAttribute(k2_fast<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_fast<false, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_eval_thread<true, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k2_eval_thread<true, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  cudaFuncSetAttribute(k2_fast<true, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_fast<true, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(k2_general<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_general<B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(k2_explain<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
@@ -1280,7 +1303,14 @@ __host__ __device__ constexpr int tinstance(int n, int mmax) {
 template <int B, int BM>
 static int grid_b(int sms) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_eval_thread<false, B, BM>, kTThreads, tsmem<B, BM>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_fast<false, B, BM>, kTThreads, tsmem<B, BM>());
+  return max(1, per) * sms;
+}
+
+template <int B, int BM>
+static int ggrid_b(int sms) {
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_general<B, BM>, kTThreads, tsmem<B, BM>());
   return max(1, per) * sms;
 }
 
@@ -1296,7 +1326,7 @@ void eval_thread_attrs() {
   k2t_attrs<128, 16>();
 }
 
-// persistent grid of instance i
+// persistent grids of instance i: fast kernel, general kernel
 int eval_thread_grid(int sms, int i) {
   switch (i) {
     case 0: return grid_b<32, 32>(sms);
@@ -1305,6 +1335,17 @@ int eval_thread_grid(int sms, int i) {
     case 4: return grid_b<64, 16>(sms);
     case 5: return grid_b<128, 16>(sms);
     default: return grid_b<128, 128>(sms);
+  }
+}
+
+int eval_general_grid(int sms, int i) {
+  switch (i) {
+    case 0: return ggrid_b<32, 32>(sms);
+    case 1: return ggrid_b<64, 64>(sms);
+    case 2: return ggrid_b<128, 64>(sms);
+    case 4: return ggrid_b<64, 16>(sms);
+    case 5: return ggrid_b<128, 16>(sms);
+    default: return ggrid_b<128, 128>(sms);
   }
 }
 
@@ -1330,26 +1371,79 @@ cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_
   return cudaGetLastError();
 }
 
+// K2 mode 1: the range (or index list) a chunk at a time, so that the queue
+// (gqcap slots, less the batches every fast warp may leave half used) holds
+// every candidate a chunk can hand over; per chunk the fast kernel (the first
+// one overlapping K1 by programmatic dependent launch) then the general one.
+// Range chunks are whole multiples of block x world global indices from
+// begin, so the block-cyclic shard is the same as in one launch.
 template <int B, int BM>
-static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a, cudaStream_t st) {
+static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaStream_t st) {
   const size_t smem = (size_t)tsmem<B, BM>();
-  if (a.index) {
-    k2_eval_thread<true, B, BM><<<a.grid, kTThreads, smem, st>>>(c, a);
+  const uint64_t margin = (uint64_t)kGqBatch * a0.grid * (kTThreads / 32);
+  if (a0.gqcap <= margin) return cudaErrorInvalidValue;
+  const uint64_t room = a0.gqcap - margin;
+  EvalArgs a = a0;
+  a.first_chunk = 1;
+  cudaError_t e = cudaSuccess;
+  auto chunk = [&](bool pdl) -> cudaError_t {
+    cudaError_t r = cudaMemsetAsync(a.gqn, 0, sizeof(unsigned), st);
+    if (r == cudaSuccess) r = cudaMemsetAsync(a.counter2, 0, 8, st);
+    if (r != cudaSuccess) return r;
+    if (a.index) {
+      k2_fast<true, B, BM><<<a.grid, kTThreads, smem, st>>>(c, a);
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)a.grid);
+      cfg.blockDim = dim3(kTThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = pdl ? 1 : 0;  // may start while K1 (which triggers at its start) still runs
+      r = cudaLaunchKernelEx(&cfg, k2_fast<false, B, BM>, c, a);
+      if (r != cudaSuccess) return r;
+    }
+    k2_general<B, BM><<<a.grid2, kTThreads, smem, st>>>(c, a);
+    a.first_chunk = 0;
     return cudaGetLastError();
+  };
+  if (a0.index) {
+    uint64_t off = 0;
+    do {
+      a.index = a0.index + off;
+      a.count = min(room, a0.count - off);
+      a.lat_out = a0.lat_out ? a0.lat_out + off : nullptr;
+      if (off > 0 && (e = cudaMemsetAsync(a.counter, 0, 8, st)) != cudaSuccess) return e;
+      if ((e = chunk(false)) != cudaSuccess) return e;
+      off += a.count;
+    } while (off < a0.count);
+  } else {
+    const uint64_t per = (uint64_t)a0.block * a0.world;
+    const uint64_t C = max((uint64_t)1, room / a0.block) * per;
+    uint64_t b = a0.begin;
+    do {
+      a.begin = b;
+      a.end = min(a0.end, b + C);
+      a.lat_out = a0.lat_out ? a0.lat_out + (b - a0.begin) : nullptr;
+      if (b > a0.begin && (e = cudaMemsetAsync(a.pclaim, 0, (size_t)a.nplans * 8, st)) != cudaSuccess) return e;
+      if ((e = chunk(b == a0.begin)) != cudaSuccess) return e;
+      b = a.end;
+    } while (b < a0.end);
   }
-  // programmatic dependent launch: may start while K1 (which triggers at its
-  // start) still runs; plan readiness is K1's pdone counters
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)a.grid);
-  cfg.blockDim = dim3(kTThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k2_eval_thread<false, B, BM>, c, a);
+  return cudaSuccess;
+}
+
+// chunks launch_eval_thread_b splits a call into (two kernels each)
+int eval_thread_chunks(const EvalArgs& a) {
+  const uint64_t margin = (uint64_t)kGqBatch * a.grid * (kTThreads / 32);
+  if (a.gqcap <= margin) return 1;
+  const uint64_t room = a.gqcap - margin;
+  if (a.index) return (int)max((uint64_t)1, (a.count + room - 1) / room);
+  const uint64_t C = max((uint64_t)1, room / a.block) * (uint64_t)a.block * a.world;
+  return (int)max((uint64_t)1, (a.end - a.begin + C - 1) / C);
 }
 
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st) {

@@ -165,13 +165,26 @@ struct EvalArgs {
   cudaEvent_t ev0, ev1;       // optional: recorded around K2 for per-kernel timing
   unsigned long long* pclaim;  // [nplans] K2 per-plan chunk counters, reset by K3
   int nplans;
-  unsigned long long* stats;  // [6] cumulative: candidates, algorithmic ops, fwd iters, fwd attempts, bwd iters, bwd attempts
+  unsigned long long* stats;  // [12] cumulative loop counts (optimus_eval_stats)
+  // K2 mode 1, split: the fast kernel hands candidates the general kernel
+  // evaluates through a global queue, a chunk of the range at a time
+  unsigned long long* gq;     // [gqcap] g (~0: unused slot)
+  unsigned long long* gqo;    // [gqcap] lat_out position | plan << 56
+  unsigned int* gqn;          // slots reserved (warps take batches of kGqBatch)
+  uint64_t gqcap;
+  int64_t* partials2;         // [grid2][2] general kernel's block bests
+  unsigned long long* counter2;  // general kernel's work counter
+  int grid2;
+  int first_chunk;            // 1: blocks write their partials, 0: merge into them
 };
+constexpr int kGqBatch = 64;    // queue slots a fast-kernel warp reserves at a time
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
 cudaError_t launch_order_dump(const Cfg& c, const int64_t* d_explain, int64_t* d_out, cudaStream_t st);
 int eval_grid(int sms);
 int eval_thread_grid(int sms, int instance);
+int eval_general_grid(int sms, int instance);
+int eval_thread_chunks(const EvalArgs& a);
 int eval_thread_instance(int n, int mmax);
 }  // namespace optimus
