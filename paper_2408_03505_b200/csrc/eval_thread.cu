@@ -553,10 +553,10 @@ __device__ __forceinline__ int64_t tdep_mask(const TPlan& p, const int64_t* G, i
 // non-increasing in the slot, so for a rank r > max kf the largest term is at
 // the coarse entry of jmax (largest N, highest j) at level N_max - r + 1, and
 // ranks r <= max kf are dominated by a moved entry of that rank.  E[x] =
-// {j : c_j = x} on entry (clobbered by the moved-entry sort; the caller
-// zeroes it).
-__device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS& s, uint32_t* E, uint32_t all,
-                                     uint32_t MV, int maxN, int jmax, int sumc, int64_t Df, int64_t& dep_b) {
+// {j : c_j = x} (read only); mv (after E[max N]) receives the sorted moved
+// entries.
+__device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS& s, const uint32_t* E, uint32_t all,
+                                     uint32_t MV, int maxN, int jmax, int sumc, int64_t Df, const SB mv, int64_t& dep_b) {
   const int kmax = p.kmax;
   int maxc = maxN;
 #pragma unroll 1
@@ -584,32 +584,90 @@ __device__ __forceinline__ bool tsep(const TPlan& p, const int64_t* D, const TS&
     A &= ~E[u];
   }
   // moved entries sorted by (value, key): inserted in (j, k) order, so a
-  // stable insertion by value keeps key order among equal values
+  // stable insertion by value keeps key order among equal values (a single
+  // moved pipeline's are already in order); kept as (j, k) byte pairs in mv
+  // for the first backward trial (tbwd1)
   int nm = 0;
+  const bool one = (MV & (MV - 1)) == 0u;
 #pragma unroll 1
   for (uint32_t b = MV; b; b &= b - 1) {
     const int j = __ffs(b) - 1, a = row_of(p, j), kfj = (int)s.N[j] - (int)s.c[j];
 #pragma unroll 1
     for (int k = 0; k < kfj; ++k) {
-      const int64_t v = p.at(p.inbF, a * kmax + k);
       int q = nm++;
+      if (!one) {
+        const int64_t v = p.at(p.inbF, a * kmax + k);
 #pragma unroll 1
-      for (; q > 0 && p.at(p.inbF, row_of(p, s.mvj[q - 1]) * kmax + s.mvk[q - 1]) > v; --q) {
-        s.mvj[q] = s.mvj[q - 1];
-        s.mvk[q] = s.mvk[q - 1];
+        for (; q > 0 && p.at(p.inbF, row_of(p, mv[2 * q - 2]) * kmax + mv[2 * q - 1]) > v; --q) {
+          mv[2 * q] = mv[2 * q - 2];
+          mv[2 * q + 1] = mv[2 * q - 1];
+        }
       }
-      s.mvj[q] = (uint8_t)j;
-      s.mvk[q] = (uint8_t)k;
+      mv[2 * q] = (uint8_t)j;
+      mv[2 * q + 1] = (uint8_t)k;
     }
   }
 #pragma unroll 1
   for (int q = 0; q < nm; ++q) {
-    const int j = s.mvj[q];
-    OPT_CHECK(sumc + q < kMaxN && (int)s.N[j] - (int)s.c[j] - (int)s.mvk[q] >= 1);
-    best = max(best, p.at(p.preBEF, (int)s.N[j] - (int)s.c[j] - (int)s.mvk[q]) - D[sumc + q]);
+    const int j = mv[2 * q];
+    OPT_CHECK(sumc + q < kMaxN);
+    best = max(best, p.at(p.preBEF, (int)s.N[j] - (int)s.c[j] - (int)mv[2 * q + 1]) - D[sumc + q]);
   }
   dep_b = best;
   return true;
+}
+
+// First backward trial (R13 in mirrored time, R15) on tsep's ordering: no
+// backward move yet (Qcb = 0, cb = N), js gives one coarse backward
+// microbatch whose chain ends at EFb.  Only js's entries change (need = rank -
+// [EFb <= D]; INF if js's first entry, rank N_js, loses its cover).  The
+// others' maximum: every moved entry of theirs, and their coarse entries of
+// the ranks r > kf_o = their largest kf, whose largest slot is at jx (largest
+// N among them, highest j) on level N_jx - r + 1 (smaller ranks are
+// dominated by a moved entry of that rank, whose slot is later).
+__device__ __forceinline__ int64_t tbwd1(const TPlan& p, const int64_t* D, const TS& s, const uint32_t* E,
+                                         uint32_t all, const SB mv, int nm, int sumc, int m, int jmax, int js,
+                                         int64_t EFb) {
+  const int Njs = s.N[js], cjs = s.c[js];
+  int64_t best = kNegInf;
+  int kfo = 0;
+#pragma unroll 1
+  for (int q = 0; q < nm; ++q) {
+    const int j = mv[2 * q], k = mv[2 * q + 1], kfj = (int)s.N[j] - (int)s.c[j];
+    const int64_t d = D[sumc + q];
+    if (j != js) {
+      best = max(best, p.at(p.preBEF, kfj - k) - d);
+      kfo = max(kfo, kfj);
+    } else {
+      if (k == 0 && cjs == 0 && EFb > d) return kInf;  // js's first entry is this moved one
+      const int need = kfj - k - (EFb <= d ? 1 : 0);
+      if (need > 0) best = max(best, p.at(p.preBEF, need) - d);
+    }
+  }
+  int jx = jmax, Nx = s.N[jmax];
+  if (jmax == js) {  // the others' largest N, highest j
+    jx = -1;
+    Nx = 0;
+#pragma unroll 1
+    for (int j = 0; j < m; ++j)
+      if (j != js && (int)s.N[j] >= Nx) { Nx = s.N[j]; jx = j; }
+  }
+  const int ux = jx >= 0 ? Nx - kfo : 0;  // others' coarse levels that count
+  const uint32_t below_s = (1u << js) - 1u, below_x = jx >= 0 ? (1u << jx) - 1u : 0u;
+  uint32_t A = all & ~E[0];
+#pragma unroll 1
+  for (int t = 1, pos = 0, tl = max(ux, cjs); t <= tl; ++t) {
+    if (t <= cjs) {
+      const int64_t d = D[pos + __popc(A & below_s)];
+      if (t == 1 && EFb > d) return kInf;  // js's first entry (coarse, level 1)
+      const int need = Njs - t + 1 - (EFb <= d ? 1 : 0);
+      if (need > 0) best = max(best, p.at(p.preBEF, need) - d);
+    }
+    if (t <= ux) best = max(best, p.at(p.preBEF, Nx - t + 1) - D[pos + __popc(A & below_x)]);
+    pos += __popc(A);
+    A &= ~E[t];
+  }
+  return best;
 }
 
 // One candidate, sequentially in this thread (the general path).
@@ -728,7 +786,8 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   bool have_order = true;
   int64_t dep_b = kNegInf;
   bool done_b = false;
-  if (kMask && p.strict && tsep(p, D, s, E, all, MV, maxN, jmax, sumc, Df, dep_b)) {
+  const SB mv{(uint32_t)((reinterpret_cast<unsigned char*>(E) - k2sm) + 4 * (maxN + 1))};  // after E[maxN]
+  if (kMask && p.strict && tsep(p, D, s, E, all, MV, maxN, jmax, sumc, Df, mv, dep_b)) {
     have_order = false;  // owners and ranks materialised if a backward move is tried
     done_b = true;
   }
@@ -754,8 +813,15 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (kbj >= (int)p.at(p.lenB, rowoff)) break;
     const int64_t EFb = p.at(p.inbB, rowoff * kmax + kbj);
     ++atb;
-    if (!have_order) {  // materialise owners and ranks (same order, same initial shift)
-      order_strict(p, D, m, Df, s);
+    int64_t dep2 = kNegInf;
+    bool have2 = false;
+    if (!have_order) {
+      if (kMask && !init_b) {  // first trial on tsep's ordering, nothing materialised
+        dep2 = tbwd1(p, D, s, E, all, mv, M, sumc, m, jmax, js, EFb);
+        if (dep2 > Delta) break;
+        have2 = true;  // the move commits: owners and ranks for the rest of the phase
+      }
+      order_strict(p, D, m, Df, s);  // materialise owners and ranks (same order, same initial shift)
       have_order = true;
     }
     if (!init_b) {  // backward moves are rare: per-pipeline state on first use
@@ -765,7 +831,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
       for (int i = 0; i < n; ++i) s.Qcb[i] = 0;
       init_b = true;
     }
-    const int64_t dep2 = tdep_bwd(p, D, n, js, EFb, s);
+    if (!have2) dep2 = tdep_bwd(p, D, n, js, EFb, s);
     if (dep2 > Delta) break;
     #pragma unroll 1
     for (int i = 0; i < n; ++i) s.Qcb[i] += (s.own[i] == js && EFb <= D[i]) ? 1 : 0;
