@@ -510,7 +510,7 @@ def main():
                 tsrc = tj.get("source")
         except Exception:
             pass
-    roofline = {"bound": "alu", "kernel": "k2_eval", "achieved": achieved, "peak": peak_gops,
+    roofline = {"bound": "alu", "kernel": "K2 (k2_fast + k2_general, mode 1)", "achieved": achieved, "peak": peak_gops,
                 "unit": "Gop/s (32-bit integer lane-ops)", "frac": achieved / peak_gops, "traffic": traffic,
                 "traffic_source": tsrc, "issue_slot_pct_ncu": issue,
                 "peak_basis": f"{sms} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
