@@ -57,6 +57,7 @@ struct Prep {
   std::vector<int32_t> lkind, loff, blayers;
   std::vector<int64_t> lns;
   std::vector<uint64_t> binom;
+  std::vector<uint32_t> binom32;  // the same, saturated to 32 bits (K2 unranks plans of < 2^32 candidates in 32 bits)
   std::vector<HostPlan> plans;
   uint64_t total = 0;
   int64_t n_tables = 0, n_slots = 0, fwd_units = 0, bwd_units = 0, n_flags = 0;
@@ -65,7 +66,7 @@ struct Prep {
   int nk_max = 0;
   int k0_trials = 0;
   // layout (byte offsets in the workspace)
-  size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_plans, inputs_bytes;
+  size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_binom32, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
       o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_gq, o_gqo, o_gqn, o_partials2, o_explain, o_order, o_rec, o_base, total_bytes;
   int base_L = 0, base_Le = 0;
@@ -197,6 +198,8 @@ int prepare(const optimus_problem* pb, Prep& X) {
     X.binom.assign((size_t)S * S, 0);
     for (int a = 0; a < S; ++a)
       for (int b = 0; b < S; ++b) X.binom[a * S + b] = binom_sat(a, b);
+    X.binom32.resize(X.binom.size());
+    for (size_t i = 0; i < X.binom.size(); ++i) X.binom32[i] = (uint32_t)std::min<uint64_t>(X.binom[i], UINT32_MAX);
   }
 
   // model planner: encoder plans (P | PP_llm, T | TP_llm), memory prune (R17, R19)
@@ -287,6 +290,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_loff = take(X.loff.size() * 4);
   X.o_blayers = take(X.blayers.size() * 4);
   X.o_binom = take(X.binom.size() * 8);
+  X.o_binom32 = take(X.binom32.size() * 4);
   X.o_plans = take(X.plans.size() * sizeof(PlanDesc));
   X.o_units = take(std::max<size_t>(X.units.size(), 1) * 4);
   X.o_k2order = take(std::max<size_t>(X.k2order.size(), 1) * 4);
@@ -406,6 +410,7 @@ Cfg make_cfg(const Prep& X, const optimus_problem* pb, char* ws) {
   c.loff = (const int32_t*)(ws + X.o_loff);
   c.blayers = (const int32_t*)(ws + X.o_blayers);
   c.binom = (const uint64_t*)(ws + X.o_binom);
+  c.binom32 = (const uint32_t*)(ws + X.o_binom32);
   c.plans = (const PlanDesc*)(ws + X.o_plans);
   c.W = (int32_t*)(ws + X.o_W);
   c.Wdef = (int32_t*)(ws + X.o_Wdef);
@@ -504,6 +509,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   memcpy(h.data() + X.o_loff, X.loff.data(), X.loff.size() * 4);
   memcpy(h.data() + X.o_blayers, X.blayers.data(), X.blayers.size() * 4);
   memcpy(h.data() + X.o_binom, X.binom.data(), X.binom.size() * 8);
+  memcpy(h.data() + X.o_binom32, X.binom32.data(), X.binom32.size() * 4);
   for (size_t i = 0; i < X.plans.size(); ++i) memcpy(h.data() + X.o_plans + i * sizeof(PlanDesc), &X.plans[i].d, sizeof(PlanDesc));
   memcpy(h.data() + X.o_units, X.units.data(), X.units.size() * 4);
   memcpy(h.data() + X.o_k2order, X.k2order.data(), X.k2order.size() * 4);

@@ -46,6 +46,9 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #ifndef K2T_GMINB
 #define K2T_GMINB 5  // general kernel
 #endif
+#ifndef K2T_MINB_WIDE
+#define K2T_MINB_WIDE 5  // fast kernel of the n > 32 instances (small per-thread state: registers decide)
+#endif
 // per-thread scratch for n <= B slots and m <= BM pipelines, an odd number of
 // words: (32, 32) 260 bytes; (64, 64) 516; (128, 64) 780; (128, 128) 1028;
 // (64, 16) 364; (128, 16) 684 (at least N, c, the fast path's masks E[B + 2] and thresholds[B]; the
@@ -57,6 +60,27 @@ __host__ __device__ constexpr int tstride() {
 // dynamic shared memory of a K2 mode 1 block: the per-thread scratch
 template <int B, int BM>
 __host__ __device__ constexpr int tsmem() { return kTThreads * tstride<B, BM>(); }
+// the fast kernel's: the composition and the level masks only (16-bit masks
+// when m <= 16), an odd number of words
+template <int BM>
+struct FMask {
+  using T = uint32_t;
+};
+template <>
+struct FMask<16> {
+  using T = uint16_t;
+};
+template <int B, int BM>
+__host__ __device__ constexpr int fstride() {
+  return ((BM + (B + 2) * (int)sizeof(typename FMask<BM>::T) + 3) / 4 * 4) | 4;
+}
+template <int B, int BM>
+__host__ __device__ constexpr int fsmem() { return kTThreads * fstride<B, BM>(); }
+// the general kernel's: teval's byte arrays; the level masks only at B = 32
+template <int B, int BM>
+__host__ __device__ constexpr int gstride() { return B == 32 ? tstride<B, BM>() : (4 * BM + 4 * B + 4) | 4; }
+template <int B, int BM>
+__host__ __device__ constexpr int gsmem() { return kTThreads * gstride<B, BM>(); }
 
 // Per-thread scratch (bytes 0..8B-1, B = 32 shown).  The three phases of one
 // candidate use disjoint live sets, so bytes 2B..8B-1 are shared between them:
@@ -187,23 +211,53 @@ __device__ int tfind_plan(const Cfg& c, uint64_t g) {
 }
 
 // Lexicographic unranking (R17) into N[0..m); binomial rows of stride B + 1.
-template <int B>
-__device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
+// Part j's value x is the smallest x whose cumulative count
+// S(x) = sum_{y<=x} C(rem - y - 1, parts - 2) = C(rem - 1, parts - 1) - C(rem - x - 1, parts - 1)
+// exceeds the rank (hockey stick): a linear scan over x when the range of x
+// is short, a binary search on C(rem - x - 1, parts - 1) when it is long
+// (large n, few pipelines: the scan's length differs from lane to lane).
+template <typename T>
+__device__ __forceinline__ void tunrank_t(const T* bt, int S, int n, int m, T r, TS& s) {
   int rem = n;
+  const bool bin = n - m + 1 > 16;
   #pragma unroll 1
   for (int j = 0; j < m - 1; ++j) {
     const int parts = m - j;
     int x = 1;
-    #pragma unroll 1
-    for (; x <= rem - (parts - 1); ++x) {
-      const uint64_t cnt = __ldg(&c.binom[(rem - x - 1) * (B + 1) + (parts - 2)]);
-      if (rank < cnt) break;
-      rank -= cnt;
+    if (!bin) {
+      const T* row = bt + (parts - 2);
+      #pragma unroll 1
+      for (; x <= rem - (parts - 1); ++x) {
+        const T cnt = __ldg(&row[(rem - x - 1) * S]);
+        if (r < cnt) break;
+        r -= cnt;
+      }
+    } else {
+      const T* col = bt + (parts - 1);
+      const T tot = __ldg(&col[(rem - 1) * S]);  // C(rem - 1, parts - 1)
+      const T thr = tot - r;                     // find the smallest x with C(rem - x - 1, parts - 1) < thr
+      int lo = 1, hi = rem - parts + 1;
+      #pragma unroll 1
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&col[(rem - mid - 1) * S]) < thr) hi = mid; else lo = mid + 1;
+      }
+      x = lo;
+      r -= tot - __ldg(&col[(rem - x) * S]);  // S(x - 1)
     }
     s.N[j] = (uint8_t)x;
     rem -= x;
   }
   s.N[m - 1] = (uint8_t)rem;
+}
+
+template <int B>
+__device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
+  // plans of < 2^32 compositions: every count met is below 2^32 too
+  if (m > 1 && __ldg(&c.binom[(n - 1) * (B + 1) + (m - 1)]) <= 0xffffffffull)
+    tunrank_t<uint32_t>(c.binom32, B + 1, n, m, (uint32_t)rank, s);
+  else
+    tunrank_t<uint64_t>(c.binom, B + 1, n, m, rank, s);
 }
 
 // Lexicographic successor of N (m parts); false past the last composition.
@@ -512,6 +566,21 @@ __device__ __forceinline__ int64_t critical(const TPlan& p, TV dev, int half, co
   return crit_value(p, dev, cnt8, best, js);
 }
 
+// the two largest forward keys over the pipelines' current counts
+__device__ __forceinline__ void critical2(const TPlan& p, const SB cnt8, int m, uint32_t& k0, uint32_t& k1) {
+  const uint32_t* key = reinterpret_cast<const uint32_t*>(p.ptr(p.kj));
+  const int np1 = p.np1;
+  uint32_t a = 0, b = 0;
+#pragma unroll 2
+  for (int j = 0; j < m; ++j) {
+    const uint32_t k = __ldg(&key[2 * (j * np1 + cnt8[j])]);
+    b = max(b, min(a, k));
+    a = max(a, k);
+  }
+  k0 = a;
+  k1 = b;
+}
+
 // One candidate, sequentially in this thread.
 // EXPLAIN (NEXT-1, one candidate): xo[8 + t] = pipeline of the t-th committed
 // forward move, xo[8 + n + t] = of the t-th backward move; xo[1..4] = Df, Db,
@@ -692,7 +761,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     for (int t = 0; t < (n + 5) / 4; ++t) s.cnt.w(t) = 0u;  // cnt[0..n+1] (4-aligned)
   }
   // the first findCritical of both phases runs on N: one pass for both keys
-  uint32_t kf0 = 0, kb0 = 0;
+  uint32_t kf0 = 0, kf1 = 0, kb0 = 0;
   int maxN = 0;
 #pragma unroll 1
   for (int j = 0, off = 0; j < m; ++j, off += p.np1) {
@@ -702,6 +771,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     else s.cnt[Nj] += 1;
     maxN = max(maxN, Nj);
     const uint64_t k = __ldg(reinterpret_cast<const uint64_t*>(p.ptr(p.kj)) + off + Nj);
+    kf1 = max(kf1, min(kf0, (uint32_t)k));  // the two largest forward keys (keys are distinct: j in the low bits)
     kf0 = max(kf0, (uint32_t)k);
     kb0 = max(kb0, (uint32_t)(k >> 32));
   }
@@ -734,8 +804,11 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   for (;;) {
     ++itf;
     int js;
-    const int64_t dev = itf == 1 ? crit_value(p, p.devF, s.c, kf0, js)  // findCritical (R11)
-                                 : critical(p, p.devF, 0, s.c, m, js);
+    // findCritical (R11): the picks are a merge of the pipelines' key lists,
+    // each non-increasing in the count, so while the last pick's next key
+    // still beats the runner-up (kf1, untouched by the pick) it is the max
+    if (itf > 1 && kf0 <= kf1) critical2(p, s.c, m, kf0, kf1);
+    const int64_t dev = crit_value(p, p.devF, s.c, kf0, js);
     Delta = max((int64_t)0, max(dev, dep));
     if (Delta == 0 || sumc == 0) break;
     const int as = row_of(p, js), cjs = s.c[js], kfj = s.N[js] - cjs;
@@ -780,6 +853,8 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
     if (EXPLAIN) xo[8 + M - 1] = js;
     dep = dep2;
     --sumc;
+    // the pick's next key (count c_js - 1); below the runner-up: rescan next time
+    kf0 = s.c[js] > 0 ? __ldg(reinterpret_cast<const uint32_t*>(p.ptr(p.kj)) + 2 * (js * p.np1 + s.c[js])) : 0u;
   }
   const int64_t Df = Delta;
   // ---------------- global ordering (R14) -------------------------------
@@ -887,10 +962,10 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
 //   * backward trial of jb (no backward move yet, Qcb = 0): only jb's entries
 //     change (need = r - [EFb <= D]); the others' maximum is the shift above,
 //     or, when jb = jmax, the same walk over j2 (largest N among j != jmax).
-// Leaves E zeroed.
-template <int B>
+// Leaves E zeroed.  MT: the mask word (16 bits for instances of m <= 16).
+template <int B, typename MT>
 __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const int64_t* D, int n, const TS& s,
-                                      uint32_t* E, int64_t& Df, int64_t& Db, TStats& st) {
+                                      MT* E, int64_t& Df, int64_t& Db, TStats& st) {
   const int m = p.m, np1 = p.np1;
   uint32_t kf0 = 0, kb0 = 0;
   int Nmax = 0;
@@ -899,13 +974,13 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
   for (int j = 0, off = 0; j < m; ++j, off += np1) {
     const int Nj = s.N[j];
     OPT_CHECK(Nj >= 1 && Nj <= n && Nj <= B);
-    E[Nj] |= 1u << j;
+    E[Nj] |= (MT)(1u << j);
     const uint64_t k = __ldg(kj + off + Nj);  // first findCritical of both phases (R11)
     kf0 = max(kf0, (uint32_t)k);
     kb0 = max(kb0, (uint32_t)(k >> 32));
     Nmax = max(Nmax, Nj);
   }
-  const int jmax = 31 - __clz(E[Nmax]);  // highest j with N_j = N_max
+  const int jmax = 31 - __clz((uint32_t)E[Nmax]);  // highest j with N_j = N_max
   const uint32_t all = m == 32 ? 0xffffffffu : (1u << m) - 1u;
   const uint32_t below_max = (1u << jmax) - 1u;
   int64_t dep = kNegInf, depb = kNegInf;
@@ -914,7 +989,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
 #pragma unroll 1
     for (int t = 1, pos = 0; t <= Nmax; ++t) {
       const uint32_t e = E[t];
-      E[t] = A;
+      E[t] = (MT)A;
       OPT_CHECK(t <= n && pos < n && pos + __popc(A & below_max) < n);
       dep = max(dep, p.at(p.preEF, t) - G[pos]);
       depb = max(depb, p.at(p.preBEF, Nmax - t + 1) - D[pos + __popc(A & below_max)]);
@@ -970,7 +1045,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
           if (other2) {
 #pragma unroll 1
             for (N2 = Nmax; N2 > 0 && __popc(E[N2]) < 2; --N2) {}
-            if (N2 > 0) j2 = 31 - __clz(E[N2] & ~(1u << jmax));
+            if (N2 > 0) j2 = 31 - __clz((uint32_t)E[N2] & ~(1u << jmax));
           }
           const int tl = max(Njb, N2);
           const uint32_t below_b = (1u << jb) - 1u, below_2 = (1u << j2) - 1u;
@@ -994,7 +1069,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
     Db = Delta_b;
   }
 #pragma unroll 1
-  for (int t = 1; t <= Nmax; ++t) E[t] = 0u;
+  for (int t = 1; t <= Nmax; ++t) E[t] = 0;
   if (!general) {
     st.v[0] += 1;
     st.v[1] += m;
@@ -1070,7 +1145,7 @@ __device__ __forceinline__ void flush_stats(const TStats& st, unsigned long long
 // increasing) go to the global queue for k2_general, one warp-reserved batch
 // of kGqBatch slots at a time (unused slots marked ~0).
 template <bool EXPLICIT, int B, int BM>
-__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
+__global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
     k2_fast(Cfg c, EvalArgs A) {
   __shared__ int64_t G[B], D[B];
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
@@ -1098,9 +1173,11 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     for (int k = c.n_k2order - 1; k >= 0; --k) psuf[k] = acc += pn[c.k2order[k]];
   }
   __syncthreads();
-  TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * tstride<B, BM>()));
-  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * tstride<B, BM>() + 2 * BM);  // tfast's masks (zero)
-  for (int t = 0; t < B + 2; ++t) E[t] = 0u;
+  TS s;  // the fast path only keeps the composition and its masks per thread
+  s.N = SB{(uint32_t)(threadIdx.x * fstride<B, BM>())};
+  using MT = typename FMask<BM>::T;
+  MT* E = reinterpret_cast<MT*>(k2sm + threadIdx.x * fstride<B, BM>() + BM);  // tfast's masks (zero)
+  for (int t = 0; t < B + 2; ++t) E[t] = 0;
   TPlan p;
   p.e = -1;
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
@@ -1113,7 +1190,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : BM == 16 ? (B 
     bool pend = false;
     if (valid) {
       int64_t Df, Db;
-      if (p.fast && tfast<B>(p, G, D, n, s, E, Df, Db, st)) {
+      if (p.fast && tfast<B, MT>(p, G, D, n, s, E, Df, Db, st)) {
         const int64_t lat = T_end + Df + Db;  // R16
         if (A.lat_out) A.lat_out[out] = lat;
         tbetter(lat, g, bl, bg);
@@ -1248,9 +1325,10 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
     D[i] = T_end - c.B[i] - c.L;
   }
   __syncthreads();
-  TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * tstride<B, BM>()));
-  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * tstride<B, BM>() + 2 * BM);
-  for (int t = 0; t < B + 2; ++t) E[t] = 0u;
+  TS s = ts_at<B, BM>((uint32_t)(threadIdx.x * gstride<B, BM>()));
+  uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + threadIdx.x * gstride<B, BM>() + 2 * BM);  // (B = 32 only)
+  if (B == 32)
+    for (int t = 0; t < B + 2; ++t) E[t] = 0u;
   TPlan p;
   p.e = -1;
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
@@ -1272,7 +1350,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
       const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st);
       if (A.lat_out) A.lat_out[qo & ((1ull << 56) - 1)] = lat;
       tbetter(lat, g, bl, bg);
-      for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval leaves its masks and scratch dirty
+      if (B == 32)
+        for (int t = 0; t < B + 2; ++t) E[t] = 0u;  // teval leaves its masks and scratch dirty
     }
   }
   flush_stats(st, A.stats);
@@ -1346,14 +1425,14 @@ __global__ void k_order_dump(Cfg c, const int64_t* xo, int64_t* out) {
 
 template <int B, int BM>
 static void k2t_attrs() {
-  constexpr int smem = tsmem<B, BM>();
-  cudaFuncSetAttribute(k2_fast<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  constexpr int smem = tsmem<B, BM>(), fsm = fsmem<B, BM>();
+  cudaFuncSetAttribute(k2_fast<false, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   cudaFuncSetAttribute(k2_fast<false, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_fast<true, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_fast<true, B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, fsm);
   cudaFuncSetAttribute(k2_fast<true, B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-  cudaFuncSetAttribute(k2_general<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k2_general<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, gsmem<B, BM>());
   cudaFuncSetAttribute(k2_general<B, BM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
   cudaFuncSetAttribute(k2_explain<B, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1369,14 +1448,14 @@ __host__ __device__ constexpr int tinstance(int n, int mmax) {
 template <int B, int BM>
 static int grid_b(int sms) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_fast<false, B, BM>, kTThreads, tsmem<B, BM>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_fast<false, B, BM>, kTThreads, fsmem<B, BM>());
   return max(1, per) * sms;
 }
 
 template <int B, int BM>
 static int ggrid_b(int sms) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_general<B, BM>, kTThreads, tsmem<B, BM>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k2_general<B, BM>, kTThreads, gsmem<B, BM>());
   return max(1, per) * sms;
 }
 
@@ -1445,7 +1524,6 @@ cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_
 // begin, so the block-cyclic shard is the same as in one launch.
 template <int B, int BM>
 static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaStream_t st) {
-  const size_t smem = (size_t)tsmem<B, BM>();
   const uint64_t margin = (uint64_t)kGqBatch * a0.grid * (kTThreads / 32);
   if (a0.gqcap <= margin) return cudaErrorInvalidValue;
   const uint64_t room = a0.gqcap - margin;
@@ -1457,12 +1535,12 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
     if (r == cudaSuccess) r = cudaMemsetAsync(a.counter2, 0, 8, st);
     if (r != cudaSuccess) return r;
     if (a.index) {
-      k2_fast<true, B, BM><<<a.grid, kTThreads, smem, st>>>(c, a);
+      k2_fast<true, B, BM><<<a.grid, kTThreads, fsmem<B, BM>(), st>>>(c, a);
     } else {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)a.grid);
       cfg.blockDim = dim3(kTThreads);
-      cfg.dynamicSmemBytes = smem;
+      cfg.dynamicSmemBytes = fsmem<B, BM>();
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1472,7 +1550,7 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
       r = cudaLaunchKernelEx(&cfg, k2_fast<false, B, BM>, c, a);
       if (r != cudaSuccess) return r;
     }
-    k2_general<B, BM><<<a.grid2, kTThreads, smem, st>>>(c, a);
+    k2_general<B, BM><<<a.grid2, kTThreads, gsmem<B, BM>(), st>>>(c, a);
     a.first_chunk = 0;
     return cudaGetLastError();
   };

@@ -107,6 +107,7 @@ struct Cfg {
   unsigned long long* pclaim;  // [E] K2 chunks of each plan claimed; zeroed by K3
   const int32_t* k2order; // plans with candidates, in the order K2 takes them (short chains first)
   int32_t n_k2order;
+  const uint32_t* binom32;  // the same table saturated to 32 bits
   const uint64_t* binom;  // [S*S], S = B + 1 of the K2 mode 1 instance (33 / 65 / 129): C(a, b) at [a*S+b]; mode 0 reads it at S = 33
 };
 

@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int w
 // warps at once; the smallest successful w wins) and record the final
 // schedule.  Writes W, T_end and the ok flag.
 __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
-  __shared__ int Wcur[kMaxP], firstb[kMaxP + 1];
+  __shared__ int Wcur[kMaxP];
   __shared__ int s0_sm, wbest;
   const int p = c.p, v = c.v, n = c.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t span_def = c.k0res[0];
@@ -286,11 +286,6 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_final(Cfg c, int wpb) {
   }
   int64_t df, db;
   dur_fb(c, df, db);
-  if (threadIdx.x == 0) {
-    int base = 1;
-    for (int s = 0; s < p; ++s) { firstb[s] = base; base += default_w(p, v, n, s) + 1; }
-  }
-  __syncthreads();
   __shared__ int bestw_sm[kMaxP];
   if (threadIdx.x < p) bestw_sm[threadIdx.x] = INT32_MAX;
   __syncthreads();
