@@ -327,7 +327,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.gqcap = std::min<uint64_t>(X.total, (uint64_t)1 << K2_QUEUE_LOG2) + (uint64_t)kGqBatch * 4096 * 4;
   X.o_gq = take((size_t)X.gqcap * 8);
   X.o_gqo = take((size_t)X.gqcap * 8);
-  X.o_gqn = take(64);  // [0] u32 reserved slots, [8] u64 general kernel's work counter
+  X.o_gqn = take(64);  // [0] u32 reserved slots, [8] u64 general kernel's work counter, [16] u32 blocks done
   X.o_partials2 = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
   X.o_stats = take(16 * 8);
@@ -519,6 +519,7 @@ int optimus_load_costs(const optimus_problem* pb, void* d_workspace, size_t byte
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_scal, 0, 4 * 8, st);  // scal[3] = 0: K0 wave protocol
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_sync, 0, 64 + (size_t)kMaxE * 12, st);  // K1/K2 counters
   if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_iv, 0, (size_t)X.p * 8 * 12, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->ws + X.o_gqn, 0, 64, st);  // K2 queue counters (then kept by k2_general)
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is pageable and goes out of scope
   if (e != cudaSuccess) { delete c; return fail(OPTIMUS_ECUDA, "copying inputs: %s", cudaGetErrorString(e)); }
   rc = build(c, st);
@@ -574,6 +575,7 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.gqo = (unsigned long long*)(c->ws + c->X.o_gqo);
   a.gqn = (unsigned int*)(c->ws + c->X.o_gqn);
   a.counter2 = (unsigned long long*)(c->ws + c->X.o_gqn + 8);
+  a.gdone = (unsigned int*)(c->ws + c->X.o_gqn + 16);
   a.gqcap = c->X.gqcap;
   a.partials2 = (int64_t*)(c->ws + c->X.o_partials2);
   a.grid2 = c->mode == 1 ? c->grid_general : 0;

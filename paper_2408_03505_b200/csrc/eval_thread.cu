@@ -1147,6 +1147,7 @@ __device__ __forceinline__ void flush_stats(const TStats& st, unsigned long long
 template <bool EXPLICIT, int B, int BM>
 __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
     k2_fast(Cfg c, EvalArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k2_general may become resident as blocks leave
   __shared__ int64_t G[B], D[B];
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
   __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
@@ -1334,7 +1335,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   int64_t bl = INT64_MAX;
   uint64_t bg = UINT64_MAX;
-  const uint64_t total = *reinterpret_cast<volatile unsigned*>(A.gqn);  // written by the fast kernel before
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel (programmatic dependency) has finished
+  const uint64_t total = *reinterpret_cast<volatile unsigned*>(A.gqn);
   for (;;) {
     unsigned long long ch = 0;
     if (lane == 0) ch = atomicAdd(A.counter2, 32ull);
@@ -1356,6 +1358,22 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
   }
   flush_stats(st, A.stats);
   block_best(bl, bg, A.partials2, A.first_chunk);
+  // the last block out resets the queue and claim counters for the next
+  // chunk or call (every block read the queue length before leaving), so
+  // that no memset separates K1 from the next fast kernel (its programmatic
+  // dependent launch)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(A.gdone, 1u) == gridDim.x - 1) {
+      *A.gqn = 0u;
+      *A.counter2 = 0ull;
+      *A.counter = 0ull;
+      for (int e = 0; e < A.nplans; ++e) A.pclaim[e] = 0ull;
+      __threadfence();
+      *A.gdone = 0u;
+    }
+  }
 }
 
 // NEXT-1: one candidate's decisions (the schedule's moves), for emission.
@@ -1531,9 +1549,7 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
   a.first_chunk = 1;
   cudaError_t e = cudaSuccess;
   auto chunk = [&](bool pdl) -> cudaError_t {
-    cudaError_t r = cudaMemsetAsync(a.gqn, 0, sizeof(unsigned), st);
-    if (r == cudaSuccess) r = cudaMemsetAsync(a.counter2, 0, 8, st);
-    if (r != cudaSuccess) return r;
+    cudaError_t r = cudaSuccess;  // (queue and claim counters are zero: load, then k2_general's last block)
     if (a.index) {
       k2_fast<true, B, BM><<<a.grid, kTThreads, fsmem<B, BM>(), st>>>(c, a);
     } else {
@@ -1550,7 +1566,20 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
       r = cudaLaunchKernelEx(&cfg, k2_fast<false, B, BM>, c, a);
       if (r != cudaSuccess) return r;
     }
-    k2_general<B, BM><<<a.grid2, kTThreads, gsmem<B, BM>(), st>>>(c, a);
+    {  // programmatic dependent launch: its prologue overlaps the fast kernel's tail
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)a.grid2);
+      cfg.blockDim = dim3(kTThreads);
+      cfg.dynamicSmemBytes = gsmem<B, BM>();
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      r = cudaLaunchKernelEx(&cfg, k2_general<B, BM>, c, a);
+      if (r != cudaSuccess) return r;
+    }
     a.first_chunk = 0;
     return cudaGetLastError();
   };
@@ -1560,7 +1589,6 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
       a.index = a0.index + off;
       a.count = min(room, a0.count - off);
       a.lat_out = a0.lat_out ? a0.lat_out + off : nullptr;
-      if (off > 0 && (e = cudaMemsetAsync(a.counter, 0, 8, st)) != cudaSuccess) return e;
       if ((e = chunk(false)) != cudaSuccess) return e;
       off += a.count;
     } while (off < a0.count);
@@ -1572,7 +1600,6 @@ static cudaError_t launch_eval_thread_b(const Cfg& c, const EvalArgs& a0, cudaSt
       a.begin = b;
       a.end = min(a0.end, b + C);
       a.lat_out = a0.lat_out ? a0.lat_out + (b - a0.begin) : nullptr;
-      if (b > a0.begin && (e = cudaMemsetAsync(a.pclaim, 0, (size_t)a.nplans * 8, st)) != cudaSuccess) return e;
       if ((e = chunk(b == a0.begin)) != cudaSuccess) return e;
       b = a.end;
     } while (b < a0.end);

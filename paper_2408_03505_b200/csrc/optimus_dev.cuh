@@ -175,6 +175,7 @@ struct EvalArgs {
   uint64_t gqcap;
   int64_t* partials2;         // [grid2][2] general kernel's block bests
   unsigned long long* counter2;  // general kernel's work counter
+  unsigned int* gdone;        // general kernel blocks finished (its last block resets the counters)
   int grid2;
   int first_chunk;            // 1: blocks write their partials, 0: merge into them
 };
