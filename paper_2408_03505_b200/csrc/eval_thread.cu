@@ -46,6 +46,9 @@ constexpr int kTGss = K2T_GSS, kTGssDen = K2T_GSS_DEN;  // guided claim = remain
 #ifndef K2T_GMINB
 #define K2T_GMINB 5  // general kernel
 #endif
+#ifndef K2T_BIN_UNRANK
+#define K2T_BIN_UNRANK 40  // unranking binary-searches a part when n - m + 1 exceeds this (16 measured 4% slower on config 3)
+#endif
 #ifndef K2T_MINB_WIDE
 #define K2T_MINB_WIDE 5  // fast kernel of the n > 32 instances (small per-thread state: registers decide)
 #endif
@@ -219,7 +222,7 @@ __device__ int tfind_plan(const Cfg& c, uint64_t g) {
 template <typename T>
 __device__ __forceinline__ void tunrank_t(const T* bt, int S, int n, int m, T r, TS& s) {
   int rem = n;
-  const bool bin = n - m + 1 > 16;
+  const bool bin = n - m + 1 > K2T_BIN_UNRANK;
   #pragma unroll 1
   for (int j = 0; j < m - 1; ++j) {
     const int parts = m - j;
