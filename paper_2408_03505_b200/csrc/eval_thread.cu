@@ -219,6 +219,7 @@ __device__ int tfind_plan(const Cfg& c, uint64_t g) {
 // exceeds the rank (hockey stick): a linear scan over x when the range of x
 // is short, a binary search on C(rem - x - 1, parts - 1) when it is long
 // (large n, few pipelines: the scan's length differs from lane to lane).
+// (plain loads: bt may be a shared-memory table)
 template <typename T>
 __device__ __forceinline__ void tunrank_t(const T* bt, int S, int n, int m, T r, TS& s) {
   int rem = n;
@@ -231,22 +232,22 @@ __device__ __forceinline__ void tunrank_t(const T* bt, int S, int n, int m, T r,
       const T* row = bt + (parts - 2);
       #pragma unroll 1
       for (; x <= rem - (parts - 1); ++x) {
-        const T cnt = __ldg(&row[(rem - x - 1) * S]);
+        const T cnt = row[(rem - x - 1) * S];
         if (r < cnt) break;
         r -= cnt;
       }
     } else {
       const T* col = bt + (parts - 1);
-      const T tot = __ldg(&col[(rem - 1) * S]);  // C(rem - 1, parts - 1)
+      const T tot = col[(rem - 1) * S];  // C(rem - 1, parts - 1)
       const T thr = tot - r;                     // find the smallest x with C(rem - x - 1, parts - 1) < thr
       int lo = 1, hi = rem - parts + 1;
       #pragma unroll 1
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(&col[(rem - mid - 1) * S]) < thr) hi = mid; else lo = mid + 1;
+        if (col[(rem - mid - 1) * S] < thr) hi = mid; else lo = mid + 1;
       }
       x = lo;
-      r -= tot - __ldg(&col[(rem - x) * S]);  // S(x - 1)
+      r -= tot - col[(rem - x) * S];  // S(x - 1)
     }
     s.N[j] = (uint8_t)x;
     rem -= x;
@@ -255,12 +256,21 @@ __device__ __forceinline__ void tunrank_t(const T* bt, int S, int n, int m, T r,
 }
 
 template <int B>
-__device__ void tunrank(const Cfg& c, int n, int m, uint64_t rank, TS& s) {
-  // plans of < 2^32 compositions: every count met is below 2^32 too
-  if (m > 1 && __ldg(&c.binom[(n - 1) * (B + 1) + (m - 1)]) <= 0xffffffffull)
-    tunrank_t<uint32_t>(c.binom32, B + 1, n, m, (uint32_t)rank, s);
+__device__ __forceinline__ void tunrank(const Cfg& c, const uint32_t* b32, const TPlan& p, int n, uint64_t rank, TS& s) {
+  // plans of < 2^32 compositions: every count met is below 2^32 too (b32:
+  // the 32-bit table, staged in shared memory by the B = 32 kernels)
+  if (p.count <= 0xffffffffull)
+    tunrank_t<uint32_t>(b32, B + 1, n, p.m, (uint32_t)rank, s);
   else
-    tunrank_t<uint64_t>(c.binom, B + 1, n, m, rank, s);
+    tunrank_t<uint64_t>(c.binom, B + 1, n, p.m, rank, s);
+}
+
+// the kernels' 32-bit binomial table: staged in shared memory at B = 32 (33 x 33 words)
+template <int B>
+__device__ __forceinline__ const uint32_t* stage_binom32(const Cfg& c, uint32_t* sm) {
+  if (B != 32) return c.binom32;
+  for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) sm[i] = __ldg(&c.binom32[i]);
+  return sm;
 }
 
 // Lexicographic successor of N (m parts); false past the last composition.
@@ -1152,6 +1162,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
     k2_fast(Cfg c, EvalArgs A) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k2_general may become resident as blocks leave
   __shared__ int64_t G[B], D[B];
+  __shared__ uint32_t bsm[B == 32 ? 33 * 33 : 1];
+  const uint32_t* b32 = stage_binom32<B>(c, bsm);
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
   __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
   __shared__ uint64_t psuf[EXPLICIT ? 1 : kMaxE + 1];  // this rank's positions of the plans at k2order[k..]
@@ -1237,7 +1249,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
         e = tfind_plan(c, g);
         if (e >= 0) {
           if (e != p.e) tplan(c, e, p);
-          tunrank<B>(c, n, p.m, g - p.first, s);
+          tunrank<B>(c, b32, p, n, g - p.first, s);
           valid = true;
         }
       }
@@ -1298,7 +1310,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
           if (it == 0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
             const uint64_t rb = q / A.block;
             g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
-            tunrank<B>(c, n, p.m, g - p.first, s);
+            tunrank<B>(c, b32, p, n, g - p.first, s);
 #ifndef K2T_GSTATS
             st.v[11] += 1;
 #endif
@@ -1322,6 +1334,8 @@ template <int B, int BM>
 __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B == 64 ? 4 : 2) : B == 64 ? 3 : BM == 64 ? 2 : 1)
     k2_general(Cfg c, EvalArgs A) {
   __shared__ int64_t G[B], D[B];
+  __shared__ uint32_t bsm[B == 32 ? 33 * 33 : 1];
+  const uint32_t* b32 = stage_binom32<B>(c, bsm);
   const int lane = threadIdx.x & 31, n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1351,7 +1365,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
       const uint64_t qo = A.gqo[i];
       const int e = (int)(qo >> 56);
       if (e != p.e) tplan(c, e, p);
-      tunrank<B>(c, n, p.m, g - p.first, s);
+      tunrank<B>(c, b32, p, n, g - p.first, s);
       const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st);
       if (A.lat_out) A.lat_out[qo & ((1ull << 56) - 1)] = lat;
       tbetter(lat, g, bl, bg);
@@ -1386,6 +1400,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
 template <int B, int BM>
 __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64_t* out) {
   __shared__ int64_t G[B], D[B];
+  __shared__ uint32_t bsm[B == 32 ? 33 * 33 : 1];
+  const uint32_t* b32 = stage_binom32<B>(c, bsm);
   const int n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1402,7 +1418,7 @@ __global__ void __launch_bounds__(kTThreads) k2_explain(Cfg c, uint64_t g, int64
   TS s = ts_at<B, BM>(0u);
   uint32_t* E = reinterpret_cast<uint32_t*>(k2sm + 2 * BM);
   for (int t = 0; t < B + 2; ++t) E[t] = 0u;
-  tunrank<B>(c, n, p.m, g - p.first, s);
+  tunrank<B>(c, b32, p, n, g - p.first, s);
   TStats st = {{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
   out[5] = e;
   out[6] = p.m;
