@@ -1165,8 +1165,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
   __shared__ uint32_t bsm[B == 32 ? 33 * 33 : 1];
   const uint32_t* b32 = stage_binom32<B>(c, bsm);
   __shared__ uint64_t plo[EXPLICIT ? 1 : kMaxE], pn[EXPLICIT ? 1 : kMaxE];
-  __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready, 2 no chunks left
-  __shared__ uint64_t psuf[EXPLICIT ? 1 : kMaxE + 1];  // this rank's positions of the plans at k2order[k..]
+  __shared__ int pstate[EXPLICIT ? 1 : kMaxE];  // 0 not known ready, 1 ready
+  __shared__ uint64_t psum[EXPLICIT ? 1 : kMaxE + 1];  // this rank's positions of the plans before k2order[k]
   const int lane = threadIdx.x & 31, n = c.n;
   const int64_t T_end = c.scal[1];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1185,8 +1185,11 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
   __syncthreads();
   if (!EXPLICIT && threadIdx.x == 0) {
     uint64_t acc = 0;
-    psuf[c.n_k2order] = 0;
-    for (int k = c.n_k2order - 1; k >= 0; --k) psuf[k] = acc += pn[c.k2order[k]];
+    for (int k = 0; k < c.n_k2order; ++k) {
+      psum[k] = acc;
+      acc += pn[c.k2order[k]];
+    }
+    psum[c.n_k2order] = acc;
   }
   __syncthreads();
   TS s;  // the fast path only keeps the composition and its masks per thread
@@ -1256,70 +1259,70 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
       step(valid, g, i, e);
     }
   } else {
-    // Plan by plan in k2order, each plan once K1 has completed it (this
-    // launch may overlap K1).  This rank's positions: block-cyclic over
-    // [begin, end); plan e's are [plo[e], plo[e] + pn[e]).  A warp claims
-    // 32 * r consecutive positions of one plan at a time (r consecutive
-    // candidates per lane), r from kTRun down to 1 as the launch's remaining
-    // work shrinks (guided self-scheduling: no long tail when work is scarce).
+    // This rank's positions of the plans, concatenated in k2order: plan
+    // k2order[k] holds [psum[k], psum[k + 1]) of this order space, its
+    // positions of the block-cyclic sharding over [begin, end) being
+    // [plo[e], plo[e] + pn[e]).  A warp claims 32 * r consecutive order
+    // positions with one atomic (r from kTRun down to kTMinRun as the
+    // remaining work shrinks: guided self-scheduling) and evaluates them
+    // plan segment by plan segment, r consecutive candidates per lane, each
+    // segment once K1 has completed its plan (this launch may overlap K1;
+    // K1 finishes plans in k2order).
     const uint64_t nwarps = (uint64_t)gridDim.x * (kTThreads / 32);
+    const uint64_t T = psum[c.n_k2order];
+    int k = 0;  // plan cursor in k2order (claims only move forward)
     for (;;) {
-      int e = -1;
-      unsigned long long chunk = 0, take = 0;
+      unsigned long long x0 = 0, tk = 0;
       if (lane == 0) {
-        volatile int* pst = pstate;  // shared by the block's warps; only ever raised
-        for (;;) {
-          bool pending = false;
-          for (int k = 0; k < c.n_k2order; ++k) {
-            const int e2 = c.k2order[k];
-            const int ps = pst[e2];
-            if (ps == 2 || pn[e2] == 0) continue;
-            if (ps == 0) {  // poll relaxed (an acquire load invalidates L1), acquire once when complete
-              if (ld_relaxed(&c.pdone[e2]) < plan_items(c.plans[e2])) { pending = true; continue; }
-              (void)ld_acquire(&c.pdone[e2]);
-              pst[e2] = 1;
-            }
-            const unsigned long long done = *(volatile unsigned long long*)&c.pclaim[e2];
-            const unsigned long long rem = pn[e2] > done ? pn[e2] - done : 0;
-            const unsigned long long left = rem + psuf[k + 1];
-            const unsigned long long tk = min(32ull * kTRun, max(32ull * kTMinRun, left * kTGss / (kTGssDen * nwarps) / 32 * 32));
-            const unsigned long long st0 = atomicAdd(&c.pclaim[e2], tk);
-            if (st0 < pn[e2]) { e = e2; chunk = st0; take = tk; break; }
-            pst[e2] = 2;
-          }
-          if (e >= 0 || !pending) break;
-          __nanosleep(500);
-        }
+        const unsigned long long seen = *(volatile unsigned long long*)A.counter;
+        const unsigned long long left = T > seen ? T - seen : 0;
+        tk = min(32ull * kTRun, max(32ull * kTMinRun, left * kTGss / (kTGssDen * nwarps) / 32 * 32));
+        x0 = left ? atomicAdd(A.counter, tk) : T;
       }
-      e = __shfl_sync(0xffffffffu, e, 0);
-      chunk = __shfl_sync(0xffffffffu, chunk, 0);
-      take = __shfl_sync(0xffffffffu, take, 0);
-      __syncwarp();  // the lanes' table reads follow lane 0's acquire
-      if (e < 0) break;
-      if (e != p.e) tplan(c, e, p);
-      const int r = (int)(take / 32);
+      x0 = __shfl_sync(0xffffffffu, x0, 0);
+      tk = __shfl_sync(0xffffffffu, tk, 0);
+      if (x0 >= T) break;
+      const uint64_t x1 = min((uint64_t)(x0 + tk), T);
 #ifndef K2T_GSTATS
       st.v[10] += lane == 0;
 #endif
-      const uint64_t p0 = plo[e] + chunk + (uint64_t)lane * r, pend = plo[e] + pn[e];
-      uint64_t g = 0;
-      for (int it = 0; it < r; ++it) {  // the same trip count on every lane (warp-synchronous queue)
-        const uint64_t q = p0 + it;
-        const bool valid = q < pend;
-        if (valid) {
-          if (it == 0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
-            const uint64_t rb = q / A.block;
-            g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
-            tunrank<B>(c, b32, p, n, g - p.first, s);
-#ifndef K2T_GSTATS
-            st.v[11] += 1;
-#endif
-          } else {
-            ++g;
-            tnext(p.m, s);
+      for (uint64_t x = x0; x < x1;) {
+        while (psum[k + 1] <= x) ++k;
+        const int e = c.k2order[k];
+        const uint64_t xb = min(x1, psum[k + 1]);
+        if (__shfl_sync(0xffffffffu, pstate[e], 0) == 0) {  // wait for K1 to complete plan e
+          if (lane == 0) {
+            volatile int* pst = pstate;  // shared by the block's warps; only ever raised
+            // poll relaxed (an acquire load invalidates L1), acquire once when complete
+            while (pst[e] == 0 && ld_relaxed(&c.pdone[e]) < plan_items(c.plans[e])) __nanosleep(500);
+            (void)ld_acquire(&c.pdone[e]);
+            pst[e] = 1;
           }
+          __syncwarp();  // the lanes' table reads follow lane 0's acquire
         }
-        step(valid, g, g - A.begin, e);
+        if (e != p.e) tplan(c, e, p);
+        const int r = (int)((xb - x + 31) / 32);
+        const uint64_t p0 = plo[e] + (x - psum[k]) + (uint64_t)lane * r, pend = plo[e] + (xb - psum[k]);
+        uint64_t g = 0;
+        for (int it = 0; it < r; ++it) {  // the same trip count on every lane (warp-synchronous queue)
+          const uint64_t q = p0 + it;
+          const bool valid = q < pend;
+          if (valid) {
+            if (it == 0 || q % A.block == 0) {  // (re)locate: positions -> global indices jump at rank blocks
+              const uint64_t rb = q / A.block;
+              g = A.begin + (rb * A.world + A.rank) * (uint64_t)A.block + (q - rb * A.block);
+              tunrank<B>(c, b32, p, n, g - p.first, s);
+#ifndef K2T_GSTATS
+              st.v[11] += 1;
+#endif
+            } else {
+              ++g;
+              tnext(p.m, s);
+            }
+          }
+          step(valid, g, g - A.begin, e);
+        }
+        x = xb;
       }
     }
   }
