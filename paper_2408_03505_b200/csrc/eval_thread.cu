@@ -274,6 +274,25 @@ __device__ __forceinline__ const uint32_t* stage_binom32(const Cfg& c, uint32_t*
 }
 
 // Lexicographic successor of N (m parts); false past the last composition.
+// A composition packed into 64 bits for k2_general's queue: N_j - 1 in
+// kPackBits bits each, for m <= kPackParts (N_j <= B).
+template <int B>
+__host__ __device__ constexpr int kPackBits() { return B <= 32 ? 5 : B <= 64 ? 6 : 7; }
+template <int B>
+__host__ __device__ constexpr int kPackParts() { return 64 / kPackBits<B>(); }
+template <int B>
+__device__ __forceinline__ uint64_t tpack(const SB N, int m) {
+  uint64_t v = 0;
+#pragma unroll 1
+  for (int j = m - 1; j >= 0; --j) v = v << kPackBits<B>() | (uint64_t)(N[j] - 1);
+  return v;
+}
+template <int B>
+__device__ __forceinline__ void tunpack(uint64_t v, int m, const SB N) {
+#pragma unroll 1
+  for (int j = 0; j < m; ++j, v >>= kPackBits<B>()) N[j] = (uint8_t)((v & ((1u << kPackBits<B>()) - 1u)) + 1u);
+}
+
 __device__ bool tnext(int m, TS& s) {
   if (m < 2) return false;
   const int last = s.N[m - 1];
@@ -1233,6 +1252,7 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
       const unsigned x = qb + __popc(want & lt_mask);
       A.gq[x] = g;
       A.gqo[x] = out | (uint64_t)e << 56;
+      if (p.m <= kPackParts<B>()) A.gqc[x] = tpack<B>(s.N, p.m);  // the composition: no unranking in k2_general
     }
     qb += k;
   };
@@ -1368,7 +1388,8 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
       const uint64_t qo = A.gqo[i];
       const int e = (int)(qo >> 56);
       if (e != p.e) tplan(c, e, p);
-      tunrank<B>(c, b32, p, n, g - p.first, s);
+      if (p.m <= kPackParts<B>()) tunpack<B>(A.gqc[i], p.m, s.N);
+      else tunrank<B>(c, b32, p, n, g - p.first, s);
       const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st);
       if (A.lat_out) A.lat_out[qo & ((1ull << 56) - 1)] = lat;
       tbetter(lat, g, bl, bg);
