@@ -68,7 +68,7 @@ struct Prep {
   // layout (byte offsets in the workspace)
   size_t o_lkind, o_lns, o_loff, o_blayers, o_binom, o_binom32, o_plans, inputs_bytes;
   size_t o_W, o_Wdef, o_scal, o_F, o_B, o_w, o_z, o_opstart, o_ncomp, o_ncomm, o_comp_lo, o_comp_hi, o_comm_lo,
-      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_gq, o_gqo, o_gqc, o_gqn, o_partials2, o_explain, o_order, o_rec, o_base, total_bytes;
+      o_comm_hi, o_bmax, o_sim, o_k0res, o_tables, o_snap, o_bfill, o_snap_own, o_units, o_k1flags, o_k2order, o_sync, o_iv, o_partials, o_counter, o_stats, o_gq, o_gqo, o_gqc, o_gqd, o_gqn, o_partials2, o_explain, o_order, o_rec, o_base, total_bytes;
   int base_L = 0, base_Le = 0;
   uint64_t gqcap = 0;  // Megatron baselines: layers in the sequence, encoder layers among them
   int grid;
@@ -328,6 +328,7 @@ int prepare(const optimus_problem* pb, Prep& X) {
   X.o_gq = take((size_t)X.gqcap * 8);
   X.o_gqo = take((size_t)X.gqcap * 8);
   X.o_gqc = take((size_t)X.gqcap * 8);
+  X.o_gqd = take((size_t)X.gqcap * 8);
   X.o_gqn = take(64);  // [0] u32 reserved slots, [8] u64 general kernel's work counter, [16] u32 blocks done
   X.o_partials2 = take((size_t)4096 * 2 * 8);
   X.o_counter = take(8);
@@ -575,6 +576,7 @@ static int eval_common(optimus_ctx* c, EvalArgs& a, cudaStream_t st) {
   a.gq = (unsigned long long*)(c->ws + c->X.o_gq);
   a.gqo = (unsigned long long*)(c->ws + c->X.o_gqo);
   a.gqc = (unsigned long long*)(c->ws + c->X.o_gqc);
+  a.gqd = (long long*)(c->ws + c->X.o_gqd);
   a.gqn = (unsigned int*)(c->ws + c->X.o_gqn);
   a.counter2 = (unsigned long long*)(c->ws + c->X.o_gqn + 8);
   a.gdone = (unsigned int*)(c->ws + c->X.o_gqn + 16);

@@ -782,7 +782,7 @@ __device__ __forceinline__ int64_t tbwd1(const TPlan& p, const int64_t* D, const
 // forward / backward move counts.
 template <int B, bool EXPLAIN = false>
 __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const int64_t* D, int64_t T_end, TS& s,
-                         uint32_t* E, TStats& st, int64_t* xo = nullptr) {
+                         uint32_t* E, TStats& st, int64_t* xo = nullptr, int js1 = -1, int64_t dep1 = 0) {
   constexpr bool kMask = B == 32;
   const int n = c.n, m = p.m, kmax = p.kmax;
   const uint32_t all = m >= 32 ? 0xffffffffu : (1u << m) - 1u;
@@ -818,7 +818,23 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
   // initial forward shift (no thresholds, no trial): the first slot of each
   // level t sits at position sum_{t' < t} cnt[t'] (tdep_fwd with M = 0)
   int64_t dep = kNegInf;
-  {
+  if (kMask && js1 >= 0) {
+    // resume after the fast path's first forward iteration, which committed
+    // pipeline js1's move with forward shift dep1 (tfast: the same pick and
+    // trial as this loop's first iteration; B = 32 plans only)
+    const uint32_t bit = 1u << js1;
+    const int cjs = s.c[js1];
+    E[cjs] &= ~bit;
+    E[cjs - 1] |= bit;
+    thr[0] = (uint8_t)p.at(p.bpF, row_of(p, js1) * kmax);
+    s.c[js1] = (uint8_t)(cjs - 1);
+    MV = bit;
+    M = 1;
+    dep = dep1;
+    --sumc;
+    itf = atf = 1;
+    kf0 = cjs > 1 ? __ldg(reinterpret_cast<const uint32_t*>(p.ptr(p.kj)) + 2 * (js1 * p.np1 + cjs - 1)) : 0u;
+  } else {
     uint32_t A = all;
 #pragma unroll 1
     for (int t = 1, pos = 0; pos < n; ++t) {
@@ -997,7 +1013,7 @@ __device__ int64_t teval(const Cfg& c, const TPlan& p, const int64_t* G, const i
 // Leaves E zeroed.  MT: the mask word (16 bits for instances of m <= 16).
 template <int B, typename MT>
 __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const int64_t* D, int n, const TS& s,
-                                      MT* E, int64_t& Df, int64_t& Db, TStats& st) {
+                                      MT* E, int64_t& Df, int64_t& Db, TStats& st, int& js1, int64_t& dep1) {
   const int m = p.m, np1 = p.np1;
   uint32_t kf0 = 0, kb0 = 0;
   int Nmax = 0;
@@ -1030,6 +1046,7 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
     }
   }
   bool general = false;
+  js1 = -1;
   // ---- forward, first iteration
   int js;
   const int64_t dev = crit_value(p, p.devF, s.N, kf0, js);
@@ -1054,6 +1071,10 @@ __device__ __forceinline__ bool tfast(const TPlan& p, const int64_t* G, const in
           pos += __popc(A);
         }
         general = dep2 <= Delta;  // checkEncLLMDep holds: the move commits
+        if (general) {  // k2_general resumes after this commit
+          js1 = js;
+          dep1 = dep2;
+        }
       }
     }
   }
@@ -1226,9 +1247,11 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
   // one candidate per lane (valid lanes): fast path, else into the queue
   auto step = [&](bool valid, uint64_t g, uint64_t out, int e) {
     bool pend = false;
+    int js1 = -1;
+    int64_t dep1 = 0;
     if (valid) {
       int64_t Df, Db;
-      if (p.fast && tfast<B, MT>(p, G, D, n, s, E, Df, Db, st)) {
+      if (p.fast && tfast<B, MT>(p, G, D, n, s, E, Df, Db, st, js1, dep1)) {
         const int64_t lat = T_end + Df + Db;  // R16
         if (A.lat_out) A.lat_out[out] = lat;
         tbetter(lat, g, bl, bg);
@@ -1252,7 +1275,11 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_MINB : K2T_MINB_WIDE)
       const unsigned x = qb + __popc(want & lt_mask);
       A.gq[x] = g;
       A.gqo[x] = out | (uint64_t)e << 56;
-      if (p.m <= kPackParts<B>()) A.gqc[x] = tpack<B>(s.N, p.m);  // the composition: no unranking in k2_general
+      if (p.m <= kPackParts<B>()) {  // the composition (no unranking in k2_general) and the first forward commit
+        const bool r = B == 32 && js1 >= 0 && kPackBits<B>() * p.m + 4 <= 64 && js1 < 15;
+        A.gqc[x] = tpack<B>(s.N, p.m) | (r ? (uint64_t)(js1 + 1) << (kPackBits<B>() * p.m) : 0ull);
+        if (r) A.gqd[x] = dep1;
+      }
     }
     qb += k;
   };
@@ -1388,9 +1415,17 @@ __global__ void __launch_bounds__(kTThreads, B == 32 ? K2T_GMINB : BM == 16 ? (B
       const uint64_t qo = A.gqo[i];
       const int e = (int)(qo >> 56);
       if (e != p.e) tplan(c, e, p);
-      if (p.m <= kPackParts<B>()) tunpack<B>(A.gqc[i], p.m, s.N);
-      else tunrank<B>(c, b32, p, n, g - p.first, s);
-      const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st);
+      int js1 = -1;
+      int64_t dep1 = 0;
+      if (p.m <= kPackParts<B>()) {
+        const uint64_t v = A.gqc[i];
+        tunpack<B>(v, p.m, s.N);
+        if (B == 32 && kPackBits<B>() * p.m + 4 <= 64) js1 = (int)(v >> (kPackBits<B>() * p.m)) - 1;
+        if (js1 >= 0) dep1 = A.gqd[i];
+      } else {
+        tunrank<B>(c, b32, p, n, g - p.first, s);
+      }
+      const int64_t lat = teval<B>(c, p, G, D, T_end, s, E, st, nullptr, js1, dep1);
       if (A.lat_out) A.lat_out[qo & ((1ull << 56) - 1)] = lat;
       tbetter(lat, g, bl, bg);
       if (B == 32)

@@ -171,7 +171,8 @@ struct EvalArgs {
   // evaluates through a global queue, a chunk of the range at a time
   unsigned long long* gq;     // [gqcap] g (~0: unused slot)
   unsigned long long* gqo;    // [gqcap] lat_out position | plan << 56
-  unsigned long long* gqc;    // [gqcap] the packed composition (plans of m <= kPackParts)
+  unsigned long long* gqc;    // [gqcap] the packed composition (plans of m <= kPackParts) | first forward pick + 1
+  long long* gqd;             // [gqcap] forward shift after that pick's commit (B = 32)
   unsigned int* gqn;          // slots reserved (warps take batches of kGqBatch)
   uint64_t gqcap;
   int64_t* partials2;         // [grid2][2] general kernel's block bests
