@@ -35,9 +35,29 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef K1_SCALAR
+#define K1_SCALAR 4  // kernels placed one by one before a 32-wide batch is tried
+#endif
+#ifndef K1_GROUPS
+#define K1_GROUPS 32  // most chains of one unit in flight (1: one chain after the other)
+#endif
+
+#ifdef K1_TRACE  // development instrumentation: per K1 work item start / end (globaltimer ns), item, block
+#define K1_STATS
+__device__ unsigned long long g_k1trace[16384][4];
+__device__ unsigned long long g_k1stats[4096][32][14];
+#endif
+
 #ifdef K1_STATS  // development instrumentation (OPTIMUS_NVCC_EXTRA=-DK1_STATS): per-warp event counts
-__shared__ unsigned long long k1st[32][8];  // placements, fast hits, ballots, window advances, place cyc, wait cyc
+// 0 place_stage prologs, 1 unit setup, 2 slow placements, 3 vwait cycles,
+// 4 placement loop, 5 upstream-stage waits, 6 total, 7 slow cycles, 8 publish, 9 fast rounds,
+// 10 window advances, 11 advance cycles, 12 slow found in the current window, 13 flush cycles
+__shared__ unsigned long long k1st[32][14];
+__shared__ int k1item;
 #define K1ST(i, v) do { if ((threadIdx.x & 31) == 0) k1st[threadIdx.x >> 5][i] += (v); } while (0)
+#ifndef K1ST_MIN
+#define K1ST_MIN 150000
+#endif
 #else
 #define K1ST(i, v) do { } while (0)
 #endif
@@ -151,6 +171,14 @@ struct VR {
   int64_t* snap0;        // this list in version 0's buffer; version o at + o * vstride
   int64_t vstride;
   int64_t T_end;
+  // chain pipeline (several chains of one stage in flight on different
+  // warps, chain k trailing chain k-1): a 32-block is "passed" by a chain
+  // once its window has left it; later chains only read passed blocks.
+  volatile int* pprev;   // blocks passed by chain k-1 on this list (smem; nullptr: chain k-1 is complete)
+  volatile int* pmine;   // blocks passed by this chain (nullptr: nobody trails it)
+  const volatile int* stopp;  // first void chain of the unit
+  int16_t* gown;         // forward: version k+1's published owner map of this list (passed blocks written on pass)
+  int passed, k;
   __device__ __forceinline__ int64_t hi_at(int i) const {
     if (!M) return H[i];
     const int r = count - 1 - i;
@@ -172,7 +200,7 @@ struct VR {
 // at or before `ready` from then on, so first fit can start there.
 struct Win {
   int base, cur;
-  bool dirty;
+  bool dirty, nok;  // nok: the prefetched next window was read after the previous chain passed it
   int64_t lo, hi, nlo, nhi;
   int64_t clo, chi;  // fill pointer / end of interval cur (clo authoritative); both -inf when cur < 0
 };
@@ -189,15 +217,73 @@ __device__ __forceinline__ void win_fetch(const VR<M>& V, int b, int64_t& lo, in
   }
 }
 
+// Blocks [V.passed, nb) of this list are final for the chains that trail
+// this one: publish their owners (forward) and the pass count.  Every lane
+// fences its own stores (window flushes) before lane 0 releases the count.
 template <bool M>
-__device__ __forceinline__ void win_open(const VR<M>& V, Win& w, int b) {
+__device__ __forceinline__ void vpass(VR<M>& V, int nb) {
+  if (nb <= V.passed) return;
+  const int lane = threadIdx.x & 31;
+  if (!M && V.gown)
+    for (int b = V.passed + lane; b < nb; b += 32) V.gown[b] = V.own[b];
+  if (V.pmine) {
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *V.pmine = nb;
+  }
+  V.passed = nb;
+}
+
+// Wait until the previous chain has passed block b of this list (false:
+// this chain is void, an earlier one failed).  Decisions on lane 0's reads.
+template <bool M>
+__device__ __forceinline__ bool vwait(const VR<M>& V, int b) {
+  if (!V.pprev) return true;
+  if (__shfl_sync(FULL, *V.pprev, 0) > b) {
+    __threadfence_block();
+    return true;
+  }
+#ifdef K1_STATS
+  const long long tv0 = clock64();
+#endif
+  for (;;) {
+    if (__shfl_sync(FULL, *V.pprev, 0) > b) break;
+    if (V.k >= __shfl_sync(FULL, *V.stopp, 0)) return false;
+    __nanosleep(32);
+  }
+#ifdef K1_STATS
+  K1ST(3, clock64() - tv0);
+#endif
+  __threadfence_block();
+  return true;
+}
+
+// prefetch window b + 32 only if the previous chain already passed it
+template <bool M>
+__device__ __forceinline__ void win_prefetch(const VR<M>& V, Win& w) {
+  const int nb = (w.base >> 5) + 1;
+  w.nok = !V.pprev || __shfl_sync(FULL, *V.pprev, 0) > nb;
+  if (w.nok) {
+    __threadfence_block();
+    win_fetch(V, w.base + 32, w.nlo, w.nhi);
+  }
+}
+
+template <bool M>
+__device__ __forceinline__ bool win_open(VR<M>& V, Win& w, int b) {
   w.base = b;
   w.cur = -1;
   w.clo = kNegInf;  // no current interval: the fast path's max-plus terms must stay inert
   w.chi = kNegInf;
   w.dirty = false;
+  w.nok = false;
+  // the blocks before the ready time are never touched by this chain: their
+  // owners are final once the previous chain has passed them
+  if (!vwait(V, b >> 5)) return false;
+  vpass(V, b >> 5);
   win_fetch(V, b, w.lo, w.hi);
-  win_fetch(V, b + 32, w.nlo, w.nhi);
+  win_prefetch(V, w);
+  return true;
 }
 
 __device__ __forceinline__ void win_sync_cur(Win& w) {
@@ -218,7 +304,7 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   const int64_t cap = warp_max64(i < V.count ? w.hi - w.lo : kNegInf);
   if (lane == 0) {
     V.bm[w.base >> 5] = cap;
-    if (M) V.wm[w.base >> 10] |= 1u << ((w.base >> 5) & 31);
+    if (M) atomicOr(&V.wm[w.base >> 10], 1u << ((w.base >> 5) & 31));  // chains in flight share the word
     else V.own[w.base >> 5] = (int16_t)V.ver;
   }
   w.dirty = false;
@@ -253,6 +339,9 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
       const int64_t x = max(ready, w.lo);
       const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
       if (b) {
+#ifdef K1_STATS
+        K1ST(12, 1);
+#endif
         const int f = __ffs(b) - 1;
         const int64_t xf = __shfl_sync(FULL, x, f);
         w.chi = __shfl_sync(FULL, w.hi, f);
@@ -263,17 +352,29 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
         return true;
       }
     }
+#ifdef K1_STATS
+    const long long ta0 = clock64();
+#endif
     win_flush(V, w);
+#ifdef K1_STATS
+    K1ST(13, clock64() - ta0);
+    K1ST(10, 1);
+#endif
     const int nb = next_block(ci, bm, CI, blk + 1, ready, d);
     if (32 * nb >= V.count) return false;
-    if (32 * nb == w.base + 32) {
+    if (!vwait(V, nb)) return false;
+    vpass(V, nb);
+    if (32 * nb == w.base + 32 && w.nok) {
       w.lo = w.nlo;
       w.hi = w.nhi;
     } else {
       win_fetch(V, 32 * nb, w.lo, w.hi);
     }
     w.base = 32 * nb;
-    win_fetch(V, w.base + 32, w.nlo, w.nhi);
+    win_prefetch(V, w);
+#ifdef K1_STATS
+    K1ST(11, clock64() - ta0);
+#endif
   }
 }
 
@@ -285,13 +386,16 @@ struct UnitSm {
   int64_t* ci;        // [P][2][CI] coarse index: end of the last interval of each 32-block
   int64_t* bm;        // [P][2][CI] largest base capacity of each 32-block (this orientation)
   int16_t* own;       // [P][2][CI] snapshot block owners (forward: current, mirror: snapshot kf); int16: versions reach kmax = n - m + 1 <= 128
+  int64_t* pe;        // [NK + P] stage-local exclusive duration prefix: pe[s + x] = sum of d over [soff[s], x), x in [soff[s], soff[s+1]]
+  uint32_t* lcp;      // [NK] 1 + the last comm kernel <= x of its stage (low 16 bits), 1 + the last compute kernel (high; 0: none)
   int CI, MW;
 };
 
 __host__ __device__ inline size_t unit_smem_bytes(int NK, int P, int CI) {
   const int MW = (CI + 31) / 32;
   return ((size_t)NK * 8 + 15) / 16 * 16 + ((size_t)(P + 1) * 4 + 15) / 16 * 16 +
-         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI * 2 + 15) / 16 * 16;
+         ((size_t)P * 2 * MW * 4 + 15) / 16 * 16 + (size_t)P * 2 * CI * 8 * 2 + ((size_t)P * 2 * CI * 2 + 15) / 16 * 16 +
+         (size_t)(NK + P) * 8 + ((size_t)NK * 4 + 15) / 16 * 16;
 }
 
 __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
@@ -306,6 +410,10 @@ __device__ UnitSm carve(unsigned char* p, int NK, int P, int CI) {
   u.bm = u.ci + (size_t)P * 2 * CI;
   p += (size_t)P * 2 * CI * 8 * 2;
   u.own = (int16_t*)p;
+  p += ((size_t)P * 2 * CI * 2 + 15) / 16 * 16;
+  u.pe = (int64_t*)p;
+  p += (size_t)(NK + P) * 8;
+  u.lcp = (uint32_t*)p;
   u.CI = CI;
   u.MW = (CI + 31) / 32;
   return u;
@@ -338,6 +446,37 @@ __device__ void build_seq(const Cfg& c, const PlanDesc& pd, bool mirror, UnitSm&
     pos += cnt;
   }
   if (lane == 0 && s == P - 1) U.soff[P] = pos;
+  __syncwarp();
+  // the fast path's run tables: duration prefix and last kernel of each kind
+  const int i0 = U.soff[s];
+  int64_t carry = 0;
+  int lc = 0, lp = 0;
+  if (lane == 0) U.pe[s + i0] = 0;
+  for (int b = i0; b < pos; b += 32) {
+    const int x = b + lane;
+    const int64_t v = x < pos ? U.seq[x] : 0;
+    int64_t d = v & INT64_MAX;
+    int mc = x < pos && v < 0 ? x - i0 + 1 : 0, mp = x < pos && v >= 0 ? x - i0 + 1 : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(FULL, d, o);
+      const int tc = __shfl_up_sync(FULL, mc, o), tp = __shfl_up_sync(FULL, mp, o);
+      if (lane >= o) {
+        d += t;
+        mc = max(mc, tc);
+        mp = max(mp, tp);
+      }
+    }
+    mc = max(mc, lc);
+    mp = max(mp, lp);
+    if (x < pos) {
+      U.pe[s + x + 1] = carry + d;
+      U.lcp[x] = (uint32_t)(mc ? mc + i0 : 0) | (uint32_t)(mp ? mp + i0 : 0) << 16;
+    }
+    carry += __shfl_sync(FULL, d, 31);
+    lc = __shfl_sync(FULL, mc, 31);
+    lp = __shfl_sync(FULL, mp, 31);
+  }
 }
 
 // view of list r of stage s of row a; fill = this unit's fill array of the
@@ -358,6 +497,12 @@ __device__ VR<M> make_view(const Cfg& c, const PlanDesc& pd, int a, int s, int r
   V.vstride = (int64_t)pd.rp * pd.P * (c.icapc + c.icapm);
   V.wm = U.wm + (2 * s + r) * U.MW;
   V.T_end = c.scal[1];
+  V.pprev = nullptr;
+  V.pmine = nullptr;
+  V.stopp = nullptr;
+  V.gown = nullptr;
+  V.passed = 0;
+  V.k = 0;
   return V;
 }
 
@@ -393,9 +538,17 @@ struct UnitCtx {
 // (the unit stops).
 // REC (schedule emission, NEXT-1): rec[q] = {stage, comm, start, end} of
 // kernel q of the chain (q = index in the flattened stage-major list).
+// the chain pipeline's links of one chain-stage (per resource r)
+struct Link {
+  volatile int* pprev[2];      // pass counts of chain k-1 (nullptr: no wait)
+  volatile int* pmine[2];      // this chain's pass counts (nullptr: nobody trails)
+  int16_t* gown[2];            // forward: version k+1's owner maps (nullptr: not published)
+  const volatile int* stopp;
+};
+
 template <bool M, bool REC = false>
 __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, UnitSm& U, int s, int k,
-                            int64_t ready, int64_t* end, int64_t* rec = nullptr) {
+                            int64_t ready, int64_t* end, const Link& lk, int64_t* rec = nullptr) {
 #ifdef K1_STATS
   const long long tp0 = clock64();
 #endif
@@ -404,9 +557,18 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
   int64_t* s0 = X.snap0 + (int64_t)s * icap;
   VR<M> V0 = make_view<M>(c, pd, X.a, s, 0, f0, U, s0, k + 1);
   VR<M> V1 = make_view<M>(c, pd, X.a, s, 1, f0, U, s0, k + 1);
+  V0.pprev = lk.pprev[0];
+  V1.pprev = lk.pprev[1];
+  V0.pmine = lk.pmine[0];
+  V1.pmine = lk.pmine[1];
+  V0.gown = lk.gown[0];
+  V1.gown = lk.gown[1];
+  V0.stopp = V1.stopp = lk.stopp;
+  V0.passed = V1.passed = 0;
+  V0.k = V1.k = k;
   Win w0, w1;  // compute-free / comm-free windows of this stage
-  win_open(V0, w0, ci_search(U.ci + (2 * s) * U.CI, U.CI, ready));
-  win_open(V1, w1, ci_search(U.ci + (2 * s + 1) * U.CI, U.CI, ready));
+  if (!win_open(V0, w0, ci_search(U.ci + (2 * s) * U.CI, U.CI, ready))) return false;
+  if (!win_open(V1, w1, ci_search(U.ci + (2 * s + 1) * U.CI, U.CI, ready))) return false;
   const int i1 = U.soff[s + 1];
   const int64_t* seq = U.seq;
   const int i0 = U.soff[s];
@@ -416,68 +578,67 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
   K1ST(0, t0 - tp0);
 #endif
   for (;;) {
-    // fast path, 32 kernels at a time (lane l = kernel i+l): while every
-    // kernel fits the current interval of its resource (chi = -inf when
-    // there is none), a kernel starts at the previous end unless it is the
-    // first of its resource in the batch (then at max(prev end, clo)), so
-    // e_l = D_l + max(ready, clo_r - Dex_{f_r} for each resource r whose
-    // first lane f_r <= l), D = inclusive prefix sum of the durations.
-    // The first kernel that does not fit goes to the slow path.
-    while (i < i1) {
-      const int lane = threadIdx.x & 31;
-      const bool valid = i + lane < i1;
-      const int64_t v = valid ? seq[i + lane] : 0;
+    // scalar steps first (warp-uniform, the sequential definition): after a
+    // slow placement the next kernels often leave the current intervals
+    // within a few steps, where a 32-wide batch would mostly be wasted
+    bool fits = true;
+#pragma unroll 1
+    for (int ns = 0; ns < K1_SCALAR && i < i1; ++ns) {
+      const int64_t v = seq[i];
       const bool comm = v < 0;
       const int64_t d = v & INT64_MAX;
-      int64_t D, Dc, Dp;  // inclusive prefix sum; exclusive sums at the first lane of each resource
-      const unsigned mc = __ballot_sync(FULL, valid && comm), mp = __ballot_sync(FULL, valid && !comm);
-      const int fc = mc ? __ffs(mc) - 1 : 32, fp = mp ? __ffs(mp) - 1 : 32;
-      if (__all_sync(FULL, d < (int64_t(1) << 26))) {  // the usual case: a 32-bit scan cannot overflow
-        unsigned D32 = (unsigned)d;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned t = __shfl_up_sync(FULL, D32, o);
-          if (lane >= o) D32 += t;
-        }
-        const unsigned Dex32 = D32 - (unsigned)d;
-        D = D32;
-        Dc = __shfl_sync(FULL, Dex32, fc & 31);
-        Dp = __shfl_sync(FULL, Dex32, fp & 31);
-      } else {
-        D = d;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int64_t t = __shfl_up_sync(FULL, D, o);
-          if (lane >= o) D += t;
-        }
-        const int64_t Dex = D - d;
-        Dc = __shfl_sync(FULL, Dex, fc & 31);
-        Dp = __shfl_sync(FULL, Dex, fp & 31);
+      const int64_t e = max(ready, comm ? w1.clo : w0.clo) + d;
+      if (e > (comm ? w1.chi : w0.chi)) {
+        fits = false;
+        break;
       }
-      const int64_t Ac = w1.clo - Dc;
-      const int64_t Ap = w0.clo - Dp;
-      int64_t st = ready;
-      if (lane >= fc) st = max(st, Ac);
-      if (lane >= fp) st = max(st, Ap);
-      const int64_t e = D + st;
-      const unsigned bad = __ballot_sync(FULL, valid && e > (comm ? w1.chi : w0.chi));
-      const int nv = min(32, i1 - i);
-      const int f = bad ? __ffs(bad) - 1 : nv;  // kernels placed by this batch
-      if (REC && lane < f) {
-        int64_t* r = rec + (int64_t)(i + lane) * 4;
+      if (REC && (threadIdx.x & 31) == 0) {
+        int64_t* r = rec + (int64_t)i * 4;
         r[0] = s;
         r[1] = comm;
         r[2] = e - d;
         r[3] = e;
       }
+      ready = e;
+      if (comm) w1.clo = e;
+      else w0.clo = e;
+      ++i;
+    }
+    // fast path, runs of up to 32 kernels (lane l = kernel i+l): inside the
+    // current intervals every kernel starts at the previous end (the fill
+    // pointers never pass `ready`), so kernel l ends at ready + pe(i, l] and
+    // "kernels i..x all fit" holds iff the last kernel of each kind up to x
+    // ends within its resource's current interval (ends only grow with x):
+    // two table lookups per lane and one ballot per run of 32
+    const int64_t* pe = U.pe + s;
+    while (fits && i < i1) {
+      const int lane = threadIdx.x & 31;
+      const int64_t base = ready - pe[i];
+      const int64_t thc = w1.chi - base, thp = w0.chi - base;
+      const int x = i + lane;
+      bool ok = true;
+      if (x < i1) {
+        const uint32_t q = U.lcp[x];
+        const int lc = (int)(q & 0xffffu) - 1, lp = (int)(q >> 16) - 1;
+        ok = (lc < i || pe[lc + 1] <= thc) && (lp < i || pe[lp + 1] <= thp);
+      }
+      const unsigned okm = __ballot_sync(FULL, ok);
+      K1ST(9, 1);
+      const int nv = min(32, i1 - i);
+      const int f = min(nv, okm == FULL ? 32 : __ffs(~okm) - 1);  // kernels [i, i+f) fit
+      if (REC && lane < f) {
+        int64_t* r = rec + (int64_t)(i + lane) * 4;
+        r[0] = s;
+        r[1] = U.seq[i + lane] < 0;
+        r[2] = base + pe[i + lane];
+        r[3] = base + pe[i + lane + 1];
+      }
       if (f > 0) {
-        ready = __shfl_sync(FULL, e, f - 1);
-        const unsigned below = f == 32 ? FULL : ((1u << f) - 1u);
-        const unsigned lc = mc & below, lp = mp & below;
-        const int64_t ec = __shfl_sync(FULL, e, lc ? 31 - __clz(lc) : 0);
-        const int64_t ep = __shfl_sync(FULL, e, lp ? 31 - __clz(lp) : 0);
-        if (lc) w1.clo = ec;
-        if (lp) w0.clo = ep;
+        const uint32_t q = U.lcp[i + f - 1];
+        const int lc = (int)(q & 0xffffu) - 1, lp = (int)(q >> 16) - 1;
+        if (lc >= i) w1.clo = base + pe[lc + 1];
+        if (lp >= i) w0.clo = base + pe[lp + 1];
+        ready = base + pe[i + f];
         i += f;
       }
       if (f < nv) break;
@@ -510,6 +671,10 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
 #endif
   win_flush(V0, w0);
   win_flush(V1, w1);
+  // the rest of both lists: final once the previous chain is complete
+  if (!vwait(V0, U.CI - 1) || !vwait(V1, U.CI - 1)) return false;
+  vpass(V0, U.CI);
+  vpass(V1, U.CI);
   __syncwarp();
   *end = ready;
   return true;
@@ -521,7 +686,7 @@ struct K1Launch {
 };
 
 __host__ __device__ inline size_t k1_smem_bytes(const K1Launch& L) {
-  return unit_smem_bytes(L.NK, L.Pmax, L.CI) + (size_t)L.Pmax * L.KM * (8 + 4) + 16;
+  return unit_smem_bytes(L.NK, L.Pmax, L.CI) + (size_t)L.Pmax * L.KM * (8 + 4 + 8) + 16;
 }
 
 __device__ __forceinline__ int ld_relaxed(const int* p) {
@@ -536,24 +701,33 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// One K1 unit per block, one warp per encoder stage s (a wavefront over
-// chains): chain k of stage s starts when chain k of stage s-1 has ended
-// (shared-memory flags) and chain k-1 of stage s is done (program order).
-// Forward (M = false): successive chains on fresh instances; after chain k
-// each stage publishes version k+1 of its fill state (flags[k+1] counts the
-// stages), and the unit ends with flags[0] = 1.  Backward (M = true):
-// mirrored chains on top of forward version kf, started once it is
-// published (or skipped when the forward unit ended with fewer chains).
-// Both stop at the first failure.
+// One K1 unit per block, warp w = stage s of chain group g (s = w mod P,
+// g = w div P, G = W div P groups): group g places chains k = g, g + G, ...
+// A wavefront over stages and a pipeline over chains: chain k of stage s
+// starts when chain k of stage s-1 has ended (shared-memory flags), and
+// reads a 32-interval block of a list only once chain k-1 has passed it
+// (its window left the block: the block's fill state and owner are final).
+// Chain k's kernels never start before chain k-1's (same ready times or
+// later, fill pointers only advance), so it trails chain k-1 and ends after
+// it.  Forward (M = false): successive chains on fresh instances; chain k
+// publishes version k+1 of each stage's fill state (the owner map, block by
+// block as it passes them; flags[k+1] counts the stages), and the unit ends
+// with flags[0] = 1.  Backward (M = true): mirrored chains on top of forward
+// version kf, started once it is published (or skipped when the forward
+// unit ended with fewer chains).  Both stop at the first failure; chains
+// after it are void (they quit at their next wait).
 template <bool M, bool REC = false>
 __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, int a, int kf, int klimit = 1 << 30,
                                         int64_t* rec = nullptr) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int stop_at;  // first chain index known to fail (chains >= it are void)
   __shared__ int go;
-  const int s = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PlanDesc pd = c.plans[e];
   const int P = pd.P, icap = c.icapc + c.icapm;
+  // chain groups: REC replays one chain after the other
+  const int G = REC ? 1 : max(1, min((int)(blockDim.x >> 5) / P, K1_GROUPS));
+  const int s = w % P, g = w / P;
   int* flags = c.k1flags + pd.flag_base + (int64_t)a * (pd.kmax + 1);
   OPT_CHECK(pd.flag_base + (int64_t)(a + 1) * (pd.kmax + 1) <= c.nflags && kf <= pd.kmax);
   if (M && kf > 0) {  // wait for forward version kf of this row
@@ -572,11 +746,13 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
     __syncthreads();
     if (!go) return;  // uniform: no pipeline of this row has kf forward chains
   }
-  const bool active = s < P;  // warps beyond this plan's P only join the barriers
+  const bool active = g < G;  // warps beyond G * P only join the barriers
   UnitSm U = carve(dsm, L.NK, L.Pmax, L.CI);
   const size_t ub = unit_smem_bytes(L.NK, L.Pmax, L.CI);
   volatile int* status = (volatile int*)(dsm + ub);  // [P][KM]: 0 pending, 1 done, 2 failed
-  volatile int64_t* endv = (volatile int64_t*)(dsm + ub + (((size_t)L.Pmax * L.KM * 4 + 15) & ~size_t(15)));
+  const size_t sb = (((size_t)L.Pmax * L.KM * 4 + 15) & ~size_t(15));
+  volatile int64_t* endv = (volatile int64_t*)(dsm + ub + sb);
+  volatile int* prog = (volatile int*)(dsm + ub + sb + (size_t)L.Pmax * L.KM * 8);  // [P][KM][2] blocks passed
   volatile int* stop = &stop_at;
   auto slot = [&](int k, int st) {
     OPT_CHECK(k >= 0 && k <= pd.kmax && st >= 0 && st < P);
@@ -584,14 +760,15 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
   };
 #ifdef K1_STATS
   const long long tk0 = clock64();
-  if (threadIdx.x < 32 * 8) k1st[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+  for (int i = threadIdx.x; i < 32 * 14; i += blockDim.x) k1st[i / 14][i % 14] = 0;
   __syncthreads();
 #endif
-  if (active) build_seq(c, pd, M, U, s);
+  if (active && g == 0) build_seq(c, pd, M, U, s);
   for (int i = threadIdx.x; i < P * L.KM; i += blockDim.x) status[i] = 0;
+  for (int i = threadIdx.x; i < 2 * P * L.KM; i += blockDim.x) prog[i] = 0;
   if (threadIdx.x == 0) stop_at = pd.kmax;
   int64_t* snap0 = c.snap + slot(0, 0) * icap;
-  if (active) {
+  if (active && g == 0) {
     for (int r = 0; r < 2; ++r) {
       // block owners: forward starts untouched; mirror loads snapshot kf's map
       int16_t* own = U.own + (2 * s + r) * U.CI;
@@ -614,10 +791,11 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
     const int64_t T_end = c.scal[1];
     const int q = a * P + s;
     const int64_t ws = M ? T_end - c.z[q] : c.w[q];
+    const int kend = min(pd.kmax, klimit);
     // every decision on a value another warp may change is taken from lane
     // 0's read (broadcast), so that the warp never splits before its
     // full-mask collectives
-    for (int k = 0; k < min(pd.kmax, klimit); ++k) {
+    for (int k = g; k < kend; k += G) {
       if (k >= __shfl_sync(FULL, *stop, 0)) break;
       int64_t ready = ws;
       if (s > 0) {  // wait for chain k of the upstream stage
@@ -635,11 +813,25 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
 #ifdef K1_STATS
         K1ST(5, clock64() - tw0);
 #endif
-        if (quit || st == 2) break;
+        if (quit || st == 2) {
+          if (lane == 0) {
+            atomicMin(&stop_at, k);
+            status[s * L.KM + k] = 2;
+          }
+          break;
+        }
+        __threadfence_block();
         ready = max(endv[(s - 1) * L.KM + k] + c.enc_p2p, ws);
       }
+      Link lk;
+      for (int r = 0; r < 2; ++r) {
+        lk.pprev[r] = (G > 1 && k > 0) ? prog + ((int64_t)s * L.KM + k - 1) * 2 + r : nullptr;
+        lk.pmine[r] = (G > 1 && k + 1 < kend) ? prog + ((int64_t)s * L.KM + k) * 2 + r : nullptr;
+        lk.gown[r] = (!M && !REC) ? c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n : nullptr;
+      }
+      lk.stopp = stop;
       int64_t end;
-      if (!place_stage<M, REC>(c, pd, X, U, s, k, ready, &end,
+      if (!place_stage<M, REC>(c, pd, X, U, s, k, ready, &end, lk,
                                REC ? rec + (int64_t)k * U.soff[P] * 4 : nullptr)) {
         if (lane == 0) {
           atomicMin(&stop_at, k);
@@ -657,23 +849,29 @@ __device__ __forceinline__ void k1_unit(const Cfg& c, const K1Launch& L, int e, 
         }
       }
       __syncwarp();
-      if (!M && !REC) {  // publish version k+1 of this stage: the block owner maps after chain k
-        for (int r = 0; r < 2; ++r) {
-          const int16_t* own = U.own + (2 * s + r) * U.CI;
-          int16_t* gown = c.snap_own + (slot(k + 1, s) * 2 + r) * c.ci_n;
-          for (int b = lane; b < U.CI; b += 32) gown[b] = own[b];
-        }
+      if (!M && !REC) {  // publish version k+1 of this stage (its owner map went out block by block)
+#ifdef K1_STATS
+        const long long tq0 = clock64();
+#endif
         __threadfence();  // this lane's block and map stores before the count
         __syncwarp();
         if (lane == 0) atomicAdd(&flags[k + 1], 1);
+#ifdef K1_STATS
+        K1ST(8, clock64() - tq0);
+#endif
       }
     }
   }
 #ifdef K1_STATS
   K1ST(6, clock64() - tk0);
-  if (active && lane == 0 && k1st[s][6] > 150000)
-    printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d prolog=%llu setup=%llu slow=%llu x=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
-           (int)M, e, a, kf, s, P, k1st[s][0], k1st[s][1], k1st[s][2], k1st[s][3], k1st[s][4], k1st[s][5], k1st[s][6], k1st[s][7]);
+#ifdef K1_TRACE
+  if (lane == 0 && k1item < 4096)
+    for (int q = 0; q < 14; ++q) g_k1stats[k1item][w][q] = k1st[w][q];
+#else
+  if (active && lane == 0 && k1st[w][6] > K1ST_MIN)
+    printf("K1ST M=%d e=%d a=%d kf=%d s=%d/%d g=%d/%d prolog=%llu setup=%llu slow=%llu x=%llu pcyc=%llu wcyc=%llu tot=%llu scyc=%llu\n",
+           (int)M, e, a, kf, s, P, g, G, k1st[w][0], k1st[w][1], k1st[w][2], k1st[w][3], k1st[w][4], k1st[w][5], k1st[w][6], k1st[w][7]);
+#endif
 #endif
   __syncthreads();
   if (REC) return;  // emission replay: the build's tables stay as they are
@@ -797,10 +995,25 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
     }
     const uint32_t u = (uint32_t)c.k1units[it];
     const int type = u >> 30, e = (u >> 16) & 0x3FFF, a = (u >> 8) & 255, kf = u & 255;
+#ifdef K1_TRACE
+    if (threadIdx.x == 0) k1item = it;
+    unsigned long long tt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt0));
+#endif
     if (type == 2) plan_tables(c, e);
     else if (type == 0) k1_unit<false>(c, L, e, a, 0);
     else k1_unit<true>(c, L, e, a, kf);
     __syncthreads();
+#ifdef K1_TRACE
+    if (threadIdx.x == 0 && it < 16384) {
+      unsigned long long tt1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt1));
+      g_k1trace[it][0] = tt0;
+      g_k1trace[it][1] = tt1;
+      g_k1trace[it][2] = u;
+      g_k1trace[it][3] = blockIdx.x;
+    }
+#endif
     if (threadIdx.x == 0) {
       __threadfence();
 #ifdef PDL_PROBE
@@ -829,8 +1042,11 @@ static void k1_attrs() {
 }
 
 #ifndef K1_MINB
-#define K1_MINB 2
+#define K1_MINB 1  // one K1 block per SM: the register cap of 2 blocks spilled the placement loop (K1 -25% without)
 #endif
+// K1 block: 12 warps up to p = 12 (every stage count P <= p gets 12 / P
+// chain groups), then 16 and 32
+__host__ __device__ inline int k1_threads(int p) { return p <= 12 ? 384 : (p <= 16 ? 512 : 1024); }
 #ifndef K1_PER_SM
 #define K1_PER_SM 1
 #endif
@@ -838,7 +1054,7 @@ static void k1_attrs() {
 template <int MAXT, int MINB>
 static int k1_grid_b(const Cfg& c, size_t smem) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, 32 * c.p, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, k1_threads(c.p), smem);
   // one block per SM (occupancy permitting) leaves room on every SM for K2
   // blocks, which start as soon as the first plans are complete
   return std::max(1, std::min(c.k1_total, std::max(1, std::min(per, K1_PER_SM)) * c.sms));
@@ -906,7 +1122,7 @@ cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
   if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;
   if (launches) *launches += 1;
   const int grid = c.k1_grid;
-  const int nt = 32 * c.p;
+  const int nt = k1_threads(c.p);
   if (c.p <= 12) k1_chains<384, K1_MINB><<<grid, nt, smem, st>>>(c, L);
   else if (c.p <= 16) k1_chains<512, 1><<<grid, nt, smem, st>>>(c, L);
   else k1_chains<1024, 1><<<grid, nt, smem, st>>>(c, L);
@@ -914,3 +1130,16 @@ cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
 }
 
 }  // namespace optimus
+
+#ifdef K1_TRACE
+extern "C" int optimus_debug_k1trace(void* out, int n) {
+  return (int)cudaMemcpyFromSymbol(out, optimus::g_k1trace, (size_t)n * 32);
+}
+extern "C" int optimus_debug_k1stats(void* out) {
+  return (int)cudaMemcpyFromSymbol(out, optimus::g_k1stats, sizeof(optimus::g_k1stats));
+}
+extern "C" int optimus_debug_k1reset() {
+  static unsigned long long z[16384][4];
+  return (int)cudaMemcpyToSymbol(optimus::g_k1trace, z, sizeof(z));
+}
+#endif
