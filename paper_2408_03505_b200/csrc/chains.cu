@@ -966,8 +966,7 @@ __global__ void k_eff(Cfg c, const int64_t* xo, unsigned long long* out) {
 // start at once (programmatic dependent launch): K2 takes a plan's
 // candidates once pdone says its tables are complete.
 // Block size 32 * p: register budgets per p range (MAXT threads, MINB blocks per SM).
-template <int MAXT, int MINB>
-__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
+__device__ __forceinline__ void k1_body(const Cfg& c, const K1Launch& L) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #ifdef PDL_PROBE  // development: K1 / K2 timeline (globaltimer ns) in the sync words
   unsigned long long* probe = reinterpret_cast<unsigned long long*>(c.k1next) + 1;
@@ -1031,19 +1030,26 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) {
 }
 
 template <int MAXT, int MINB>
-static void k1_attrs() {
-  cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+__global__ void __launch_bounds__(MAXT, MINB) k1_chains(Cfg c, K1Launch L) { k1_body(c, L); }
+
+#ifndef K1_MAXNREG
+#define K1_MAXNREG 112
+#endif
+// 12-warp blocks (p <= 12), one per SM: registers capped below the whole
+// file (164 uncapped, no spills at 112) so that K2 blocks fit beside the K1
+// block while both run
+__global__ void __maxnreg__(K1_MAXNREG) k1_chains12(Cfg c, K1Launch L) { k1_body(c, L); }
+
+template <typename F>
+static void k1_attrs(F f) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   // the whole unified L1 as shared memory: K2 blocks must fit next to the
   // K1 blocks while both run
 #ifndef K1_NO_CARVEOUT
-  cudaFuncSetAttribute(k1_chains<MAXT, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       cudaSharedmemCarveoutMaxShared);
+  cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
 #endif
 }
 
-#ifndef K1_MINB
-#define K1_MINB 1  // one K1 block per SM: the register cap of 2 blocks spilled the placement loop (K1 -25% without)
-#endif
 // K1 block: 12 warps up to p = 12 (every stage count P <= p gets 12 / P
 // chain groups), then 16 and 32
 __host__ __device__ inline int k1_threads(int p) { return p <= 12 ? 384 : (p <= 16 ? 512 : 1024); }
@@ -1051,10 +1057,10 @@ __host__ __device__ inline int k1_threads(int p) { return p <= 12 ? 384 : (p <= 
 #define K1_PER_SM 1
 #endif
 
-template <int MAXT, int MINB>
-static int k1_grid_b(const Cfg& c, size_t smem) {
+template <typename F>
+static int k1_grid_b(F f, const Cfg& c, size_t smem) {
   int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k1_chains<MAXT, MINB>, k1_threads(c.p), smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, k1_threads(c.p), smem);
   // one block per SM (occupancy permitting) leaves room on every SM for K2
   // blocks, which start as soon as the first plans are complete
   return std::max(1, std::min(c.k1_total, std::max(1, std::min(per, K1_PER_SM)) * c.sms));
@@ -1092,9 +1098,9 @@ cudaError_t launch_record(const Cfg& c, int e, int a, int kf, int klimit, int64_
 
 // large dynamic shared memory opt-in of every K1 variant (once per device, capi's device_info)
 void chains_attrs() {
-  k1_attrs<384, K1_MINB>();
-  k1_attrs<512, 1>();
-  k1_attrs<1024, 1>();
+  k1_attrs(k1_chains12);
+  k1_attrs(k1_chains<512, 1>);
+  k1_attrs(k1_chains<1024, 1>);
   cudaFuncSetAttribute(k1_record<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   cudaFuncSetAttribute(k1_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
 }
@@ -1111,9 +1117,9 @@ static K1Launch k1_launch_of(const Cfg& c) {
 // persistent K1 grid for this problem (computed once at load)
 int k1_grid(const Cfg& c) {
   const size_t smem = k1_smem_bytes(k1_launch_of(c));
-  if (c.p <= 12) return k1_grid_b<384, K1_MINB>(c, smem);
-  if (c.p <= 16) return k1_grid_b<512, 1>(c, smem);
-  return k1_grid_b<1024, 1>(c, smem);
+  if (c.p <= 12) return k1_grid_b(k1_chains12, c, smem);
+  if (c.p <= 16) return k1_grid_b(k1_chains<512, 1>, c, smem);
+  return k1_grid_b(k1_chains<1024, 1>, c, smem);
 }
 
 cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
@@ -1123,7 +1129,7 @@ cudaError_t launch_chain_tables(const Cfg& c, cudaStream_t st, int* launches) {
   if (launches) *launches += 1;
   const int grid = c.k1_grid;
   const int nt = k1_threads(c.p);
-  if (c.p <= 12) k1_chains<384, K1_MINB><<<grid, nt, smem, st>>>(c, L);
+  if (c.p <= 12) k1_chains12<<<grid, nt, smem, st>>>(c, L);
   else if (c.p <= 16) k1_chains<512, 1><<<grid, nt, smem, st>>>(c, L);
   else k1_chains<1024, 1><<<grid, nt, smem, st>>>(c, L);
   return cudaGetLastError();
