@@ -66,7 +66,7 @@ __host__ __device__ __forceinline__ int k0_sim_warps(int p, int v, int n) {
 // op at position pos of stage s under warm-up count Ws (R2): its endv slot,
 // dependency slot and whether the dependency is on another stage
 __device__ __forceinline__ void op_slots(int p, int v, int n, int s, int pos, int Ws, const short* vch,
-                                         const short* vmb, int& self, int& dep, int& fwd, int& cross) {
+                                         const short* vmb, int& self, int& dep, int& fwd, int& cross, int& dstage) {
   const int nv = n * v, r = pos - Ws;
   int k;
   if (r < 0) { k = pos; fwd = 1; }
@@ -85,6 +85,7 @@ __device__ __forceinline__ void op_slots(int p, int v, int n, int s, int pos, in
   self = ((s * 2 + fwd) * v + ch) * n + mb;
   dep = ds < 0 ? (int)kNone : ((ds * 2 + df) * v + dc) * n + mb;
   cross = ds >= 0 && ds != s;
+  dstage = ds;
 }
 
 __device__ void build_vtab(const Cfg& c) {
@@ -120,12 +121,17 @@ __device__ int64_t warp_simulate(const Cfg& c, const int* W, int64_t* endv_, uin
   const int s = lane;
   // op tables, built by the whole warp: self slot | dep slot << 15 (0x7FFF
   // none) | fwd << 30 | cross << 31 (padded slots)
-  for (int idx = lane; idx < p * nops; idx += 32) {
-    const int st = idx / nops, pos = idx - st * nops;
-    int self, dep, fwd, cross;
-    op_slots(p, v, n, st, pos, W[st], vch, vmb, self, dep, fwd, cross);
-    const int ps = self + self / S, pd = dep == kNone ? 0x7FFF : dep + dep / S;
-    optab[(size_t)st * (nops + 1) + pos] = (uint32_t)ps | (uint32_t)pd << 15 | (uint32_t)fwd << 30 | (uint32_t)cross << 31;
+  // (no integer division: slot / S is the slot's stage, so the padded slot
+  // of stage t's slot x is x + t; the op tables used to spend most of a
+  // simulation's time in divisions)
+  for (int st = 0; st < p; ++st) {
+    const int Ws = W[st];
+    for (int pos = lane; pos < nops; pos += 32) {
+      int self, dep, fwd, cross, ds;
+      op_slots(p, v, n, st, pos, Ws, vch, vmb, self, dep, fwd, cross, ds);
+      const int ps = self + st, pd = dep == kNone ? 0x7FFF : dep + ds;
+      optab[(size_t)st * (nops + 1) + pos] = (uint32_t)ps | (uint32_t)pd << 15 | (uint32_t)fwd << 30 | (uint32_t)cross << 31;
+    }
   }
   const uint32_t* tab = optab + (size_t)s * (nops + 1);
   __syncwarp();
@@ -214,8 +220,16 @@ __device__ __forceinline__ void dur_fb(const Cfg& c, int64_t& f, int64_t& b) {
 // assuming the later stages take their guessed value; the trial with every
 // stage at its guess records its schedule (it is the final one when K0b
 // verifies every guess).  res[b] = span, or -1 if the schedule deadlocks.
+#ifdef K0_CYC
+__device__ long long g_k0cyc[1024][4];
+#endif
 __global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int wpb) {
   const int p = c.p, v = c.v, n = c.n, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef K0_CYC
+  const long long tc0 = clock64();
+  long long tg0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg0));
+#endif
   build_vtab(c);
   const int b = blockIdx.x * wpb + warp;
   if (warp >= wpb || b >= nsim) return;
@@ -243,7 +257,20 @@ __global__ void __launch_bounds__(32 * kSimWarps) k0_wave(Cfg c, int nsim, int w
 #ifdef K0_STATS
   const long long t0 = clock64();
 #endif
+#ifdef K0_CYC
+  const long long tc1 = clock64();
+#endif
   const int64_t sp = warp_simulate(c, Wsm, endv, optab, record, df, db, INT64_MAX, b > 0 && !record);
+#ifdef K0_CYC
+  if (lane == 0 && b < 1024) {
+    long long tg1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tg1));
+    g_k0cyc[b][0] = tc1 - tc0;
+    g_k0cyc[b][1] = clock64() - tc1;
+    g_k0cyc[b][2] = tg0;
+    g_k0cyc[b][3] = tg1;
+  }
+#endif
 #ifdef K0_STATS
   if (lane == 0) printf("K0ST b=%d s=%d w=%d sp=%lld cyc=%lld blk=%d\n", b, s, w, (long long)sp, clock64() - t0, blockIdx.x);
 #endif
@@ -589,3 +616,9 @@ cudaError_t launch_template(const Cfg& c, cudaStream_t st, int* launches) {
 }
 
 }  // namespace optimus
+
+#ifdef K0_CYC
+extern "C" int optimus_debug_k0cyc(void* out) {
+  return (int)cudaMemcpyFromSymbol(out, optimus::g_k0cyc, sizeof(optimus::g_k0cyc));
+}
+#endif
