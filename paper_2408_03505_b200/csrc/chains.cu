@@ -335,7 +335,7 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
   win_sync_cur(w);
   for (;;) {
     const int blk = w.base >> 5;
-    if (ci[blk] > ready && bm[blk] >= d) {  // else no interval of the window can take it
+    {  // the window first (registers; the block indices only filter)
       const int64_t x = max(ready, w.lo);
       const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
       if (b) {
