@@ -337,7 +337,7 @@ __device__ __forceinline__ bool place_slow(VR<M>& V, Win& w, int64_t d, int64_t&
     const int blk = w.base >> 5;
     {  // the window first (registers; the block indices only filter)
       const int64_t x = max(ready, w.lo);
-      const unsigned b = __ballot_sync(FULL, w.hi > ready && x + d <= w.hi);
+      const unsigned b = __ballot_sync(FULL, x + d <= w.hi);  // (d >= 1: such an end is after ready)
       if (b) {
 #ifdef K1_STATS
         K1ST(12, 1);
@@ -582,6 +582,7 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
     // slow placement the next kernels often leave the current intervals
     // within a few steps, where a 32-wide batch would mostly be wasted
     bool fits = true;
+    int64_t vmiss = 0;  // the kernel the scalar steps could not place (fits == false)
 #pragma unroll 1
     for (int ns = 0; ns < K1_SCALAR && i < i1; ++ns) {
       const int64_t v = seq[i];
@@ -590,6 +591,7 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
       const int64_t e = max(ready, comm ? w1.clo : w0.clo) + d;
       if (e > (comm ? w1.chi : w0.chi)) {
         fits = false;
+        vmiss = v;
         break;
       }
       if (REC && (threadIdx.x & 31) == 0) {
@@ -644,7 +646,7 @@ __device__ bool place_stage(const Cfg& c, const PlanDesc& pd, const UnitCtx& X, 
       if (f < nv) break;
     }
     if (i >= i1) break;
-    const int64_t v = seq[i];
+    const int64_t v = fits ? seq[i] : vmiss;
     K1ST(2, 1);
 #ifdef K1_STATS
     const long long ts0 = clock64();
