@@ -301,9 +301,12 @@ __device__ __forceinline__ void win_flush(VR<M>& V, Win& w) {
   const int i = w.base + lane;
   OPT_CHECK(M || (V.ver >= 0 && V.ver <= 32767));
   if (i < V.count) (M ? V.fill : V.snap0 + V.ver * V.vstride)[i] = w.lo;  // forward: the whole block
-  const int64_t cap = warp_max64(i < V.count ? w.hi - w.lo : kNegInf);
+  // the block's largest capacity, an upper bound for the skip test: one
+  // 32-bit redux over capacities saturated at 2^32 - 1 (read back as +inf)
+  const int64_t c64 = i < V.count ? w.hi - w.lo : 0;
+  const unsigned c32 = __reduce_max_sync(FULL, c64 >= 0xFFFFFFFFll ? 0xFFFFFFFFu : (unsigned)max(c64, (int64_t)0));
   if (lane == 0) {
-    V.bm[w.base >> 5] = cap;
+    V.bm[w.base >> 5] = c32 == 0xFFFFFFFFu ? kInf : (int64_t)c32;
     if (M) atomicOr(&V.wm[w.base >> 10], 1u << ((w.base >> 5) & 31));  // chains in flight share the word
     else V.own[w.base >> 5] = (int16_t)V.ver;
   }
