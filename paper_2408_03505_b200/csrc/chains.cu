@@ -39,7 +39,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define K1_SCALAR 4  // kernels placed one by one before a 32-wide batch is tried
 #endif
 #ifndef K1_GROUPS
-#define K1_GROUPS 32  // most chains of one unit in flight (1: one chain after the other)
+#define K1_GROUPS 2  // most chains of one unit in flight (1: one chain after the other; config 2 build: 1 -> 0.99 ms, 2 -> 0.70, 4 -> 0.71, 12 -> 0.72)
 #endif
 
 #ifdef K1_TRACE  // development instrumentation: per K1 work item start / end (globaltimer ns), item, block
