@@ -181,7 +181,10 @@ struct EvalArgs {
   int grid2;
   int first_chunk;            // 1: blocks write their partials, 0: merge into them
 };
-constexpr int kGqBatch = 64;    // queue slots a fast-kernel warp reserves at a time
+#ifndef K2_GQBATCH
+#define K2_GQBATCH 32  // >= 32 (one step of a warp); 64 measured 1% / 4% slower on 1 / 4 ranks (more half-used batches)
+#endif
+constexpr int kGqBatch = K2_GQBATCH;  // queue slots a fast-kernel warp reserves at a time
 cudaError_t launch_eval(const Cfg& c, const EvalArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_eval_thread(const Cfg& c, const EvalArgs& a, cudaStream_t st);
 cudaError_t launch_explain(const Cfg& c, uint64_t g, int64_t* d_out, cudaStream_t st);
