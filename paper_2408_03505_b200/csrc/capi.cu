@@ -267,17 +267,22 @@ int prepare(const optimus_problem* pb, Prep& X) {
   std::stable_sort(X.k2order.begin(), X.k2order.end(),
                    [&](int32_t x, int32_t y) { return X.plans[x].d.P > X.plans[y].d.P; });
   // K1 work list: every forward unit first (all start at once; a backward
-  // unit only waits on forward units already taken), then plan by plan in
-  // K2's order its tables and backward units by kf, so that plans complete
-  // one after the other while K2 already evaluates the finished ones
+  // unit only waits on forward units already taken), then every plan's
+  // tables, then the backward units
   for (int32_t e : X.k2order)
     for (int a = 0; a < X.plans[e].d.rp; ++a) X.units.push_back((int32_t)(e << 16 | a << 8));
-  for (int32_t e : X.k2order) {
-    const PlanDesc& d = X.plans[e].d;
-    X.units.push_back((int32_t)(2u << 30 | e << 16));
-    for (int kf = 0; kf <= d.kmax; ++kf)
+  // backward units by kf across the plans (kf-major): a unit comes after
+  // every unit of a smaller kf, so it is usually taken once its version is
+  // published, and the units of the long forward chains (the plans with the
+  // largest kmax) come last (config 4's build 0.253 -> 0.221 ms against
+  // plan by plan)
+  for (int32_t e : X.k2order) X.units.push_back((int32_t)(2u << 30 | e << 16));
+  for (int kf = 0; kf <= X.kmax_all; ++kf)
+    for (int32_t e : X.k2order) {
+      const PlanDesc& d = X.plans[e].d;
+      if (kf > d.kmax) continue;
       for (int a = 0; a < d.rp; ++a) X.units.push_back((int32_t)(1u << 30 | e << 16 | a << 8 | kf));
-  }
+    }
   X.n_flags = std::max<int64_t>(X.n_flags, 1);
   X.n_tables = std::max<int64_t>(toff, 1);
   X.n_slots = std::max<int64_t>(slot, 1);
